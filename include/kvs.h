@@ -1,0 +1,214 @@
+/* kvs.h — C ABI over the per-node tiered KV store (symsim::KvStore).
+ *
+ * The reference exposes its store only as a C++ class
+ * (/root/reference/proj/include/symsim/kvstore.hpp:107-229); it has no FFI.
+ * This flat C surface is what a non-C++ host (ctypes, cgo, JNI) binds, and it
+ * is compiled twice from one source file (paper_2412_16434_b200/csrc/host/
+ * kvs_capi.cpp): into the product library against this repo's KvStore, and
+ * into the oracle library (oracle/_ref) against the reference KvStore. The two
+ * libraries therefore export byte-identical entry points, which is what the
+ * state-parity tests drive side by side.
+ *
+ * Conventions: every call returns 0 on success or a KVS_ERR_* code; the
+ * message of the C++ exception that produced it is kvs_last_error() (thread
+ * local). Variable-length results (scheduled transfers, created keys,
+ * per-layer plan times, eviction candidates) are left in per-store output
+ * buffers read through kvs_out_*(); they stay valid until the next call on the
+ * same store. Times are int64 nanoseconds, sizes int64 bytes.
+ */
+#ifndef KVS_H_
+#define KVS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVS_OK 0
+#define KVS_ERR_LOGIC 1       /* std::logic_error: contract violation       */
+#define KVS_ERR_RUNTIME 2     /* std::runtime_error: resource/config error  */
+#define KVS_ERR_OTHER 3       /* any other exception                        */
+#define KVS_ERR_UNSUPPORTED 4 /* entry point not available in this build    */
+
+typedef struct kvs_store kvs_store;
+
+typedef struct {
+  double prefill_throughput;
+  double decode_base_ms;
+  double decode_half_batch;
+  int64_t hbm_capacity;
+  int64_t kv_bytes_per_token;
+  int32_t num_layers;
+  int32_t curve_points; /* number of (batch, ms) pairs in curve_batch/curve_ms */
+  const int32_t* curve_batch;
+  const double* curve_ms;
+} kvs_gpu_profile; /* reference costmodel.hpp:17-27 */
+
+typedef struct {
+  double pcie_bandwidth;
+  double disk_bandwidth;
+  double network_bandwidth;
+  int64_t per_transfer_latency;
+} kvs_link_profile; /* reference costmodel.hpp:29-36 */
+
+typedef struct {
+  int32_t node_id;
+  int32_t block_tokens;
+  int64_t device_capacity;
+  int64_t host_capacity;
+  int64_t disk_capacity;
+  int32_t write_behind;
+} kvs_options; /* reference kvstore.hpp:109-116 */
+
+typedef struct {
+  uint64_t id;
+  int64_t complete_at;
+} kvs_scheduled; /* ScheduledTransfer, kvstore.hpp:70-73 */
+
+typedef struct {
+  uint32_t session;
+  uint16_t layer;
+  uint16_t pad_;
+  uint32_t block_index;
+} kvs_block_key; /* BlockKey, kvstore.hpp:24-28 */
+
+typedef struct {
+  int64_t time;
+  int32_t node;
+  uint32_t session;
+  uint16_t layer_lo;
+  uint16_t layer_hi;
+  int32_t from; /* Tier: 0 device, 1 host, 2 disk */
+  int32_t to;
+  int32_t reason; /* TransferReason: prefetch, demand, purge, persist, migrate */
+  int64_t bytes;
+} kvs_record; /* TransferRecord, kvstore.hpp:47-57 */
+
+typedef struct {
+  uint32_t session;
+  uint16_t layer;
+  uint8_t device_layer_ready;
+  uint8_t persists_drained;
+  uint8_t migration_arrived;
+  uint8_t migration_complete;
+  uint8_t voided;
+  uint8_t pad_;
+} kvs_apply_result; /* KvStore::ApplyResult, kvstore.hpp:204-212 */
+
+typedef struct {
+  int32_t has_plan; /* 0 when the store declined (std::nullopt) */
+  int32_t any_load;
+  int64_t decode_start;
+  int64_t finish;
+  int64_t total_stall;
+} kvs_load_plan; /* LoadPlan, kvstore.hpp:77-83; layer_ready via kvs_out_times */
+
+typedef struct {
+  int32_t device_layers;
+  int32_t staged_layers;
+  int32_t scheduled;
+} kvs_promote_result; /* PromoteResult, kvstore.hpp:98-102 */
+
+typedef struct {
+  int64_t first_step_end;
+  int64_t gate_start;
+  int64_t stall;
+} kvs_gate_result; /* GateResult, kvstore.hpp:85-89 */
+
+typedef struct {
+  int64_t device_capacity;
+  int64_t device_used;
+  int64_t device_free;
+  int64_t host_used;
+  int64_t disk_used;
+  int64_t layer_block_bytes;
+} kvs_counters;
+
+typedef struct {
+  int64_t cached_tokens;
+  int64_t session_bytes;
+  int32_t fully_device_resident;
+  int32_t has_any_copy;
+  int32_t pending_persists;
+  int32_t migrating_out;
+  int32_t is_active;
+  int32_t pad_;
+} kvs_session_info;
+
+typedef struct {
+  kvs_block_key key;
+  int64_t session_bytes;
+  const char* session_id; /* evict_order input; output points into the store */
+  int32_t pinned;
+  int32_t pad_;
+} kvs_block_meta; /* BlockMeta, kvstore.hpp:32-37 */
+
+const char* kvs_last_error(void);
+/* 1 for the product build, 0 for the oracle build of the same source. */
+int kvs_is_product(void);
+
+int kvs_create(const kvs_gpu_profile* gpu, const kvs_link_profile* links, const kvs_options* opts,
+               kvs_store** out);
+void kvs_destroy(kvs_store* s);
+
+int kvs_register_session(kvs_store* s, uint32_t session, const char* id, int32_t priority);
+int kvs_finalize_sessions(kvs_store* s);
+
+int kvs_get_counters(kvs_store* s, kvs_counters* out);
+int kvs_get_session(kvs_store* s, uint32_t session, kvs_session_info* out);
+int kvs_bytes_for_new_blocks(kvs_store* s, uint32_t session, int64_t new_tokens, int64_t* out);
+int kvs_bytes_for_load(kvs_store* s, uint32_t session, int64_t* out);
+int kvs_bytes_for_promote(kvs_store* s, uint32_t session, int64_t* out);
+int kvs_reserve_device(kvs_store* s, int64_t bytes);
+int kvs_unreserve_device(kvs_store* s, int64_t bytes);
+int kvs_set_active(kvs_store* s, uint32_t session, int32_t active, int64_t now);
+
+/* Scheduled transfers -> kvs_out_scheduled; created keys -> kvs_out_keys. */
+int kvs_append_blocks(kvs_store* s, uint32_t session, int64_t new_tokens, int64_t now);
+int kvs_purge_from_device(kvs_store* s, int64_t bytes_needed, int64_t now, int32_t spare_high_priority,
+                          int64_t* freed);
+/* layer_ready -> kvs_out_times. */
+int kvs_plan_layerwise_load(kvs_store* s, uint32_t session, int64_t now, int64_t compute_per_layer,
+                            int32_t reason, kvs_load_plan* out);
+int kvs_promote(kvs_store* s, uint32_t session, int64_t now, kvs_promote_result* out);
+int kvs_offload_session(kvs_store* s, uint32_t session, int64_t now);
+int kvs_release_session(kvs_store* s, uint32_t session, int64_t now);
+int kvs_mark_migrating_out(kvs_store* s, uint32_t session);
+int kvs_import_migration(kvs_store* s, uint32_t session, int64_t tokens, int64_t now);
+int kvs_apply_transfer(kvs_store* s, uint64_t id, int64_t now, kvs_apply_result* out);
+int kvs_void_session_loads(kvs_store* s, uint32_t session);
+int kvs_void_session_offload(kvs_store* s, uint32_t session);
+/* Candidates in eviction order -> kvs_out_metas. */
+int kvs_evictable_blocks(kvs_store* s, int32_t spare_high_priority);
+int kvs_check_budgets(kvs_store* s);
+int kvs_device_usage_debug(kvs_store* s, char* buf, size_t cap);
+
+size_t kvs_ledger_size(kvs_store* s);
+int kvs_ledger_copy(kvs_store* s, size_t start, size_t count, kvs_record* out);
+
+size_t kvs_out_scheduled(kvs_store* s, const kvs_scheduled** out);
+size_t kvs_out_keys(kvs_store* s, const kvs_block_key** out);
+size_t kvs_out_times(kvs_store* s, const int64_t** out);
+size_t kvs_out_metas(kvs_store* s, const kvs_block_meta** out);
+
+/* Free functions of the reference API. evict_order writes the permutation of
+ * the input indices into `order` (n entries). */
+int kvs_evict_order(const kvs_block_meta* candidates, size_t n, uint32_t* order);
+int kvs_pipeline_gate(const int64_t* layer_ready, size_t n, int64_t compute_ready, int64_t step_ns,
+                      kvs_gate_result* out);
+int kvs_transfer_time(int64_t bytes, int32_t link, const kvs_link_profile* links, int64_t* out);
+int kvs_decode_step_time(int32_t batch, const kvs_gpu_profile* gpu, int64_t* out);
+int kvs_prefill_time(int64_t tokens, const kvs_gpu_profile* gpu, int64_t* out);
+int kvs_kv_bytes_per_layer(int64_t tokens, const kvs_gpu_profile* gpu, int64_t* out);
+
+/* Product-only (KVS_ERR_UNSUPPORTED in the oracle build): residency bits
+ * (1 << Tier) of one block. */
+int kvs_residency(kvs_store* s, uint32_t session, uint16_t layer, uint32_t block, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVS_H_ */

@@ -1,0 +1,150 @@
+/* kvx.h — C ABI of the B200 KV payload path (sm_100a kernels).
+ *
+ * The reference stores no KV bytes ("bytes are accounted,
+ * not stored"); its per-(session, layer, block) accounting unit is
+ * layer_block_bytes = kv_bytes_per_layer(block_tokens)
+ * (/root/reference/proj/src/kvstore.cpp:67, costmodel.cpp:48-52). This ABI
+ * gives each such block a physical PAGE of exactly that many bytes and moves
+ * pages with hand-written kernels. Each entry point replaces a modelled
+ * transfer of the reference:
+ *
+ *   kvx_pack        K1  DEVICE pages -> contiguous buffer (one layer's block
+ *                       range): the D2H side of HostCopy/SwapOut
+ *                       (kvstore.cpp:230-269, 691-706) and the send side of a
+ *                       migration (import_migration, kvstore.cpp:753-769)
+ *   kvx_unpack      K2  contiguous -> DEVICE pages: LoadH2D landing of
+ *                       plan_layerwise_load/promote (kvstore.cpp:522-533,
+ *                       599-611) and NetArrive landing (kvstore.cpp:914-923)
+ *   kvx_copy_pages  K3  page -> page between any two pools (local HBM, a peer
+ *                       GPU's pool over NVLink, mapped pinned host memory):
+ *                       the fused pack+send+unpack of one migration layer
+ *   kvx_fill_pages  K5  deterministic synthetic page contents (tests/bench)
+ *   kvx_append_kv   K5  write one token's K/V into its page slot
+ *                       (the bytes behind append_blocks, kvstore.cpp:202-271)
+ *   kvx_decode_attention  K4  paged decode attention over block tables;
+ *                       replaces the modelled decode step
+ *                       (costmodel.cpp:59-80, engine.cpp:256-257)
+ *
+ * Conventions: plain pointers and sizes, no torch types; every call returns
+ * KVX_OK (0) or a KVX_ERR_* code, message in kvx_last_error() (thread
+ * local); kernels are launched asynchronously on the caller's stream
+ * (`stream` is a cudaStream_t passed as void*, NULL = legacy default stream).
+ * There is no CPU fallback: without a CUDA device every launching call fails
+ * with KVX_ERR_CUDA.
+ *
+ * Page layout (for fill/append/attention; pack/unpack/copy treat pages as
+ * opaque bytes): page = [2 (K, V)][num_kv_heads][block_tokens][head_dim]
+ * elements of `dtype`, so one kv head's K (or V) for the page's tokens is one
+ * contiguous block_tokens*head_dim run.
+ */
+#ifndef KVX_H_
+#define KVX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVX_OK 0
+#define KVX_ERR_CUDA 1        /* CUDA runtime/driver error or no device */
+#define KVX_ERR_ARG 2         /* invalid argument                       */
+#define KVX_ERR_UNSUPPORTED 3 /* shape/dtype/mode not implemented       */
+
+#define KVX_DTYPE_F32 0
+#define KVX_DTYPE_BF16 1
+
+#define KVX_FILL_BITS 0   /* page = splitmix64 words                       */
+#define KVX_FILL_VALUES 1 /* page = dtype values uniform on [-sqrt3,sqrt3) */
+
+#define KVX_COPY_AUTO 0   /* library picks (currently KVX_COPY_SM)            */
+#define KVX_COPY_SM 1     /* SM kernel, 16-B vector loads/stores             */
+#define KVX_COPY_TMA 2    /* SM kernel, cp.async.bulk (TMA) through smem     */
+#define KVX_COPY_CE 3     /* copy engines (cudaMemcpyBatchAsync); host ids   */
+
+typedef struct kvx_pool kvx_pool;
+
+typedef struct {
+  int32_t num_kv_heads;
+  int32_t head_dim;
+  int32_t block_tokens;
+  int32_t dtype; /* KVX_DTYPE_* */
+} kvx_page_layout;
+
+typedef struct {
+  uint32_t session;
+  uint32_t layer;
+  uint32_t block;
+} kvx_block_tag; /* logical BlockKey a page holds (kvstore.hpp:24-28) */
+
+typedef struct {
+  int32_t num_q_heads; /* multiple of num_kv_heads (GQA group g = Hq / H) */
+  int32_t max_blocks;  /* row stride of the block table                  */
+  int32_t num_splits;  /* split-K over context; 0 = auto                  */
+  float scale;         /* softmax scale; 0 = 1/sqrt(head_dim)             */
+} kvx_attn_params;
+
+const char* kvx_last_error(void);
+int kvx_version(void);
+/* Bytes of one page for `layout` (2 * H * T * D * sizeof(dtype)). */
+uint64_t kvx_page_bytes(const kvx_page_layout* layout);
+
+/* ---- pools --------------------------------------------------------------- */
+/* DEVICE pool in HBM of `device` (pages 256-B aligned). */
+int kvx_pool_create(int device, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
+/* HOST pool: pinned, device-mapped host memory (HOST-tier payload). */
+int kvx_pool_create_host(uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
+/* Wraps caller-owned device memory (not freed by kvx_pool_destroy). */
+int kvx_pool_wrap(int device, void* base, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
+int kvx_pool_destroy(kvx_pool* pool);
+void* kvx_pool_base(const kvx_pool* pool);
+uint64_t kvx_pool_num_pages(const kvx_pool* pool);
+uint64_t kvx_pool_page_bytes(const kvx_pool* pool);
+int kvx_pool_device(const kvx_pool* pool); /* -1 for a host pool */
+/* CUDA IPC: export a DEVICE pool (64-byte handle) / open a peer's pool in
+ * this process so kernels here can store into it over NVLink. */
+int kvx_pool_ipc_export(const kvx_pool* pool, void* handle64);
+int kvx_pool_ipc_open(int device, const void* handle64, uint64_t num_pages, uint64_t page_bytes,
+                      kvx_pool** out);
+int kvx_enable_peer_access(int device, int peer);
+
+/* ---- page movement (K1-K3) ---------------------------------------------- */
+/* dst[i * page_bytes ...] = page(ids[i]) for i < n. ids in device memory. */
+int kvx_pack(const kvx_pool* src, const uint32_t* d_page_ids, uint64_t n, void* d_dst, int mode,
+             void* stream);
+/* page(ids[i]) = src[i * page_bytes ...]. */
+int kvx_unpack(kvx_pool* dst, const uint32_t* d_page_ids, uint64_t n, const void* d_src, int mode,
+               void* stream);
+/* dst page(dst_ids[i]) = src page(src_ids[i]); pools may live on different
+ * GPUs (peer access / IPC), or one may be a host pool. Both pools must have
+ * the same page_bytes. ids are device pointers except for KVX_COPY_CE, which
+ * takes host arrays. */
+int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
+                   uint64_t n, int mode, void* stream);
+
+/* ---- contents (K5) ------------------------------------------------------ */
+int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,
+                   uint64_t seed, const kvx_page_layout* layout, int fill_mode, void* stream);
+/* For request i: page d_page_ids[i], token slot d_slots[i] (< block_tokens)
+ * gets K = d_k[i][H][D], V = d_v[i][H][D] (layout dtype). */
+int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_page_ids,
+                  const int32_t* d_slots, const void* d_k, const void* d_v, uint64_t n, void* stream);
+
+/* ---- paged decode attention (K4) ----------------------------------------- */
+/* out[b][hq][d] (fp32) = softmax(scale * q[b][hq] . K^T) V over the first
+ * ctx_lens[b] tokens of request b, whose block table row is
+ * d_block_tables[b * max_blocks ...]. q has the layout dtype. Workspace of
+ * kvx_decode_attention_workspace() bytes (may be 0 -> NULL allowed). */
+uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx_attn_params* params,
+                                        int32_t batch, int32_t max_ctx);
+int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
+                         const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q,
+                         float* d_out, int32_t batch, int32_t max_ctx, void* d_workspace,
+                         uint64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVX_H_ */

@@ -1,0 +1,454 @@
+// K4: paged decode attention over the KV page pool — sm_100a.
+//
+// Replaces the reference's modelled decode step (decode_step_time,
+// /root/reference/proj/src/costmodel.cpp:59-80, consumed by
+// Engine::try_start, engine.cpp:256-257) with the real computation over the
+// pages the store holds: out[b][hq] = softmax(scale * q . K^T) V over the
+// first ctx_len[b] tokens of request b.
+//
+// Roofline: every K/V byte is read once; work per byte is g (GQA group)
+// multiply-adds for QK plus g for PV, i.e. 2g flop/B — 8 flop/B at g=4,
+// ~30x below the bf16 tensor ridge — so the kernel is HBM-bound and is built
+// to stream pages: per warp a private 3-stage cp.async ring (8 KiB = one
+// page's K+V of one kv head per stage, XOR-swizzled rows so ldmatrix is
+// bank-conflict free), split-K over the context so batch 1 still fills 148
+// SMs, and a log-sum-exp combine. The GQA group's QK^T and PV tiles
+// (g x 16 tokens x 128) are real dense contractions, so they go to the
+// tensor cores with mma.sync m16n8k16 (query heads on M, padded to 16;
+// tokens on N for QK, on K for PV). tcgen05/TMEM would buy nothing here:
+// the tensor pipe is idle >95% of the time even with mma.sync.
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+
+#include "kvx_common.cuh"
+
+namespace kvx {
+namespace {
+
+constexpr int kD = 128;          // head_dim of the fast path
+constexpr int kT = 16;           // block_tokens of the fast path
+constexpr int kWarps = 4;        // warps per CTA, each streams its own pages
+constexpr int kStages = 3;       // cp.async ring depth per warp
+constexpr int kTileBytes = kT * kD * 2;  // one kv head's K (or V) in a page: 4 KiB
+constexpr int kStageBytes = 2 * kTileBytes;
+constexpr int kSmemBytes = kWarps * kStages * kStageBytes;  // 96 KiB
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+// D[16x8] += A[16x16] * B[16x8], bf16 in, fp32 accumulate.
+__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Byte offset of 16-B chunk `col16` (0..15) of tile row `row` (0..15): rows
+// are 256 B; chunks are XOR-swizzled within each 128-B half by (row & 7).
+__device__ __forceinline__ uint32_t swz(int row, int col16) {
+  return static_cast<uint32_t>(row * 256 + ((col16 ^ (row & 7)) << 4));
+}
+
+struct AttnArgs {
+  const uint8_t* pool;
+  uint64_t page_bytes;
+  const uint32_t* tables;
+  const int32_t* ctx_lens;
+  const uint16_t* q;  // [B][Hq][128] bf16
+  float* out;         // [B][Hq][128]
+  float* part_o;      // [B][Hq][S][128]
+  float* part_ml;     // [B][Hq][S][2]
+  int heads;          // kv heads
+  int group;          // q heads per kv head
+  int max_blocks;
+  int splits;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int ctx = a.ctx_lens[b];
+  const int n_pages = (ctx + kT - 1) / kT;
+  const int per_split = (n_pages + a.splits - 1) / a.splits;
+  const int p_begin = split * per_split;
+  const int p_end = min(n_pages, p_begin + per_split);
+  const uint32_t* table = a.tables + static_cast<uint64_t>(b) * a.max_blocks;
+  const int hq0 = h * a.group;
+
+  // Q as mma A fragments (rows = the group's query heads, zero-padded to 16).
+  uint32_t qa[kD / 16][4];
+  {
+    const int r0 = lane >> 2, c = (lane & 3) * 2;
+    const uint16_t* q0 = a.q + (static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r0) * kD;
+    const uint16_t* q8 = q0 + 8 * kD;
+    const bool v0 = r0 < a.group, v8 = r0 + 8 < a.group;
+#pragma unroll
+    for (int kk = 0; kk < kD / 16; ++kk) {
+      qa[kk][0] = v0 ? *reinterpret_cast<const uint32_t*>(q0 + kk * 16 + c) : 0u;
+      qa[kk][1] = v8 ? *reinterpret_cast<const uint32_t*>(q8 + kk * 16 + c) : 0u;
+      qa[kk][2] = v0 ? *reinterpret_cast<const uint32_t*>(q0 + kk * 16 + c + 8) : 0u;
+      qa[kk][3] = v8 ? *reinterpret_cast<const uint32_t*>(q8 + kk * 16 + c + 8) : 0u;
+    }
+  }
+
+  float o[kD / 8][4];
+#pragma unroll
+  for (int i = 0; i < kD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r = -INFINITY, m_r8 = -INFINITY, l_r = 0.f, l_r8 = 0.f;
+
+  uint8_t* ring = smem + warp * (kStages * kStageBytes);
+  const uint32_t ring_s = smem_u32(ring);
+  // This warp's pages: p_begin + warp, + kWarps, ...
+  const int my_first = p_begin + warp;
+  const int my_count = my_first < p_end ? (p_end - my_first + kWarps - 1) / kWarps : 0;
+
+  auto issue = [&](int i) {  // page i of this warp -> stage i % kStages
+    if (i < my_count) {
+      const int p = my_first + i * kWarps;
+      const uint8_t* page = a.pool + static_cast<uint64_t>(__ldg(table + p)) * a.page_bytes;
+      const uint8_t* k_src = page + static_cast<uint64_t>(h) * kTileBytes;
+      const uint8_t* v_src = page + static_cast<uint64_t>(a.heads + h) * kTileBytes;
+      uint8_t* st = ring + (i % kStages) * kStageBytes;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = lane + 32 * j, row = c >> 4, col = c & 15;
+        cp_async16(st + swz(row, col), k_src + c * 16);
+        cp_async16(st + kTileBytes + swz(row, col), v_src + c * 16);
+      }
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int i = 0; i < kStages - 1; ++i) issue(i);
+
+  for (int i = 0; i < my_count; ++i) {
+    issue(i + kStages - 1);
+    cp_async_wait<kStages - 1>();
+    __syncwarp();
+    const uint32_t ks = ring_s + (i % kStages) * kStageBytes;
+    const uint32_t vs = ks + kTileBytes;
+    const int tok0 = (my_first + i * kWarps) * kT;
+
+    // S^T[head][tok] = Q . K^T, two n-tiles of 8 tokens.
+    float s[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+      const int row = j * 8 + (lane & 7);
+#pragma unroll
+      for (int kk = 0; kk < kD / 16; kk += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(ks + swz(row, 2 * kk + (lane >> 3)), b0, b1, b2, b3);
+        mma_bf16(s[j], qa[kk], b0, b1);
+        mma_bf16(s[j], qa[kk + 1], b2, b3);
+      }
+    }
+    // Online softmax (base 2), rows lane/4 and lane/4 + 8.
+    float mx = -INFINITY, mx8 = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const bool valid = tok0 + j * 8 + (lane & 3) * 2 + e < ctx;
+        s[j][e] = valid ? s[j][e] * a.scale_log2 : -INFINITY;
+        s[j][e + 2] = valid ? s[j][e + 2] * a.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, s[j][e]);
+        mx8 = fmaxf(mx8, s[j][e + 2]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    mx8 = fmaxf(mx8, __shfl_xor_sync(0xffffffffu, mx8, 1));
+    mx8 = fmaxf(mx8, __shfl_xor_sync(0xffffffffu, mx8, 2));
+    const float mn = fmaxf(m_r, mx), mn8 = fmaxf(m_r8, mx8);
+    const float base = mn == -INFINITY ? 0.f : mn, base8 = mn8 == -INFINITY ? 0.f : mn8;
+    const float corr = exp2f(m_r - base), corr8 = exp2f(m_r8 - base8);
+    m_r = mn;
+    m_r8 = mn8;
+    float p[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      p[j][0] = exp2f(s[j][0] - base);
+      p[j][1] = exp2f(s[j][1] - base);
+      p[j][2] = exp2f(s[j][2] - base8);
+      p[j][3] = exp2f(s[j][3] - base8);
+    }
+    l_r = l_r * corr + (p[0][0] + p[0][1] + p[1][0] + p[1][1]);
+    l_r8 = l_r8 * corr8 + (p[0][2] + p[0][3] + p[1][2] + p[1][3]);
+#pragma unroll
+    for (int n = 0; n < kD / 8; ++n) {
+      o[n][0] *= corr;
+      o[n][1] *= corr;
+      o[n][2] *= corr8;
+      o[n][3] *= corr8;
+    }
+    // O[head][d] += P[head][tok] . V[tok][d]; P straight from the S fragments.
+    uint32_t pa[4];
+    pa[0] = pack_bf16(p[0][0], p[0][1]);
+    pa[1] = pack_bf16(p[0][2], p[0][3]);
+    pa[2] = pack_bf16(p[1][0], p[1][1]);
+    pa[3] = pack_bf16(p[1][2], p[1][3]);
+    const int vrow = ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+    for (int n = 0; n < kD / 8; n += 2) {
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(vs + swz(vrow, n + (lane >> 4)), b0, b1, b2, b3);
+      mma_bf16(o[n], pa, b0, b1);
+      mma_bf16(o[n + 1], pa, b2, b3);
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+
+  // Full row sums across the 4 lanes sharing a row.
+  l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
+  l_r += __shfl_xor_sync(0xffffffffu, l_r, 2);
+  l_r8 += __shfl_xor_sync(0xffffffffu, l_r8, 1);
+  l_r8 += __shfl_xor_sync(0xffffffffu, l_r8, 2);
+
+  // Combine the 4 warps of the CTA through shared memory (reusing the rings).
+  __syncthreads();
+  float* so = reinterpret_cast<float*>(smem);                   // [warp][16][128]
+  float* sml = so + kWarps * 16 * kD;                           // [warp][16][2]
+  {
+    const int r = lane >> 2, c = (lane & 3) * 2;
+    float* ow = so + warp * 16 * kD;
+#pragma unroll
+    for (int n = 0; n < kD / 8; ++n) {
+      ow[r * kD + n * 8 + c] = o[n][0];
+      ow[r * kD + n * 8 + c + 1] = o[n][1];
+      ow[(r + 8) * kD + n * 8 + c] = o[n][2];
+      ow[(r + 8) * kD + n * 8 + c + 1] = o[n][3];
+    }
+    if ((lane & 3) == 0) {
+      sml[(warp * 16 + r) * 2] = m_r;
+      sml[(warp * 16 + r) * 2 + 1] = l_r;
+      sml[(warp * 16 + r + 8) * 2] = m_r8;
+      sml[(warp * 16 + r + 8) * 2 + 1] = l_r8;
+    }
+  }
+  __syncthreads();
+  const int rows = a.group;
+  for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
+    const int r = e / kD, d = e - r * kD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
+    const float Mb = M == -INFINITY ? 0.f : M;
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
+      L += f * sml[(w * 16 + r) * 2 + 1];
+      O += f * so[(w * 16 + r) * kD + d];
+    }
+    const uint64_t row = static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r;
+    if (a.splits == 1) {
+      a.out[row * kD + d] = L > 0.f ? O / L : 0.f;
+    } else {
+      a.part_o[(row * a.splits + split) * kD + d] = O;
+      if (d == 0) {
+        a.part_ml[(row * a.splits + split) * 2] = M;
+        a.part_ml[(row * a.splits + split) * 2 + 1] = L;
+      }
+    }
+  }
+}
+
+// Log-sum-exp merge of the split partials: one CTA per (request, q head).
+__global__ void attn_combine(const float* part_o, const float* part_ml, float* out, int splits, int d) {
+  const uint64_t row = blockIdx.x;
+  const float* ml = part_ml + row * splits * 2;
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, ml[2 * s]);
+  const float Mb = M == -INFINITY ? 0.f : M;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float L = 0.f, O = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float f = exp2f(ml[2 * s] - Mb);
+      L += f * ml[2 * s + 1];
+      O += f * part_o[(row * splits + s) * d + j];
+    }
+    out[row * d + j] = L > 0.f ? O / L : 0.f;
+  }
+}
+
+// Generic path (any head_dim <= 256 that is a multiple of 32, fp32 or bf16,
+// any block_tokens): one warp per (request, query head), fp32 online softmax.
+// Serves the tiny fp32 configuration; not a performance path.
+template <typename T>
+__device__ __forceinline__ float ld_elt(const T* p);
+template <>
+__device__ __forceinline__ float ld_elt<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ld_elt<uint16_t>(const uint16_t* p) {
+  return __uint_as_float(static_cast<uint32_t>(*p) << 16);
+}
+
+template <typename T>
+__global__ void attn_generic(const uint8_t* pool, uint64_t page_bytes, const uint32_t* tables, const int32_t* ctx_lens,
+                             const T* q, float* out, int heads, int group, int head_dim, int block_tokens,
+                             int max_blocks, float scale) {
+  const int b = blockIdx.y, hq = blockIdx.x, h = hq / group, lane = threadIdx.x;
+  const int per_lane = head_dim / 32;
+  float qv[8], acc[8];
+  const T* qrow = q + (static_cast<uint64_t>(b) * heads * group + hq) * head_dim;
+  for (int i = 0; i < per_lane; ++i) {
+    qv[i] = ld_elt<T>(qrow + lane + 32 * i);
+    acc[i] = 0.f;
+  }
+  const int ctx = ctx_lens[b];
+  float m = -INFINITY, l = 0.f;
+  for (int t = 0; t < ctx; ++t) {
+    const uint32_t page = tables[static_cast<uint64_t>(b) * max_blocks + t / block_tokens];
+    const int slot = t % block_tokens;
+    const T* base = reinterpret_cast<const T*>(pool + static_cast<uint64_t>(page) * page_bytes);
+    const T* k = base + (static_cast<uint64_t>(h) * block_tokens + slot) * head_dim;
+    const T* v = base + (static_cast<uint64_t>(heads + h) * block_tokens + slot) * head_dim;
+    float dot = 0.f;
+    for (int i = 0; i < per_lane; ++i) dot += qv[i] * ld_elt<T>(k + lane + 32 * i);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+    const float x = dot * scale;
+    const float mn = fmaxf(m, x);
+    const float corr = __expf(m - mn), p = __expf(x - mn);
+    l = l * corr + p;
+    for (int i = 0; i < per_lane; ++i) acc[i] = acc[i] * corr + p * ld_elt<T>(v + lane + 32 * i);
+    m = mn;
+  }
+  float* orow = out + (static_cast<uint64_t>(b) * heads * group + hq) * head_dim;
+  for (int i = 0; i < per_lane; ++i) orow[lane + 32 * i] = l > 0.f ? acc[i] / l : 0.f;
+}
+
+bool fast_path(const kvx_page_layout* l) {
+  return l->dtype == KVX_DTYPE_BF16 && l->head_dim == kD && l->block_tokens == kT;
+}
+
+// Splits over the context so that (requests x kv heads x splits) CTAs fill
+// the machine in whole waves while each warp still streams >= 4 pages.
+int choose_splits(int batch, int heads, int max_ctx, int requested, int sms) {
+  if (requested > 0) return requested;
+  const int pages = std::max(1, (max_ctx + kT - 1) / kT);
+  const int max_splits = std::max(1, pages / (kWarps * 4));
+  const long base = static_cast<long>(batch) * heads;
+  const long slots = 2L * sms;  // 2 CTAs per SM (96 KiB smem each)
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= std::min(max_splits, 256); ++s) {
+    const long ctas = base * s;
+    const double waves = std::ceil(static_cast<double>(ctas) / slots);
+    const double cost = waves * std::ceil(static_cast<double>(pages) / s) + 0.02 * s;  // merge overhead
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
+}  // namespace
+}  // namespace kvx
+
+extern "C" {
+
+uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx_attn_params* params, int32_t batch,
+                                        int32_t max_ctx) {
+  if (!layout || !params || batch <= 0 || !kvx::fast_path(layout)) return 0;
+  const int splits = kvx::choose_splits(batch, layout->num_kv_heads, max_ctx, params->num_splits, kvx::sm_count(0));
+  if (splits <= 1) return 0;
+  const uint64_t rows = static_cast<uint64_t>(batch) * params->num_q_heads;
+  return rows * splits * (kvx::kD + 2) * sizeof(float);
+}
+
+int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
+                         const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q, float* d_out,
+                         int32_t batch, int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (!pool || !layout || !params || !d_block_tables || !d_ctx_lens || !d_q || !d_out)
+    return kvx::fail_arg("kvx_decode_attention: null argument");
+  if (batch <= 0) return KVX_OK;
+  const int H = layout->num_kv_heads, Hq = params->num_q_heads;
+  if (H <= 0 || Hq <= 0 || Hq % H != 0) return kvx::fail_arg("kvx_decode_attention: num_q_heads must be a multiple of num_kv_heads");
+  if (kvx_page_bytes(layout) != pool->page_bytes) return kvx::fail_arg("kvx_decode_attention: layout/page size mismatch");
+  const int group = Hq / H;
+  const float scale = params->scale > 0.f ? params->scale : 1.0f / std::sqrt(static_cast<float>(layout->head_dim));
+  const cudaStream_t st = kvx::as_stream(stream);
+
+  if (kvx::fast_path(layout) && group <= 16) {
+    static bool configured = false;
+    if (!configured) {
+      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kvx::kSmemBytes),
+                   "kvx_decode_attention: smem attribute");
+      configured = true;
+    }
+    const int splits = kvx::choose_splits(batch, H, max_ctx, params->num_splits, kvx::sm_count(pool->device));
+    kvx::AttnArgs a{};
+    a.pool = pool->base;
+    a.page_bytes = pool->page_bytes;
+    a.tables = d_block_tables;
+    a.ctx_lens = d_ctx_lens;
+    a.q = static_cast<const uint16_t*>(d_q);
+    a.out = d_out;
+    a.heads = H;
+    a.group = group;
+    a.max_blocks = params->max_blocks;
+    a.splits = splits;
+    a.scale_log2 = scale * kvx::kLog2e;
+    if (splits > 1) {
+      const uint64_t rows = static_cast<uint64_t>(batch) * Hq;
+      const uint64_t need = rows * splits * (kvx::kD + 2) * sizeof(float);
+      if (!d_workspace || workspace_bytes < need) return kvx::fail_arg("kvx_decode_attention: workspace too small");
+      a.part_o = static_cast<float*>(d_workspace);
+      a.part_ml = a.part_o + rows * splits * kvx::kD;
+    }
+    dim3 grid(splits, H, batch);
+    kvx::attn_bf16_d128<<<grid, kvx::kWarps * 32, kvx::kSmemBytes, st>>>(a);
+    KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");
+    if (splits > 1) {
+      kvx::attn_combine<<<static_cast<unsigned>(static_cast<uint64_t>(batch) * Hq), kvx::kD, 0, st>>>(
+          a.part_o, a.part_ml, d_out, splits, kvx::kD);
+      KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention(combine)");
+    }
+    return KVX_OK;
+  }
+
+  if (layout->head_dim % 32 != 0 || layout->head_dim > 256) {
+    kvx::set_error("kvx_decode_attention: head_dim must be a multiple of 32 and <= 256");
+    return KVX_ERR_UNSUPPORTED;
+  }
+  dim3 grid(Hq, batch);
+  if (layout->dtype == KVX_DTYPE_F32)
+    kvx::attn_generic<float><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, d_block_tables, d_ctx_lens,
+                                                  static_cast<const float*>(d_q), d_out, H, group, layout->head_dim,
+                                                  layout->block_tokens, params->max_blocks, scale);
+  else
+    kvx::attn_generic<uint16_t><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, d_block_tables, d_ctx_lens,
+                                                     static_cast<const uint16_t*>(d_q), d_out, H, group,
+                                                     layout->head_dim, layout->block_tokens, params->max_blocks,
+                                                     scale);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention(generic)");
+  return KVX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,296 @@
+// K1 pack, K2 unpack, K3 page copy (migration), K5 fill / append — sm_100a.
+//
+// All three movers are one gather/scatter over (page, chunk) work items:
+//   pack    src pages by id      -> dst contiguous   (reference SwapOut /
+//           HostCopy source side, kvstore.cpp:230-269, 691-706; migration
+//           send side, kvstore.cpp:753-769)
+//   unpack  src contiguous       -> dst pages by id  (LoadH2D / NetArrive
+//           landing, kvstore.cpp:522-533, 599-611, 914-923)
+//   copy    src pages by id      -> dst pages by id  (fused pack+send+unpack;
+//           dst may be a peer GPU's pool over NVLink or a mapped host pool)
+// The work is pure HBM traffic (2 bytes moved per payload byte), so the
+// kernels are built for bandwidth: 16-byte vectors, several loads in flight
+// per thread before any store, grid sized to the SM count, or — the TMA
+// variant — one issuing thread per SM driving cp.async.bulk through a ring of
+// shared-memory stages (no register staging at all).
+
+#include <algorithm>
+#include <vector>
+
+#include "kvx_common.cuh"
+
+namespace kvx {
+namespace {
+
+constexpr int kVecThreads = 256;
+constexpr int kVecUnroll = 4;
+constexpr uint32_t kVecChunk = kVecThreads * kVecUnroll * 16;  // 16 KiB per work item
+
+constexpr int kBulkStages = 6;
+constexpr uint32_t kBulkChunk = 32768;  // 32 KiB per TMA transfer
+constexpr uint32_t kBulkSmem = kBulkStages * kBulkChunk;
+
+struct MoveArgs {
+  const uint8_t* src;
+  const uint32_t* src_ids;  // null: contiguous
+  uint8_t* dst;
+  const uint32_t* dst_ids;  // null: contiguous
+  uint64_t n_pages;
+  uint64_t page_bytes;
+  uint32_t chunk_bytes;
+  uint32_t chunks_per_page;
+};
+
+__device__ __forceinline__ void item_addr(const MoveArgs& a, uint64_t item, const uint8_t*& s, uint8_t*& d,
+                                          uint32_t& bytes) {
+  const uint64_t page = item / a.chunks_per_page;
+  const uint32_t c = static_cast<uint32_t>(item - page * a.chunks_per_page);
+  const uint64_t sp = a.src_ids ? __ldg(a.src_ids + page) : page;
+  const uint64_t dp = a.dst_ids ? __ldg(a.dst_ids + page) : page;
+  const uint64_t off = static_cast<uint64_t>(c) * a.chunk_bytes;
+  s = a.src + sp * a.page_bytes + off;
+  d = a.dst + dp * a.page_bytes + off;
+  const uint64_t left = a.page_bytes - off;
+  bytes = static_cast<uint32_t>(left < a.chunk_bytes ? left : a.chunk_bytes);
+}
+
+// LDG.128 / STG.128: every thread issues kVecUnroll independent loads before
+// its stores, so one 256-thread CTA keeps 16 KiB in flight.
+__global__ void __launch_bounds__(kVecThreads) page_move_vec(MoveArgs a) {
+  const uint64_t items = a.n_pages * a.chunks_per_page;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint8_t* s8;
+    uint8_t* d8;
+    uint32_t bytes;
+    item_addr(a, item, s8, d8, bytes);
+    const int4* s = reinterpret_cast<const int4*>(s8);
+    int4* d = reinterpret_cast<int4*>(d8);
+    const uint32_t vecs = bytes / 16;
+    if (vecs == kVecThreads * kVecUnroll) {
+      int4 r[kVecUnroll];
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) r[u] = ld_stream(s + threadIdx.x + u * kVecThreads);
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) st_stream(d + threadIdx.x + u * kVecThreads, r[u]);
+    } else {
+      for (uint32_t v = threadIdx.x; v < vecs; v += kVecThreads) st_stream(d + v, ld_stream(s + v));
+    }
+  }
+}
+
+// TMA bulk variant: lane 0 of a single warp per SM streams chunks through a
+// kBulkStages-deep shared-memory ring. Load k+S-1 is issued as soon as the
+// bulk store of chunk k-1 has finished READING its stage.
+__global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kBulkStages];
+  if (threadIdx.x != 0) return;
+  const uint64_t items = a.n_pages * a.chunks_per_page;
+  if (blockIdx.x >= items) return;
+  const uint64_t mine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+
+  auto load = [&](uint64_t k) {
+    const uint8_t* s;
+    uint8_t* d;
+    uint32_t bytes;
+    item_addr(a, blockIdx.x + k * gridDim.x, s, d, bytes);
+    const int st = static_cast<int>(k % kBulkStages);
+    mbar_arrive_expect_tx(&full[st], bytes);
+    bulk_g2s(ring + st * kBulkChunk, s, bytes, &full[st]);
+  };
+  const uint64_t prologue = mine < kBulkStages ? mine : kBulkStages;
+  for (uint64_t k = 0; k < prologue; ++k) load(k);
+  for (uint64_t k = 0; k < mine; ++k) {
+    const int st = static_cast<int>(k % kBulkStages);
+    mbar_wait(&full[st], static_cast<uint32_t>((k / kBulkStages) & 1));
+    const uint8_t* s;
+    uint8_t* d;
+    uint32_t bytes;
+    item_addr(a, blockIdx.x + k * gridDim.x, s, d, bytes);
+    bulk_s2g(d, ring + st * kBulkChunk, bytes);
+    bulk_commit();
+    if (k >= 1 && k - 1 + kBulkStages < mine) {
+      bulk_wait_read<1>();  // store k-1 has drained its stage
+      load(k - 1 + kBulkStages);
+    }
+  }
+  bulk_wait<0>();
+}
+
+int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const char* who) {
+  if (a.n_pages == 0) return KVX_OK;
+  if (a.page_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(a.src) % 16 || reinterpret_cast<uintptr_t>(a.dst) % 16)
+    return fail_arg("page movers need 16-byte aligned pages");
+  const int sms = sm_count(device);
+  if (mode == KVX_COPY_TMA) {
+    a.chunk_bytes = static_cast<uint32_t>(std::min<uint64_t>(a.page_bytes, kBulkChunk));
+    a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + a.chunk_bytes - 1) / a.chunk_bytes);
+    static bool configured[64] = {};
+    const int dev = device < 0 ? 0 : device;
+    if (!configured[dev]) {
+      KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem), who);
+      configured[dev] = true;
+    }
+    const uint64_t items = a.n_pages * a.chunks_per_page;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms)));
+    page_move_bulk<<<grid, 32, kBulkSmem, stream>>>(a);
+  } else if (mode == KVX_COPY_AUTO || mode == KVX_COPY_SM) {
+    a.chunk_bytes = kVecChunk;
+    a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + kVecChunk - 1) / kVecChunk);
+    const uint64_t items = a.n_pages * a.chunks_per_page;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * 8));
+    page_move_vec<<<grid, kVecThreads, 0, stream>>>(a);
+  } else {
+    set_error(std::string(who) + ": unsupported copy mode");
+    return KVX_ERR_UNSUPPORTED;
+  }
+  KVX_CUDA_TRY(cudaGetLastError(), who);
+  return KVX_OK;
+}
+
+// ---- K5: contents -----------------------------------------------------------
+
+__global__ void __launch_bounds__(256) fill_pages_kernel(uint8_t* base, uint64_t page_bytes, const uint32_t* ids,
+                                                         const kvx_block_tag* tags, uint64_t n, uint64_t seed,
+                                                         int mode, int dtype) {
+  const uint32_t vecs = static_cast<uint32_t>(page_bytes / 16);
+  for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const kvx_block_tag t = tags[i];
+    const uint64_t h = block_base(seed, t.session, t.layer, t.block);
+    uint4* page = reinterpret_cast<uint4*>(base + static_cast<uint64_t>(ids[i]) * page_bytes);
+    for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
+      uint4 out;
+      if (mode == KVX_FILL_BITS) {
+        const uint64_t w0 = splitmix64(h + 2ull * v), w1 = splitmix64(h + 2ull * v + 1);
+        out = make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1),
+                         static_cast<uint32_t>(w1 >> 32));
+      } else if (dtype == KVX_DTYPE_F32) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(unit_value(splitmix64(h + 4ull * v + e)));
+        out = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t lo = f32_to_bf16_rne(unit_value(splitmix64(h + 8ull * v + 2 * e)));
+          const uint32_t hi = f32_to_bf16_rne(unit_value(splitmix64(h + 8ull * v + 2 * e + 1)));
+          w[e] = lo | (hi << 16);
+        }
+        out = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      page[v] = out;
+    }
+  }
+}
+
+// One CTA per appended token: K and V of every kv head into the page slot.
+__global__ void __launch_bounds__(128) append_kv_kernel(uint8_t* base, uint64_t page_bytes, const uint32_t* ids,
+                                                        const int32_t* slots, const uint8_t* k, const uint8_t* v,
+                                                        int heads, int tokens, int row_bytes) {
+  const uint64_t i = blockIdx.x;
+  uint8_t* page = base + static_cast<uint64_t>(ids[i]) * page_bytes;
+  const int slot = slots[i];
+  const int row_vecs = row_bytes / 16;
+  const int total = 2 * heads * row_vecs;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int kv = e / (heads * row_vecs);
+    const int rem = e - kv * heads * row_vecs;
+    const int h = rem / row_vecs, c = rem - h * row_vecs;
+    const uint8_t* src = (kv ? v : k) + (i * heads + h) * static_cast<uint64_t>(row_bytes);
+    uint8_t* dst = page + (static_cast<uint64_t>(kv * heads + h) * tokens + slot) * row_bytes;
+    reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
+  }
+}
+
+}  // namespace
+}  // namespace kvx
+
+using kvx::MoveArgs;
+
+extern "C" {
+
+int kvx_pack(const kvx_pool* src, const uint32_t* d_page_ids, uint64_t n, void* d_dst, int mode, void* stream) {
+  if (!src || (n && (!d_page_ids || !d_dst))) return kvx::fail_arg("kvx_pack: null argument");
+  MoveArgs a{src->base, d_page_ids, static_cast<uint8_t*>(d_dst), nullptr, n, src->page_bytes, 0, 0};
+  return kvx::launch_move(a, mode, src->device, kvx::as_stream(stream), "kvx_pack");
+}
+
+int kvx_unpack(kvx_pool* dst, const uint32_t* d_page_ids, uint64_t n, const void* d_src, int mode, void* stream) {
+  if (!dst || (n && (!d_page_ids || !d_src))) return kvx::fail_arg("kvx_unpack: null argument");
+  MoveArgs a{static_cast<const uint8_t*>(d_src), nullptr, dst->base, d_page_ids, n, dst->page_bytes, 0, 0};
+  return kvx::launch_move(a, mode, dst->device, kvx::as_stream(stream), "kvx_unpack");
+}
+
+int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
+                   uint64_t n, int mode, void* stream) {
+  if (!src || !dst || (n && (!src_ids || !dst_ids))) return kvx::fail_arg("kvx_copy_pages: null argument");
+  if (src->page_bytes != dst->page_bytes) return kvx::fail_arg("kvx_copy_pages: page size mismatch");
+  if (n == 0) return KVX_OK;
+  const cudaStream_t st = kvx::as_stream(stream);
+  if (mode != KVX_COPY_CE) {
+    MoveArgs a{src->base, src_ids, dst->base, dst_ids, n, src->page_bytes, 0, 0};
+    const int dev = src->device >= 0 ? src->device : dst->device;
+    return kvx::launch_move(a, mode, dev, st, "kvx_copy_pages");
+  }
+  // Copy engines: coalesce runs of consecutive ids, one batched submission.
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
+  for (uint64_t i = 0; i < n;) {
+    if (src_ids[i] >= src->num_pages || dst_ids[i] >= dst->num_pages)
+      return kvx::fail_arg("kvx_copy_pages: page id out of range");
+    uint64_t j = i + 1;
+    while (j < n && src_ids[j] == src_ids[j - 1] + 1 && dst_ids[j] == dst_ids[j - 1] + 1) ++j;
+    srcs.push_back(src->base + static_cast<uint64_t>(src_ids[i]) * src->page_bytes);
+    dsts.push_back(dst->base + static_cast<uint64_t>(dst_ids[i]) * dst->page_bytes);
+    sizes.push_back((j - i) * src->page_bytes);
+    i = j;
+  }
+  if (st == nullptr) {  // batch API needs an explicit stream
+    for (size_t r = 0; r < srcs.size(); ++r)
+      KVX_CUDA_TRY(cudaMemcpyAsync(dsts[r], srcs[r], sizes[r], cudaMemcpyDefault, st), "kvx_copy_pages(CE)");
+    return KVX_OK;
+  }
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  size_t attr_idx = 0, fail_idx = 0;
+  KVX_CUDA_TRY(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1,
+                                    &fail_idx, st),
+               "kvx_copy_pages(CE): cudaMemcpyBatchAsync");
+  return KVX_OK;
+}
+
+int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n, uint64_t seed,
+                   const kvx_page_layout* layout, int fill_mode, void* stream) {
+  if (!pool || (n && (!d_page_ids || !d_tags))) return kvx::fail_arg("kvx_fill_pages: null argument");
+  if (fill_mode != KVX_FILL_BITS && fill_mode != KVX_FILL_VALUES) return kvx::fail_arg("kvx_fill_pages: bad mode");
+  const int dtype = layout ? layout->dtype : KVX_DTYPE_BF16;
+  if (fill_mode == KVX_FILL_VALUES && (!layout || kvx_page_bytes(layout) != pool->page_bytes))
+    return kvx::fail_arg("kvx_fill_pages: layout does not match the pool's page size");
+  if (n == 0) return KVX_OK;
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, kvx::sm_count(pool->device) * 8ull));
+  kvx::fill_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(pool->base, pool->page_bytes, d_page_ids, d_tags,
+                                                                     n, seed, fill_mode, dtype);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_fill_pages");
+  return KVX_OK;
+}
+
+int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_page_ids, const int32_t* d_slots,
+                  const void* d_k, const void* d_v, uint64_t n, void* stream) {
+  if (!pool || !layout || (n && (!d_page_ids || !d_slots || !d_k || !d_v)))
+    return kvx::fail_arg("kvx_append_kv: null argument");
+  if (kvx_page_bytes(layout) != pool->page_bytes) return kvx::fail_arg("kvx_append_kv: layout/page size mismatch");
+  const int elt = layout->dtype == KVX_DTYPE_BF16 ? 2 : 4;
+  const int row_bytes = layout->head_dim * elt;
+  if (row_bytes % 16 != 0) return kvx::fail_arg("kvx_append_kv: head_dim * sizeof(dtype) must be a multiple of 16");
+  if (n == 0) return KVX_OK;
+  kvx::append_kv_kernel<<<static_cast<unsigned>(n), 128, 0, kvx::as_stream(stream)>>>(
+      pool->base, pool->page_bytes, d_page_ids, d_slots, static_cast<const uint8_t*>(d_k),
+      static_cast<const uint8_t*>(d_v), layout->num_kv_heads, layout->block_tokens, row_bytes);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_append_kv");
+  return KVX_OK;
+}
+
+}  // extern "C"

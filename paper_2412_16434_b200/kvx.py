@@ -1,0 +1,241 @@
+"""ctypes binding of the kvx C ABI (include/kvx.h) — the B200 payload path.
+
+Device memory and streams come from PyTorch (plumbing only): tensors are
+passed as raw pointers, streams as cudaStream_t handles. The library is the
+in-tree lib/libkvx.so; there is no CPU fallback — if the extension or a CUDA
+device is missing, every call raises KvxError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+from . import _build
+
+F32, BF16 = 0, 1
+FILL_BITS, FILL_VALUES = 0, 1
+COPY_AUTO, COPY_SM, COPY_TMA, COPY_CE = 0, 1, 2, 3
+
+
+class KvxError(RuntimeError):
+    pass
+
+
+class PageLayout(C.Structure):
+    _fields_ = [("num_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("block_tokens", C.c_int32),
+                ("dtype", C.c_int32)]
+
+    def page_bytes(self) -> int:
+        return 2 * self.num_kv_heads * self.block_tokens * self.head_dim * (2 if self.dtype == BF16 else 4)
+
+
+class BlockTag(C.Structure):
+    _fields_ = [("session", C.c_uint32), ("layer", C.c_uint32), ("block", C.c_uint32)]
+
+
+class AttnParams(C.Structure):
+    _fields_ = [("num_q_heads", C.c_int32), ("max_blocks", C.c_int32), ("num_splits", C.c_int32),
+                ("scale", C.c_float)]
+
+
+_LIB: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    _build.ensure_built()
+    if not _build.KVX_LIB.exists():
+        raise KvxError(f"kvx extension missing: {_build.KVX_LIB}")
+    h = C.CDLL(str(_build.KVX_LIB))
+    P, V, U64 = C.POINTER, C.c_void_p, C.c_uint64
+    sigs = {
+        "kvx_last_error": ([], C.c_char_p),
+        "kvx_version": ([], C.c_int),
+        "kvx_page_bytes": ([P(PageLayout)], U64),
+        "kvx_pool_create": ([C.c_int, U64, U64, P(V)], C.c_int),
+        "kvx_pool_create_host": ([U64, U64, P(V)], C.c_int),
+        "kvx_pool_wrap": ([C.c_int, V, U64, U64, P(V)], C.c_int),
+        "kvx_pool_destroy": ([V], C.c_int),
+        "kvx_pool_base": ([V], V),
+        "kvx_pool_num_pages": ([V], U64),
+        "kvx_pool_page_bytes": ([V], U64),
+        "kvx_pool_device": ([V], C.c_int),
+        "kvx_pool_ipc_export": ([V, V], C.c_int),
+        "kvx_pool_ipc_open": ([C.c_int, V, U64, U64, P(V)], C.c_int),
+        "kvx_enable_peer_access": ([C.c_int, C.c_int], C.c_int),
+        "kvx_pack": ([V, V, U64, V, C.c_int, V], C.c_int),
+        "kvx_unpack": ([V, V, U64, V, C.c_int, V], C.c_int),
+        "kvx_copy_pages": ([V, V, V, V, U64, C.c_int, V], C.c_int),
+        "kvx_fill_pages": ([V, V, V, U64, U64, P(PageLayout), C.c_int, V], C.c_int),
+        "kvx_append_kv": ([V, P(PageLayout), V, V, V, V, U64, V], C.c_int),
+        "kvx_decode_attention_workspace": ([P(PageLayout), P(AttnParams), C.c_int32, C.c_int32], U64),
+        "kvx_decode_attention": ([V, P(PageLayout), P(AttnParams), V, V, V, V, C.c_int32, C.c_int32, V, U64, V],
+                                 C.c_int),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(h, name)
+        fn.argtypes = args
+        fn.restype = res
+    _LIB = h
+    return h
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise KvxError((lib().kvx_last_error() or b"").decode())
+
+
+def _ptr(x) -> Optional[int]:
+    """Raw address of a tensor / int / None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Pool:
+    """A page pool (DEVICE in HBM, or HOST pinned+mapped)."""
+
+    def __init__(self, num_pages: int, page_bytes: int, device: int = 0, host: bool = False,
+                 _handle: Optional[int] = None):
+        L = lib()
+        h = C.c_void_p()
+        if _handle is not None:
+            h = C.c_void_p(_handle)
+        elif host:
+            check(L.kvx_pool_create_host(num_pages, page_bytes, C.byref(h)))
+        else:
+            check(L.kvx_pool_create(device, num_pages, page_bytes, C.byref(h)))
+        self.handle = h
+        self.num_pages = num_pages
+        self.page_bytes = page_bytes
+        self.device = -1 if host else device
+
+    @classmethod
+    def wrap(cls, tensor, num_pages: int, page_bytes: int, device: int = 0) -> "Pool":
+        h = C.c_void_p()
+        check(lib().kvx_pool_wrap(device, tensor.data_ptr(), num_pages, page_bytes, C.byref(h)))
+        p = cls(num_pages, page_bytes, device, _handle=h.value)
+        p._keep = tensor
+        return p
+
+    @classmethod
+    def ipc_open(cls, handle64: bytes, num_pages: int, page_bytes: int, device: int) -> "Pool":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(handle64), 64)
+        check(lib().kvx_pool_ipc_open(device, buf, num_pages, page_bytes, C.byref(h)))
+        return cls(num_pages, page_bytes, device, _handle=h.value)
+
+    def ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(64)
+        check(lib().kvx_pool_ipc_export(self.handle, buf))
+        return buf.raw
+
+    @property
+    def base(self) -> int:
+        return lib().kvx_pool_base(self.handle)
+
+    def as_tensor(self):
+        """uint8 view [num_pages, page_bytes] of the pool memory (no copy)."""
+        import torch
+        from torch.utils.dlpack import from_dlpack  # noqa: F401
+        n = self.num_pages * self.page_bytes
+        if self.device < 0:
+            buf = (C.c_uint8 * n).from_address(self.base)
+            return torch.frombuffer(buf, dtype=torch.uint8).view(self.num_pages, self.page_bytes)
+        return _device_view(self.base, n, self.device).view(self.num_pages, self.page_bytes)
+
+    def close(self) -> None:
+        if self.handle:
+            check(lib().kvx_pool_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_view(ptr: int, nbytes: int, device: int):
+    """Wrap raw device memory as a uint8 torch tensor (non-owning)."""
+    import torch
+
+    class _CudaArray:
+        def __init__(self, p, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (p, False), "version": 3}
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CudaArray(ptr, nbytes), device=f"cuda:{device}")
+
+
+def page_bytes(layout: PageLayout) -> int:
+    return lib().kvx_page_bytes(C.byref(layout))
+
+
+def pack(pool: Pool, page_ids, n: int, dst, mode: int = COPY_AUTO, stream=None) -> None:
+    check(lib().kvx_pack(pool.handle, _ptr(page_ids), n, _ptr(dst), mode, _stream(stream)))
+
+
+def unpack(pool: Pool, page_ids, n: int, src, mode: int = COPY_AUTO, stream=None) -> None:
+    check(lib().kvx_unpack(pool.handle, _ptr(page_ids), n, _ptr(src), mode, _stream(stream)))
+
+
+def copy_pages(src: Pool, src_ids, dst: Pool, dst_ids, n: int, mode: int = COPY_AUTO, stream=None) -> None:
+    if mode == COPY_CE:
+        import numpy as np
+        s = np.ascontiguousarray(src_ids, dtype=np.uint32)
+        d = np.ascontiguousarray(dst_ids, dtype=np.uint32)
+        check(lib().kvx_copy_pages(src.handle, s.ctypes.data, dst.handle, d.ctypes.data, n, mode, _stream(stream)))
+        return
+    check(lib().kvx_copy_pages(src.handle, _ptr(src_ids), dst.handle, _ptr(dst_ids), n, mode, _stream(stream)))
+
+
+def fill_pages(pool: Pool, page_ids, tags, n: int, seed: int, layout: Optional[PageLayout], mode: int,
+               stream=None) -> None:
+    lay = C.byref(layout) if layout is not None else None
+    check(lib().kvx_fill_pages(pool.handle, _ptr(page_ids), _ptr(tags), n, seed, lay, mode, _stream(stream)))
+
+
+def append_kv(pool: Pool, layout: PageLayout, page_ids, slots, k, v, n: int, stream=None) -> None:
+    check(lib().kvx_append_kv(pool.handle, C.byref(layout), _ptr(page_ids), _ptr(slots), _ptr(k), _ptr(v), n,
+                              _stream(stream)))
+
+
+@dataclass
+class Attention:
+    """Paged decode attention (K4) with its own workspace."""
+    layout: PageLayout
+    num_q_heads: int
+    max_blocks: int
+    num_splits: int = 0
+    scale: float = 0.0
+
+    def params(self) -> AttnParams:
+        return AttnParams(self.num_q_heads, self.max_blocks, self.num_splits, self.scale)
+
+    def workspace_bytes(self, batch: int, max_ctx: int) -> int:
+        p = self.params()
+        return lib().kvx_decode_attention_workspace(C.byref(self.layout), C.byref(p), batch, max_ctx)
+
+    def __call__(self, pool: Pool, block_tables, ctx_lens, q, out, batch: int, max_ctx: int, workspace=None,
+                 stream=None) -> None:
+        p = self.params()
+        ws = _ptr(workspace)
+        ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        check(lib().kvx_decode_attention(pool.handle, C.byref(self.layout), C.byref(p), _ptr(block_tables),
+                                         _ptr(ctx_lens), _ptr(q), _ptr(out), batch, max_ctx, ws, ws_bytes,
+                                         _stream(stream)))

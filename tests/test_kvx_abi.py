@@ -1,0 +1,39 @@
+"""CPU-side checks of the kvx C ABI library (no kernels launched here)."""
+import ctypes
+import re
+
+import pytest
+
+from conftest import ROOT
+
+
+def test_kvx_library_exports_every_declared_symbol(product_libs):
+    decl = (ROOT / "include" / "kvx.h").read_text()
+    names = re.findall(r"^\s*(?:int|void\*?|uint64_t|const char\*)\s*\*?\s*(kvx_\w+)\(", decl, re.M)
+    assert len(names) >= 20
+    lib = ctypes.CDLL(str(product_libs.KVX_LIB))
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing
+
+
+def test_kvx_fails_loudly_without_a_device(product_libs):
+    """No CPU fallback: pool creation must error when no CUDA device exists."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    from paper_2412_16434_b200 import kvx
+    with pytest.raises(kvx.KvxError):
+        kvx.Pool(4, 4096, device=0)
+
+
+def test_page_bytes_match_the_store_accounting(product_libs):
+    """kvx page size == the reference's layer_block_bytes for each config
+    (kvstore.cpp:67 = kv_bytes_per_layer(16) with kv_bytes_per_token summed
+    over layers): tiny 2 L x 4 H x d64 fp32; 8B 32 L x 8 H x d128 bf16; 70B 80 L."""
+    from paper_2412_16434_b200 import kvstore as K
+    from paper_2412_16434_b200 import kvx
+    for layers, heads, dim, dtype, elt in [(2, 4, 64, kvx.F32, 4), (32, 8, 128, kvx.BF16, 2),
+                                           (80, 8, 128, kvx.BF16, 2)]:
+        per_token = layers * 2 * heads * dim * elt
+        gpu = K.GpuProfile(kv_bytes_per_token=per_token, num_layers=layers)
+        assert K.kv_bytes_per_layer(16, gpu) == kvx.page_bytes(kvx.PageLayout(heads, dim, 16, dtype))

@@ -1,0 +1,234 @@
+"""Payload parity on the B200: every kvx kernel vs the CPU restatement
+(oracle/kvx_oracle.c), through the C ABI (include/kvx.h).
+
+Bar: bit-exact for fill / pack / unpack / page copy / append (byte
+permutations); attention within the stated tolerance against an fp64
+restatement (parity unpinned by the reference, which only models the step):
+  fp32 pages (tiny):    max|err| <= 1e-5 * max(1, |ref|)
+  bf16 pages, fp32 out: max|err| <= 2e-3 + 1e-2 * |ref|   (P is rounded to bf16
+                        before the PV product, as on any bf16 tensor-core path)
+"""
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2412_16434_b200 import kvx  # noqa: E402
+
+import oracle.oracle as O  # noqa: E402  (test infrastructure)
+
+TINY = kvx.PageLayout(4, 64, 16, kvx.F32)      # config 1: 2 layers, 4 kv heads, d 64, fp32
+LLAMA8B = kvx.PageLayout(8, 128, 16, kvx.BF16)  # configs 2/3: 8 kv heads, d 128, bf16
+
+
+def olayout(l):
+    return O.Layout(l.num_kv_heads, l.head_dim, l.block_tokens, l.dtype)
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+    return torch.device("cuda:0")
+
+
+def to_dev(a: np.ndarray, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def filled_pool(layout, num_pages, ids, tags, seed, mode, dev):
+    pb = layout.page_bytes()
+    pool = kvx.Pool(num_pages, pb, device=0)
+    kvx.fill_pages(pool, to_dev(ids.astype(np.int32), dev), to_dev(tags.view(np.int32), dev), len(ids), seed,
+                   layout, mode)
+    ref = np.zeros((num_pages, pb), np.uint8)
+    O.fill_pages(ref, pb, ids, tags, seed, olayout(layout), mode)
+    return pool, ref
+
+
+@pytest.mark.parametrize("layout", [TINY, LLAMA8B], ids=["tiny-f32", "8b-bf16"])
+@pytest.mark.parametrize("mode", [kvx.FILL_BITS, kvx.FILL_VALUES])
+def test_fill_pages_bit_exact(dev, layout, mode):
+    rng = np.random.default_rng(1)
+    n = 37
+    ids = rng.permutation(64)[:n].astype(np.uint32)
+    tags = O.tags_array(rng.integers(0, 9, n), rng.integers(0, 80, n), rng.integers(0, 2048, n))
+    pool, ref = filled_pool(layout, 64, ids, tags, 0xC0FFEE, mode, dev)
+    torch.cuda.synchronize()
+    got = pool.as_tensor().cpu().numpy()
+    assert np.array_equal(got[ids], ref[ids])
+    if mode == kvx.FILL_VALUES:
+        vals = got[ids].view(np.float32 if layout.dtype == kvx.F32 else np.uint16)
+        if layout.dtype == kvx.BF16:
+            vals = (vals.astype(np.uint32) << 16).view(np.float32)
+        assert np.all(np.abs(vals) <= 1.7321) and 0.8 < vals.std() < 1.2
+
+
+@pytest.mark.parametrize("mode", [kvx.COPY_SM, kvx.COPY_TMA])
+@pytest.mark.parametrize("layout,n", [(TINY, 1), (TINY, 24), (LLAMA8B, 0), (LLAMA8B, 1), (LLAMA8B, 333)])
+def test_pack_unpack_bit_exact(dev, layout, n, mode):
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(n)
+    pages = 2 * max(n, 1) + 3
+    ids = rng.permutation(pages)[:n].astype(np.uint32)
+    dst_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    tags = O.tags_array(7, rng.integers(0, 32, n), np.arange(n))
+    src, ref = filled_pool(layout, pages, ids, tags, 42, kvx.FILL_BITS, dev)
+    buf = torch.zeros(max(n, 1) * pb, dtype=torch.uint8, device=dev)
+    kvx.pack(src, to_dev(ids.view(np.int32), dev), n, buf, mode)
+    ref_buf = np.zeros(max(n, 1) * pb, np.uint8)
+    O.pack(ref, pb, ids, ref_buf)
+    dst = kvx.Pool(pages, pb, device=0)
+    dst.as_tensor().zero_()
+    kvx.unpack(dst, to_dev(dst_ids.view(np.int32), dev), n, buf, mode)
+    ref_dst = np.zeros((pages, pb), np.uint8)
+    O.unpack(ref_dst, pb, dst_ids, ref_buf)
+    torch.cuda.synchronize()
+    assert np.array_equal(buf.cpu().numpy(), ref_buf)
+    assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
+
+
+@pytest.mark.parametrize("mode", [kvx.COPY_SM, kvx.COPY_TMA, kvx.COPY_CE])
+def test_copy_pages_between_pools_bit_exact(dev, mode):
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(5)
+    n, pages = 200, 260
+    src_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    dst_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    dst_ids[10:20] = np.arange(100, 110)  # a run the copy engines coalesce
+    src_ids[10:20] = np.arange(30, 40)
+    tags = O.tags_array(3, 5, np.arange(n))
+    src, ref = filled_pool(layout, pages, src_ids, tags, 9, kvx.FILL_VALUES, dev)
+    dst = kvx.Pool(pages, pb, device=0)
+    dst.as_tensor().zero_()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        if mode == kvx.COPY_CE:
+            kvx.copy_pages(src, src_ids, dst, dst_ids, n, mode, stream=s)
+        else:
+            kvx.copy_pages(src, to_dev(src_ids.view(np.int32), dev), dst, to_dev(dst_ids.view(np.int32), dev), n,
+                           mode, stream=s)
+    s.synchronize()
+    ref_dst = np.zeros((pages, pb), np.uint8)
+    O.copy_pages(ref, src_ids, ref_dst, dst_ids, pb)
+    assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
+
+
+def test_host_pool_zero_copy_roundtrip(dev):
+    """DEVICE -> mapped pinned HOST pool -> DEVICE with the SM mover (PCIe)."""
+    layout = TINY
+    pb = layout.page_bytes()
+    n = 24
+    ids = np.arange(n, dtype=np.uint32)[::-1].copy()
+    tags = O.tags_array(1, 0, np.arange(n))
+    src, ref = filled_pool(layout, n, ids, tags, 11, kvx.FILL_BITS, dev)
+    host = kvx.Pool(n, pb, host=True)
+    back = kvx.Pool(n, pb, device=0)
+    hid = to_dev(np.arange(n, dtype=np.int32), dev)
+    kvx.copy_pages(src, to_dev(ids.view(np.int32), dev), host, hid, n, kvx.COPY_SM)
+    kvx.copy_pages(host, hid, back, to_dev(ids.view(np.int32), dev), n, kvx.COPY_SM)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.as_tensor().numpy(), ref[ids])
+    assert np.array_equal(back.as_tensor().cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("layout", [TINY, LLAMA8B], ids=["tiny-f32", "8b-bf16"])
+def test_append_kv_bit_exact(dev, layout):
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(3)
+    n, pages = 9, 16
+    ids = rng.permutation(pages)[:n].astype(np.uint32)
+    slots = rng.integers(0, layout.block_tokens, n).astype(np.int32)
+    elt = np.float32 if layout.dtype == kvx.F32 else np.uint16
+    k = rng.integers(0, 2**15, (n, layout.num_kv_heads, layout.head_dim)).astype(elt)
+    v = rng.integers(0, 2**15, (n, layout.num_kv_heads, layout.head_dim)).astype(elt)
+    all_ids = np.arange(pages, dtype=np.uint32)
+    pool, ref = filled_pool(layout, pages, all_ids, O.tags_array(0, 0, all_ids), 5, kvx.FILL_BITS, dev)
+    kvx.append_kv(pool, layout, to_dev(ids.view(np.int32), dev), to_dev(slots, dev), to_dev(k, dev), to_dev(v, dev), n)
+    O.append_kv(ref, olayout(layout), ids, slots, k, v)
+    torch.cuda.synchronize()
+    assert np.array_equal(pool.as_tensor().cpu().numpy(), ref)
+
+
+def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0):
+    rng = np.random.default_rng(seed)
+    pb = layout.page_bytes()
+    batch = len(ctx_lens)
+    max_ctx = int(max(ctx_lens))
+    max_blocks = (max_ctx + layout.block_tokens - 1) // layout.block_tokens
+    pages = batch * max_blocks + 5
+    perm = rng.permutation(pages).astype(np.uint32)
+    tables = perm[:batch * max_blocks].reshape(batch, max_blocks)
+    all_ids = np.arange(pages, dtype=np.uint32)
+    pool, ref = filled_pool(layout, pages, all_ids, O.tags_array(2, 1, all_ids), seed + 77, kvx.FILL_VALUES, dev)
+    if layout.dtype == kvx.BF16:
+        qf = rng.standard_normal((batch, hq, layout.head_dim)).astype(np.float32)
+        q = (qf.view(np.uint32) + 0x7FFF + ((qf.view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
+    else:
+        q = rng.standard_normal((batch, hq, layout.head_dim)).astype(np.float32)
+    ctx = np.asarray(ctx_lens, np.int32)
+    att = kvx.Attention(layout, hq, max_blocks, num_splits=splits)
+    ws_bytes = att.workspace_bytes(batch, max_ctx)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev) if ws_bytes else None
+    out = torch.full((batch, hq, layout.head_dim), float("nan"), dtype=torch.float32, device=dev)
+    att(pool, to_dev(tables.view(np.int32), dev), to_dev(ctx, dev), to_dev(q, dev), out, batch, max_ctx, ws)
+    torch.cuda.synchronize()
+    scale = 1.0 / np.sqrt(np.float32(layout.head_dim))
+    expect = O.decode_attention(ref, olayout(layout), hq, tables, ctx, q, float(np.float32(scale)))
+    return out.cpu().numpy().astype(np.float64), expect
+
+
+@pytest.mark.parametrize("ctx_lens", [[384], [1, 17, 200, 384], [16, 33]])
+def test_attention_tiny_fp32(dev, ctx_lens):
+    got, ref = _attention_case(dev, TINY, 8, ctx_lens)
+    assert np.all(np.abs(got - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref))), np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("hq,ctx_lens,splits", [
+    (32, [8192], 0), (32, [1, 15, 16, 17, 500, 1031], 0), (64, [4096, 33], 0), (8, [700], 1),
+    (32, [3000, 2999, 64], 7), (128, [257], 0), (32, [8192] * 8, 0),
+])
+def test_attention_bf16_d128(dev, hq, ctx_lens, splits):
+    got, ref = _attention_case(dev, LLAMA8B, hq, ctx_lens, splits, seed=len(ctx_lens) + hq)
+    err = np.abs(got - ref)
+    assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (err.max(), err.mean())
+    assert err.mean() < 5e-4
+
+
+def test_full_session_migration_property(dev):
+    """Config 2 at full size (1 GiB, 8B @ 8K): fill a session's 16,384 pages
+    at a random permutation, pack every layer, unpack into a second
+    permutation, and check every landed page equals a fresh fill of its tag."""
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    L, blocks = 32, 512
+    n = L * blocks
+    rng = np.random.default_rng(2026)
+    pool_pages = 2 * n
+    src_ids = rng.permutation(pool_pages)[:n].astype(np.uint32)
+    dst_ids = rng.permutation(pool_pages)[:n].astype(np.uint32)
+    tags = O.tags_array(0, np.repeat(np.arange(L), blocks), np.tile(np.arange(blocks), L))
+    src = kvx.Pool(pool_pages, pb)
+    dst = kvx.Pool(pool_pages, pb)
+    t_tags = to_dev(tags.view(np.int32), dev)
+    kvx.fill_pages(src, to_dev(src_ids.view(np.int32), dev), t_tags, n, 123, layout, kvx.FILL_BITS)
+    buf = torch.empty(blocks * pb, dtype=torch.uint8, device=dev)
+    d_src, d_dst = to_dev(src_ids.view(np.int32), dev), to_dev(dst_ids.view(np.int32), dev)
+    for l in range(L):
+        sl = slice(l * blocks, (l + 1) * blocks)
+        kvx.pack(src, d_src[sl], blocks, buf, kvx.COPY_TMA if l % 2 else kvx.COPY_SM)
+        kvx.unpack(dst, d_dst[sl], blocks, buf, kvx.COPY_SM if l % 2 else kvx.COPY_TMA)
+    expect = kvx.Pool(pool_pages, pb)
+    kvx.fill_pages(expect, d_dst, t_tags, n, 123, layout, kvx.FILL_BITS)
+    torch.cuda.synchronize()
+    a, b = dst.as_tensor(), expect.as_tensor()
+    idx = d_dst.long()
+    assert torch.equal(a[idx], b[idx])
