@@ -1,0 +1,569 @@
+#!/usr/bin/env python
+"""bench.py — KV migration hot path on B200 (Symphony, arXiv 2412.16434).
+
+Metric (BASELINE.json): "KV migrate GB/s (% HBM/NVLink roofline)".
+`value` = session KV bytes relocated per second, whole job (each byte of the
+session counted once; GB = 1e9 B).
+
+N=1 (config 2, Llama-3.1-8B KV shape @ 8K: 32 layers x 512 pages x 64 KiB =
+1 GiB): one step packs every page of the session (K1, gather by block table
+into the contiguous migration buffer) and unpacks it into a second page
+permutation (K2) — the device half of a layer-wise migration. Inputs are
+1 GiB, larger than the 126 MB L2, so no flush is needed between steps.
+Also reported: the fused page->page mover (K3), the TMA variant, paged decode
+attention (K4) at batch 1/8/64, the end-to-end path through the C ABI with
+pinned HOST buffers (H2D + unpack + pack + D2H, every step), and the CPU
+restatement on the host cores.
+
+N>1 (config 3, Llama-3.1-70B KV shape @ 32K, ~10.7 GB per session): every
+rank owns one session and migrates it to rank (r+1) % N over NVLink with the
+K3 kernel storing straight into the peer's page pool (CUDA IPC) — a
+point-to-point exchange, no collective; weak scaling.
+
+`--impl reference` times the reference's CPU path on the host cores: the
+reference KvStore's migration bookkeeping (oracle/_ref, 1 thread, as the
+reference is single-threaded) plus the payload restatement (oracle/, OpenMP on
+all cores) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV migrate GB/s (% HBM/NVLink roofline)"
+UNIT = "GB/s"
+GB = 1e9
+
+# Shapes.
+CFG_8B = dict(model="llama-3.1-8b-kv", layers=32, kv_heads=8, head_dim=128, block_tokens=16, ctx=8192)
+CFG_70B = dict(model="llama-3.1-70b-kv", layers=80, kv_heads=8, head_dim=128, block_tokens=16, ctx=32768)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+class ClockSampler:
+    """NVML sampler thread: SM clock and clock-event reasons during timing."""
+
+    NAMES = {
+        "nvmlClocksEventReasonGpuIdle": "gpu_idle",
+        "nvmlClocksEventReasonApplicationsClocksSetting": "applications_clocks_setting",
+        "nvmlClocksEventReasonSwPowerCap": "sw_power_cap",
+        "nvmlClocksEventReasonHwSlowdown": "hw_slowdown",
+        "nvmlClocksEventReasonSyncBoost": "sync_boost",
+        "nvmlClocksEventReasonSwThermalSlowdown": "sw_thermal_slowdown",
+        "nvmlClocksEventReasonHwThermalSlowdown": "hw_thermal_slowdown",
+        "nvmlClocksEventReasonHwPowerBrakeSlowdown": "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.01):
+        self.period = period_s
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join()
+
+    def summary(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"], "samples": 0}
+        reasons = [name for attr, name in self.NAMES.items()
+                   if hasattr(self.nv, attr) and self.reasons & getattr(self.nv, attr)]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes from a committed ncu --set full capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def session_pages(cfg):
+    blocks = (cfg["ctx"] + cfg["block_tokens"] - 1) // cfg["block_tokens"]
+    return blocks, cfg["layers"] * blocks
+
+
+def make_session(torch, kvx, np, cfg, seed, dev, pool_pages=None, fill=True):
+    """A pool holding one session's pages at a seeded random permutation."""
+    layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
+    pb = layout.page_bytes()
+    blocks, n = session_pages(cfg)
+    pool_pages = pool_pages or 2 * n
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(pool_pages).astype(np.uint32)
+    src_ids, dst_ids = perm[:n], perm[n:2 * n] if pool_pages >= 2 * n else perm[:n]
+    pool = kvx.Pool(pool_pages, pb, device=dev.index)
+    d_src = torch.from_numpy(src_ids.view(np.int32)).to(dev)
+    d_dst = torch.from_numpy(dst_ids.view(np.int32)).to(dev)
+    if fill:
+        layer = np.repeat(np.arange(cfg["layers"], dtype=np.uint32), blocks)
+        block = np.tile(np.arange(blocks, dtype=np.uint32), cfg["layers"])
+        tags = np.stack([np.full(n, seed & 0xFFFF, np.uint32), layer, block], axis=-1)
+        kvx.fill_pages(pool, d_src, torch.from_numpy(tags.view(np.int32)).to(dev), n, seed, layout,
+                       kvx.FILL_VALUES)
+    return layout, pool, d_src, d_dst, src_ids, dst_ids
+
+
+def time_events(torch, fn, steps, warmup, marks=1):
+    """Runs fn(i, ev_list) steps times after warmup; fn records marks+1 events."""
+    for i in range(warmup):
+        fn(i, None)
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(marks + 1)] for _ in range(steps)]
+    for i in range(steps):
+        fn(i, evs[i])
+    torch.cuda.synchronize()
+    total = evs[0][0].elapsed_time(evs[-1][-1])
+    parts = [[e[j].elapsed_time(e[j + 1]) for e in evs] for j in range(marks)]
+    return total, parts
+
+
+def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
+    cfg = CFG_8B
+    blocks, n = session_pages(cfg)
+    layout, pool, d_src, d_dst, src_ids, dst_ids = make_session(torch, kvx, np, cfg, 1, dev)
+    pb = layout.page_bytes()
+    session_bytes = n * pb
+    buf = torch.empty(session_bytes, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    mode = {"auto": kvx.COPY_AUTO, "sm": kvx.COPY_SM, "tma": kvx.COPY_TMA}[args.copy_mode]
+
+    def step(i, ev, m=mode):
+        if ev:
+            ev[0].record(stream)
+        kvx.pack(pool, d_src, n, buf, m, stream)
+        if ev:
+            ev[1].record(stream)
+        kvx.unpack(pool, d_dst, n, buf, m, stream)
+        if ev:
+            ev[2].record(stream)
+
+    with ClockSampler(dev.index) as clocks:
+        total_ms, (pack_ms, unpack_ms) = time_events(torch, step, args.steps, args.warmup, marks=2)
+    # correctness of what was timed: the last unpack landed every page
+    probe = torch.randint(0, n, (64,), device=dev)
+    pv = pool.as_tensor()
+    assert torch.equal(pv[d_src[probe].long()], pv[d_dst[probe].long()]), "migrated pages differ"
+
+    ms_per_step = total_ms / args.steps
+    value = session_bytes / (ms_per_step * 1e-3) / GB
+    pack_avg, unpack_avg = statistics.mean(pack_ms), statistics.mean(unpack_ms)
+    dom_name, dom_ms = ("kvx_pack", pack_avg) if pack_avg >= unpack_avg else ("kvx_unpack", unpack_avg)
+    achieved = 2 * session_bytes / (dom_ms * 1e-3) / GB  # read + write per launch
+    extra = {
+        "pack_ms": pack_avg, "unpack_ms": unpack_avg,
+        "pack_hbm_gbs": 2 * session_bytes / (pack_avg * 1e-3) / GB,
+        "unpack_hbm_gbs": 2 * session_bytes / (unpack_avg * 1e-3) / GB,
+    }
+
+    # Variants (not the headline): other copy mode, fused page->page K3.
+    other = kvx.COPY_TMA if mode != kvx.COPY_TMA else kvx.COPY_SM
+    _, (p2, u2) = time_events(torch, lambda i, ev: step(i, ev, other), max(5, args.steps // 2), 2, marks=2)
+    extra["alt_mode"] = "tma" if other == kvx.COPY_TMA else "sm"
+    extra["alt_pack_hbm_gbs"] = 2 * session_bytes / (statistics.mean(p2) * 1e-3) / GB
+    extra["alt_unpack_hbm_gbs"] = 2 * session_bytes / (statistics.mean(u2) * 1e-3) / GB
+
+    def fused(i, ev):
+        if ev:
+            ev[0].record(stream)
+        kvx.copy_pages(pool, d_src, pool, d_dst, n, mode, stream)
+        if ev:
+            ev[1].record(stream)
+
+    _, (fz,) = time_events(torch, fused, max(5, args.steps // 2), 2)
+    extra["fused_copy_ms"] = statistics.mean(fz)
+    extra["fused_copy_hbm_gbs"] = 2 * session_bytes / (statistics.mean(fz) * 1e-3) / GB
+    extra["fused_copy_migrate_gbs"] = session_bytes / (statistics.mean(fz) * 1e-3) / GB
+    del buf
+
+    attention = None if args.skip_attention else bench_attention(args, torch, np, kvx, dev, hbm_peak)
+    e2e = None if args.skip_e2e else bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst)
+    launches = 2 * args.steps
+    return dict(value=value, ms_per_step=ms_per_step, extra=extra, clocks=clocks.summary(),
+                roofline={"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": achieved / hbm_peak, "traffic": ncu_traffic(dom_name), "kernel": dom_name,
+                          "algorithmic_bytes_per_launch": 2 * session_bytes, "peak_kind": peak_kind},
+                attention=attention, e2e=e2e, gpu_launches=launches, session_bytes=session_bytes)
+
+
+def bench_attention(args, torch, np, kvx, dev, hbm_peak):
+    """K4 over one layer of Llama-3.1-8B KV at ctx 8192 (GQA 32/8)."""
+    cfg = CFG_8B
+    blocks = cfg["ctx"] // cfg["block_tokens"]
+    layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
+    pb = layout.page_bytes()
+    max_b = 64
+    pages = max_b * blocks
+    rng = np.random.default_rng(3)
+    pool = kvx.Pool(pages, pb, device=dev.index)
+    ids = torch.arange(pages, dtype=torch.int32, device=dev)
+    tags = torch.stack([torch.zeros_like(ids), torch.zeros_like(ids), ids], -1).contiguous()
+    kvx.fill_pages(pool, ids, tags, pages, 5, layout, kvx.FILL_VALUES)
+    perm = torch.from_numpy(rng.permutation(pages).astype(np.int32)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    res = {}
+    for batch in (1, 8, 64):
+        sets = max(1, min(pages // (batch * blocks), -(-256 // (batch * 32))))  # >= 256 MiB rotated > L2
+        tables = [perm[s * batch * blocks:(s + 1) * batch * blocks].view(batch, blocks).contiguous()
+                  for s in range(sets)]
+        ctx = torch.full((batch,), cfg["ctx"], dtype=torch.int32, device=dev)
+        q = (torch.randn(batch, 32, 128, device=dev) * 0.5).to(torch.bfloat16)
+        out = torch.empty(batch, 32, 128, dtype=torch.float32, device=dev)
+        att = kvx.Attention(layout, 32, blocks)
+        wsb = att.workspace_bytes(batch, cfg["ctx"])
+        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+
+        def run(i, ev):
+            if ev:
+                ev[0].record(stream)
+            att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws, stream)
+            if ev:
+                ev[1].record(stream)
+
+        steps = max(10, args.steps)
+        _, (ms,) = time_events(torch, run, steps, 3)
+        t = statistics.mean(ms)
+        kv_bytes = batch * cfg["ctx"] * 2 * cfg["kv_heads"] * cfg["head_dim"] * 2
+        gbs = kv_bytes / (t * 1e-3) / GB
+        res[f"batch{batch}"] = {"ms_per_layer": t, "hbm_gbs": gbs, "frac": gbs / hbm_peak,
+                                "kv_bytes": kv_bytes, "rotating_sets": sets}
+    return res
+
+
+def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):
+    """Through the C ABI with pinned HOST buffers: per layer H2D (HOST tier copy
+    -> staging) + unpack (K2, LoadH2D landing) + pack (K1, offload gather) +
+    D2H (-> HOST tier). Copy streams overlap the two PCIe directions."""
+    blocks, n = session_pages(cfg)
+    pb = layout.page_bytes()
+    lb = blocks * pb
+    L = cfg["layers"]
+    h_in = torch.empty(L * lb, dtype=torch.uint8).pin_memory()
+    h_in.view(torch.int64).random_()
+    h_out = torch.empty_like(h_in).pin_memory()
+    stage_in = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    stage_out = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    s_in, s_c, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+
+    def step():
+        e_in = [torch.cuda.Event() for _ in range(L)]
+        e_c = [torch.cuda.Event() for _ in range(L)]
+        e_out = [torch.cuda.Event() for _ in range(L)]
+        s_in.wait_stream(main)
+        for l in range(L):
+            with torch.cuda.stream(s_in):
+                if l >= 2:
+                    s_in.wait_event(e_c[l - 2])
+                stage_in[l % 2].copy_(h_in[l * lb:(l + 1) * lb], non_blocking=True)
+                e_in[l].record(s_in)
+            s_c.wait_event(e_in[l])
+            if l >= 2:
+                s_c.wait_event(e_out[l - 2])
+            ids = d_dst[l * blocks:(l + 1) * blocks]
+            kvx.unpack(pool, ids, blocks, stage_in[l % 2], kvx.COPY_AUTO, s_c)
+            kvx.pack(pool, ids, blocks, stage_out[l % 2], kvx.COPY_AUTO, s_c)
+            e_c[l].record(s_c)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(e_c[l])
+                h_out[l * lb:(l + 1) * lb].copy_(stage_out[l % 2], non_blocking=True)
+                e_out[l].record(s_out)
+        main.wait_stream(s_out)
+
+    steps = max(3, min(args.steps, 10))
+    for _ in range(max(1, min(args.warmup, 3))):
+        step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(main)
+    for _ in range(steps):
+        step()
+    t1.record(main)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    assert torch.equal(h_in, h_out), "end-to-end roundtrip differs"
+    return {"value": (L * lb) / (ms * 1e-3) / GB, "unit": UNIT, "h2d_bytes_per_step": L * lb,
+            "d2h_bytes_per_step": L * lb, "ms_per_step": ms, "steps": steps,
+            "path": "pinned HOST -> H2D -> kvx_unpack -> kvx_pack -> D2H -> pinned HOST, per layer, 3 streams"}
+
+
+def bench_multi(args, torch, np, kvx, dev, rank, world):
+    """Ring migration of one 70B@32K session per rank to rank+1 over NVLink."""
+    import torch.distributed as dist
+    cfg = CFG_70B
+    blocks, n = session_pages(cfg)
+    layout, pool, d_src, d_dst, _, _ = make_session(torch, kvx, np, cfg, 100 + rank, dev)
+    pb = layout.page_bytes()
+    handle = pool.ipc_export()
+    handles = [None] * world
+    dist.all_gather_object(handles, (handle, pool.num_pages, torch.cuda.get_device_properties(dev).uuid.hex
+                                     if hasattr(torch.cuda.get_device_properties(dev), "uuid") else ""))
+    nxt = (rank + 1) % world
+    peer = kvx.Pool.ipc_open(handles[nxt][0], handles[nxt][1], pb, dev.index)
+    stream = torch.cuda.current_stream(dev)
+    mode = {"auto": kvx.COPY_AUTO, "sm": kvx.COPY_SM, "tma": kvx.COPY_TMA}[args.copy_mode]
+    # receiver-side destinations: the peer's second half (its own dst ids are
+    # the same permutation recipe, seeded by the peer's rank)
+    rng = np.random.default_rng(100 + nxt)
+    perm = rng.permutation(2 * n).astype(np.uint32)
+    d_peer_dst = torch.from_numpy(perm[n:2 * n].view(np.int32)).to(dev)
+
+    def step(i, ev):
+        if ev:
+            ev[0].record(stream)
+        kvx.copy_pages(pool, d_src, peer, d_peer_dst, n, mode, stream)
+        if ev:
+            ev[1].record(stream)
+
+    for _ in range(args.warmup):
+        step(0, None)
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(dev.index) as clocks:
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+        for i in range(args.steps):
+            step(i, evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([start.elapsed_time(end)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()  # peers finished writing before anyone reads / frees
+    ms_per_step = ms.item() / args.steps
+    session_bytes = n * pb
+    value = world * session_bytes / (ms_per_step * 1e-3) / GB
+    kern = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    achieved = session_bytes / (kern * 1e-3) / GB
+    peer.close()
+    return dict(value=value, ms_per_step=ms_per_step, clocks=clocks.summary(), session_bytes=session_bytes,
+                roofline={"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                          "frac": achieved / NVLINK_PEAK_GBS, "traffic": None, "kernel": "kvx_copy_pages(peer)",
+                          "algorithmic_bytes_per_launch": session_bytes, "peak_kind": "measured peer copy"},
+                gpu_launches=args.steps)
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle; test infrastructure only, used here as the reported baseline)
+
+
+def cpu_migrate(np, cfg, seconds_budget, layers=None, repeat_min=1):
+    """Payload restatement pack+unpack (OpenMP, all host threads)."""
+    import oracle.oracle as O
+    blocks, n = session_pages(cfg)
+    L = layers or cfg["layers"]
+    n = L * blocks
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    rng = np.random.default_rng(7)
+    perm = rng.permutation(2 * n).astype(np.uint32)
+    pool = np.zeros((2 * n, pb), np.uint8)
+    buf = np.empty(n * pb, np.uint8)
+    lay = O.Layout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], 1)
+    tags = O.tags_array(0, np.repeat(np.arange(L), blocks), np.tile(np.arange(blocks), L))
+    O.fill_pages(pool, pb, perm[:n], tags, 1, lay, 0)
+    reps, t_total = 0, 0.0
+    while reps < repeat_min or t_total < seconds_budget:
+        t0 = time.perf_counter()
+        O.pack(pool, pb, perm[:n], buf)
+        O.unpack(pool, pb, perm[n:2 * n], buf)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    assert np.array_equal(pool[perm[n]], pool[perm[0]])
+    return n * pb * reps / t_total / GB, O.threads(), f"{L} layers x {blocks} pages x {pb} B, {reps} reps"
+
+
+def reference_state_ops(np):
+    """The reference KvStore's bookkeeping for one migrated 8B@8K session."""
+    from paper_2412_16434_b200 import kvstore as K
+    import oracle.oracle as O
+    if not O.REF_KVS_LIB.exists():
+        return None
+    cfg = CFG_8B
+    gpu = K.GpuProfile(kv_bytes_per_token=cfg["layers"] * 4096, num_layers=cfg["layers"],
+                       hbm_capacity=180_000_000_000)
+    st = K.KvStore(gpu=gpu, lib=str(O.REF_KVS_LIB))
+    st.register_session(0, "s0")
+    st.finalize_sessions()
+    t0 = time.perf_counter()
+    sched = st.import_migration(0, cfg["ctx"], 0)
+    for tid, at in sorted(sched, key=lambda t: (t[1], t[0])):
+        st.apply_transfer(tid, at)
+    st.release_session(0, 0)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    import numpy as np
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return 0
+    cfg = CFG_8B if world == 1 else CFG_70B
+    import oracle.oracle as O
+    O.build_payload()
+    blocks, n = session_pages(cfg)
+    layers = cfg["layers"] if world == 1 else 8  # 70B: bounded sample of 8 layers (2.7 GB)
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    nb = layers * blocks
+    rng = np.random.default_rng(7)
+    perm = rng.permutation(2 * nb).astype(np.uint32)
+    pool = np.zeros((2 * nb, pb), np.uint8)
+    buf = np.empty(nb * pb, np.uint8)
+    lay = O.Layout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], 1)
+    O.fill_pages(pool, pb, perm[:nb], O.tags_array(0, np.repeat(np.arange(layers), blocks),
+                                                   np.tile(np.arange(blocks), layers)), 1, lay, 0)
+    state_s = 0.0
+
+    def step():
+        nonlocal state_s
+        s = reference_state_ops(np)
+        state_s += s or 0.0
+        O.pack(pool, pb, perm[:nb], buf)
+        O.unpack(pool, pb, perm[nb:2 * nb], buf)
+
+    for _ in range(args.warmup):
+        step()
+    state_s = 0.0
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = nb * pb * args.steps / dt / GB
+    threads = O.threads()
+    sample = (f"{layers} of {cfg['layers']} layers x {blocks} pages x {pb} B per step: reference KvStore "
+              f"import_migration+apply+release (oracle/_ref, 1 thread, {1e3 * state_s / args.steps:.2f} ms/step) "
+              f"+ payload pack/unpack restatement (OpenMP {threads} threads)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{cfg['model']} @{cfg['ctx']} session migration (CPU)", "seq_len": cfg["ctx"],
+                       "layers": cfg["layers"], "parallelism": f"replicas{world}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--copy-mode", default="auto", choices=["auto", "sm", "tma"])
+    ap.add_argument("--skip-attention", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    from paper_2412_16434_b200 import kvx
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    kvx.lib()
+    hbm_peak, peak_kind = load_peaks()
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        res = bench_multi(args, torch, np, kvx, dev, rank, world)
+        cfg = CFG_70B
+        workload = "llama-3.1-70b-kv @32K session ring migration over NVLink (kvx_copy_pages into peer pool)"
+    else:
+        res = bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind)
+        cfg = CFG_8B
+        workload = "llama-3.1-8b-kv @8K session: kvx_pack all pages + kvx_unpack into a second permutation"
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": workload, "model_shape": cfg["model"], "seq_len": cfg["ctx"],
+                           "layers": cfg["layers"], "kv_heads": cfg["kv_heads"], "head_dim": cfg["head_dim"],
+                           "kv_dtype": "bf16", "page_bytes": 2 * cfg["kv_heads"] * 16 * cfg["head_dim"] * 2,
+                           "session_bytes": res["session_bytes"],
+                           "parallelism": "single" if world == 1 else f"ring-p2p{world}",
+                           "l2": "inputs (1 GiB / 10.7 GB per step) larger than the 126 MB L2; no flush"},
+                "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["gpu_launches"]}
+        if world == 1:
+            line["e2e"] = res["e2e"]
+            line["decode_attention"] = res["attention"]
+            line["detail"] = res["extra"]
+            if not args.skip_cpu:
+                v, cores, sample = cpu_migrate(np, cfg, 8.0, layers=8, repeat_min=3)
+                line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                        "sample": f"oracle pack+unpack, {sample}"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

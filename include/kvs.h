@@ -207,6 +207,49 @@ int kvs_kv_bytes_per_layer(int64_t tokens, const kvs_gpu_profile* gpu, int64_t* 
  * (1 << Tier) of one block. */
 int kvs_residency(kvs_store* s, uint32_t session, uint16_t layer, uint32_t block, uint8_t* out);
 
+/* ---- Physical payload (product build only; KVS_ERR_UNSUPPORTED in the
+ * oracle build). A payload node gives a store's tier copies real pages
+ * (include/symsim/payload.hpp): attach one per store, drive the store as
+ * usual, read any block copy back for verification. --------------------- */
+typedef struct kvs_cluster kvs_cluster;
+typedef struct kvs_payload kvs_payload;
+
+typedef struct {
+  int32_t device;
+  int32_t num_kv_heads;
+  int32_t head_dim;
+  int32_t block_tokens;
+  int32_t dtype; /* KVX_DTYPE_* */
+  int32_t fill_mode;
+  uint64_t device_pages;
+  uint64_t host_pages;
+  uint64_t landing_pages;
+  uint64_t disk_pages;
+  uint64_t seed;
+} kvs_payload_options;
+
+int kvs_cluster_create(kvs_cluster** out);
+void kvs_cluster_destroy(kvs_cluster* c);
+int kvs_payload_create(kvs_cluster* c, int32_t node_id, const kvs_payload_options* opts, kvs_payload** out);
+void kvs_payload_destroy(kvs_payload* p);
+/* Attach (or detach with NULL) a payload node to a store. */
+int kvs_attach_payload(kvs_store* s, kvs_payload* p);
+/* Copies one block's `tier` copy to host memory (page_bytes); KVS_ERR_LOGIC
+ * when the node holds no such copy. */
+int kvs_payload_read_block(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t block, int32_t tier,
+                           void* out);
+/* pool: 0 device, 1 pinned host, 2 landing (HBM), 3 disk. */
+int kvs_payload_pages_in_use(kvs_payload* p, int32_t pool, uint64_t* out);
+int kvs_payload_pool_of(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t block, int32_t tier,
+                        int32_t* out);
+int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7);
+/* Process-wide default: every KvStore constructed afterwards gets a payload
+ * node (node_id -> device node_id % num_devices) in cluster `c`, built from
+ * `tmpl`. Lets unchanged caller stacks (the reference Simulation) run with
+ * real pages. NULL clears it. Nodes are owned by the cluster. */
+int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices);
+int kvs_cluster_node(kvs_cluster* c, int32_t node_id, kvs_payload** out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,7 +58,7 @@ extern "C" {
 #define KVX_FILL_BITS 0   /* page = splitmix64 words                       */
 #define KVX_FILL_VALUES 1 /* page = dtype values uniform on [-sqrt3,sqrt3) */
 
-#define KVX_COPY_AUTO 0   /* library picks (currently KVX_COPY_SM)            */
+#define KVX_COPY_AUTO 0   /* TMA for local HBM<->HBM, SM for peer/host pools */
 #define KVX_COPY_SM 1     /* SM kernel, 16-B vector loads/stores             */
 #define KVX_COPY_TMA 2    /* SM kernel, cp.async.bulk (TMA) through smem     */
 #define KVX_COPY_CE 3     /* copy engines (cudaMemcpyBatchAsync); host ids   */
@@ -108,6 +108,19 @@ int kvx_pool_ipc_export(const kvx_pool* pool, void* handle64);
 int kvx_pool_ipc_open(int device, const void* handle64, uint64_t num_pages, uint64_t page_bytes,
                       kvx_pool** out);
 int kvx_enable_peer_access(int device, int peer);
+
+/* ---- runtime helpers for C++/FFI hosts ------------------------------------
+ * Thin wrappers so host code (libsymsim_b200's payload backend, cgo/JNI
+ * callers) needs no CUDA headers or runtime of its own. */
+int kvx_stream_create(int device, void** out);
+int kvx_stream_destroy(void* stream);
+int kvx_stream_synchronize(void* stream);
+int kvx_malloc(int device, uint64_t bytes, void** out);
+int kvx_free(void* ptr);
+/* cudaMemcpyAsync(kind = Default) on `stream`. */
+int kvx_memcpy_async(void* dst, const void* src, uint64_t bytes, void* stream);
+/* Synchronous copy of one page to host memory (verification / debugging). */
+int kvx_read_page(const kvx_pool* pool, uint64_t page, void* host_out);
 
 /* ---- page movement (K1-K3) ---------------------------------------------- */
 /* dst[i * page_bytes ...] = page(ids[i]) for i < n. ids in device memory. */

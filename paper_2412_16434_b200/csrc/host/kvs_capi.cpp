@@ -390,4 +390,139 @@ int kvs_residency(kvs_store* s, uint32_t session, uint16_t layer, uint32_t block
 #endif
 }
 
+// ---- payload (product only) ----------------------------------------------
+
+#ifdef KVS_PRODUCT
 }  // extern "C"
+
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "symsim/payload.hpp"
+
+struct kvs_cluster {
+  symsim::PayloadCluster cluster;
+  std::map<int, std::unique_ptr<symsim::NodePayload>> owned;
+  std::mutex mu;
+};
+struct kvs_payload {
+  symsim::NodePayload* node;
+  bool owned;
+};
+
+namespace {
+symsim::PayloadOptions to_payload_opts(const kvs_payload_options* o) {
+  symsim::PayloadOptions p;
+  p.device = o->device;
+  p.layout = kvx_page_layout{o->num_kv_heads, o->head_dim, o->block_tokens, o->dtype};
+  p.fill_mode = o->fill_mode;
+  p.device_pages = o->device_pages;
+  p.host_pages = o->host_pages;
+  p.landing_pages = o->landing_pages;
+  p.disk_pages = o->disk_pages;
+  p.seed = o->seed;
+  return p;
+}
+std::map<const symsim::NodePayload*, kvs_payload> g_handles;
+}  // namespace
+
+extern "C" {
+
+int kvs_cluster_create(kvs_cluster** out) {
+  return guarded([&] { *out = new kvs_cluster; });
+}
+void kvs_cluster_destroy(kvs_cluster* c) { delete c; }
+
+int kvs_payload_create(kvs_cluster* c, int32_t node_id, const kvs_payload_options* opts, kvs_payload** out) {
+  return guarded([&] {
+    auto* node = new symsim::NodePayload(c ? &c->cluster : nullptr, node_id, to_payload_opts(opts));
+    *out = new kvs_payload{node, true};
+  });
+}
+
+void kvs_payload_destroy(kvs_payload* p) {
+  if (!p) return;
+  if (p->owned) delete p->node;
+  delete p;
+}
+
+int kvs_attach_payload(kvs_store* s, kvs_payload* p) {
+  return guarded([&] { s->store.attach_backend(p ? p->node : nullptr); });
+}
+
+int kvs_payload_read_block(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t block, int32_t tier,
+                           void* out) {
+  return guarded([&] {
+    if (!p->node->read_block(session, layer, block, static_cast<symsim::Tier>(tier), out))
+      throw std::logic_error("payload: no copy of that block in that tier");
+  });
+}
+
+int kvs_payload_pages_in_use(kvs_payload* p, int32_t pool, uint64_t* out) {
+  return guarded([&] {
+    if (pool < 0 || pool > 3) throw std::logic_error("payload: pool index out of range");
+    *out = p->node->pages_in_use(static_cast<symsim::NodePayload::Pool>(pool));
+  });
+}
+
+int kvs_payload_pool_of(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t block, int32_t tier,
+                        int32_t* out) {
+  return guarded([&] { *out = p->node->pool_of(session, layer, block, static_cast<symsim::Tier>(tier)); });
+}
+
+int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7) {
+  return guarded([&] {
+    for (int i = 0; i < 7; ++i) out7[i] = p->node->bytes_moved()[i];
+  });
+}
+
+int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices) {
+  return guarded([&] {
+    if (!c || !tmpl) {
+      symsim::set_default_tier_backend_factory({});
+      return;
+    }
+    const symsim::PayloadOptions base = to_payload_opts(tmpl);
+    const int devices = num_devices > 0 ? num_devices : 1;
+    symsim::set_default_tier_backend_factory([c, base, devices](int node_id) -> symsim::TierBackend* {
+      std::lock_guard<std::mutex> lock(c->mu);
+      auto& slot = c->owned[node_id];
+      if (!slot) {
+        symsim::PayloadOptions o = base;
+        o.device = node_id % devices;
+        slot = std::make_unique<symsim::NodePayload>(&c->cluster, node_id, o);
+      }
+      return slot.get();
+    });
+  });
+}
+
+int kvs_cluster_node(kvs_cluster* c, int32_t node_id, kvs_payload** out) {
+  return guarded([&] {
+    symsim::NodePayload* n = c->cluster.node(node_id);
+    if (!n) throw std::logic_error("payload: no such node");
+    *out = new kvs_payload{n, false};
+  });
+}
+
+}  // extern "C"
+#else
+#define KVS_NO_PAYLOAD(name, ...)                                        \
+  int name(__VA_ARGS__) {                                                \
+    g_last_error = #name ": not available in the oracle build";         \
+    return KVS_ERR_UNSUPPORTED;                                          \
+  }
+KVS_NO_PAYLOAD(kvs_cluster_create, kvs_cluster**)
+void kvs_cluster_destroy(kvs_cluster*) {}
+KVS_NO_PAYLOAD(kvs_payload_create, kvs_cluster*, int32_t, const kvs_payload_options*, kvs_payload**)
+void kvs_payload_destroy(kvs_payload*) {}
+KVS_NO_PAYLOAD(kvs_attach_payload, kvs_store*, kvs_payload*)
+KVS_NO_PAYLOAD(kvs_payload_read_block, kvs_payload*, uint32_t, uint16_t, uint32_t, int32_t, void*)
+KVS_NO_PAYLOAD(kvs_payload_pages_in_use, kvs_payload*, int32_t, uint64_t*)
+KVS_NO_PAYLOAD(kvs_payload_pool_of, kvs_payload*, uint32_t, uint16_t, uint32_t, int32_t, int32_t*)
+KVS_NO_PAYLOAD(kvs_payload_bytes_moved, kvs_payload*, uint64_t*)
+KVS_NO_PAYLOAD(kvs_set_default_payload, kvs_cluster*, const kvs_payload_options*, int32_t)
+KVS_NO_PAYLOAD(kvs_cluster_node, kvs_cluster*, int32_t, kvs_payload**)
+}  // extern "C"
+#endif

@@ -1,0 +1,258 @@
+// NodePayload: physical pages behind KvStore's tier residency (lockstep).
+// See include/symsim/payload.hpp for the tier -> pool mapping. All CUDA work
+// goes through the kvx C ABI (include/kvx.h); this file has no CUDA headers.
+//
+// Reference anchors for when each copy comes into existence (the hooks fire
+// from the re-implemented state machine at exactly these points):
+//   Created      append_blocks            kvstore.cpp:221-228
+//   HostCopy     write-behind landing     kvstore.cpp:867-880
+//   DiskWrite    persist landing          kvstore.cpp:881-900
+//   SwapOut      offload / purge flush    kvstore.cpp:901-913
+//   LoadDiskHost disk stage landing       kvstore.cpp:862-866
+//   LoadH2D      demand / prefetch load   kvstore.cpp:852-861
+//   NetArrive    migration layer landing  kvstore.cpp:914-923
+//   tier_lost    purge / evict / release  kvstore.cpp:388-393, 293-295, 710-736
+
+#include "symsim/payload.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+namespace symsim {
+
+namespace {
+
+void kvx_check(int rc, const char* what) {
+  if (rc != KVX_OK) throw std::runtime_error(std::string("payload: ") + what + ": " + kvx_last_error());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// cluster registry
+
+void PayloadCluster::add(NodePayload* node) { nodes_[node->node_id()] = node; }
+
+NodePayload* PayloadCluster::node(int id) const {
+  const auto it = nodes_.find(id);
+  return it == nodes_.end() ? nullptr : it->second;
+}
+
+void PayloadCluster::note_source(std::uint32_t session, int node) { sources_[session] = node; }
+
+int PayloadCluster::take_source(std::uint32_t session) {
+  const auto it = sources_.find(session);
+  if (it == sources_.end()) return -1;
+  const int n = it->second;
+  sources_.erase(it);
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// node
+
+NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOptions& opts)
+    : cluster_(cluster), node_(node_id), opts_(opts) {
+  page_bytes_ = kvx_page_bytes(&opts_.layout);
+  if (page_bytes_ == 0) throw std::runtime_error("payload: empty page layout");
+  kvx_check(kvx_stream_create(opts_.device, &stream_), "stream");
+  const std::uint64_t counts[4] = {opts_.device_pages, opts_.host_pages, opts_.landing_pages, opts_.disk_pages};
+  for (int p = 0; p < 4; ++p) {
+    if (counts[p] == 0) continue;
+    if (p == kDevicePool || p == kLandingPool)
+      kvx_check(kvx_pool_create(opts_.device, counts[p], page_bytes_, &pools_[p]), "device pool");
+    else
+      kvx_check(kvx_pool_create_host(counts[p], page_bytes_, &pools_[p]), "host pool");
+    free_[p].resize(counts[p]);
+    // LIFO free list handing out low page ids first.
+    for (std::uint64_t i = 0; i < counts[p]; ++i) free_[p][i] = static_cast<std::uint32_t>(counts[p] - 1 - i);
+  }
+  if (cluster_) cluster_->add(this);
+}
+
+NodePayload::~NodePayload() {
+  if (stream_) kvx_stream_synchronize(stream_);
+  for (auto*& p : pools_)
+    if (p) kvx_pool_destroy(p);
+  for (auto* d : d_ids_) kvx_free(d);
+  kvx_free(d_tags_);
+  kvx_stream_destroy(stream_);
+}
+
+std::uint64_t NodePayload::pages_in_use(Pool p) const {
+  const std::uint64_t total = pools_[p] ? kvx_pool_num_pages(pools_[p]) : 0;
+  return total - free_[p].size();
+}
+
+std::uint32_t NodePayload::alloc(Pool p) {
+  if (free_[p].empty()) {
+    static const char* const kNames[] = {"device", "host", "landing", "disk"};
+    throw std::runtime_error(std::string("payload: node ") + std::to_string(node_) + " " + kNames[p] +
+                             " pool exhausted");
+  }
+  const std::uint32_t page = free_[p].back();
+  free_[p].pop_back();
+  return page;
+}
+
+void NodePayload::release(const Ref& r) {
+  if (r.pool >= 0) free_[r.pool].push_back(r.page);
+}
+
+std::uint32_t* NodePayload::device_ids(const std::vector<std::uint32_t>& ids, int slot) {
+  if (ids.size() > d_ids_cap_[slot]) {
+    kvx_free(d_ids_[slot]);
+    d_ids_[slot] = nullptr;
+    const std::size_t cap = std::max<std::size_t>(ids.size(), 4096);
+    void* p = nullptr;
+    kvx_check(kvx_malloc(opts_.device, cap * sizeof(std::uint32_t), &p), "id scratch");
+    d_ids_[slot] = static_cast<std::uint32_t*>(p);
+    d_ids_cap_[slot] = cap;
+  }
+  kvx_check(kvx_memcpy_async(d_ids_[slot], ids.data(), ids.size() * sizeof(std::uint32_t), stream_), "ids upload");
+  return d_ids_[slot];
+}
+
+// Best existing copy of a block on this node, fastest tier first, skipping
+// `exclude_tier` (the tier being created).
+NodePayload::Ref NodePayload::best_source(std::uint32_t s, std::uint16_t l, std::uint32_t b,
+                                          int exclude_tier) const {
+  const auto it = blocks_.find(key(s, l, b));
+  if (it == blocks_.end()) return Ref{};
+  for (int t = 0; t < 3; ++t)
+    if (t != exclude_tier && it->second.tier[t].pool >= 0) return it->second.tier[t];
+  return Ref{};
+}
+
+int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier tier) const {
+  const auto it = blocks_.find(key(s, l, b));
+  return it == blocks_.end() ? -1 : it->second.tier[static_cast<int>(tier)].pool;
+}
+
+// Copies src[i] -> dst[i] (dst all in this node's pools), grouped by
+// (source pool, destination pool). Device-resident pairs use the SM/TMA page
+// mover; anything touching pinned host memory uses the copy engines.
+// `src_node` owns the source pools; with push_from_source the kernel runs on
+// the source node's stream and stores into this node's memory (NVLink / peer
+// path of a migration).
+void NodePayload::move(std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node,
+                       bool push_from_source) {
+  for (int sp = 0; sp < 4; ++sp)
+    for (int dp = 0; dp < 4; ++dp) {
+      std::vector<std::uint32_t> s_ids, d_ids;
+      for (std::size_t i = 0; i < src.size(); ++i)
+        if (src[i].pool == sp && dst[i].pool == dp) {
+          s_ids.push_back(src[i].page);
+          d_ids.push_back(dst[i].page);
+        }
+      if (s_ids.empty()) continue;
+      kvx_pool* from = src_node.pools_[sp];
+      kvx_pool* to = pools_[dp];
+      const bool on_device = (sp == kDevicePool || sp == kLandingPool) && (dp == kDevicePool || dp == kLandingPool);
+      NodePayload& runner = push_from_source ? src_node : *this;
+      if (on_device) {
+        const std::uint32_t* ds = runner.device_ids(s_ids, 0);
+        const std::uint32_t* dd = runner.device_ids(d_ids, 1);
+        kvx_check(kvx_copy_pages(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO, runner.stream_), "page copy");
+      } else {
+        kvx_check(kvx_copy_pages(from, s_ids.data(), to, d_ids.data(), s_ids.size(), KVX_COPY_CE, runner.stream_),
+                  "copy-engine copy");
+      }
+      kvx_check(kvx_stream_synchronize(runner.stream_), "sync");
+    }
+}
+
+void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
+                              const std::vector<std::uint32_t>& blocks) {
+  const int t = static_cast<int>(tier);
+  moved_[static_cast<int>(why)] += blocks.size() * page_bytes_;
+
+  if (why == BlockEvent::Created) {
+    std::vector<std::uint32_t> pages;
+    std::vector<kvx_block_tag> tags;
+    for (std::uint32_t b : blocks) {
+      Copies& c = blocks_[key(session, layer, b)];
+      release(c.tier[t]);
+      c.tier[t] = Ref{kDevicePool, alloc(kDevicePool)};
+      pages.push_back(c.tier[t].page);
+      tags.push_back(kvx_block_tag{session, layer, b});
+    }
+    const std::uint32_t* d_pages = device_ids(pages, 0);
+    if (tags.size() * sizeof(kvx_block_tag) > d_tags_cap_) {
+      kvx_free(d_tags_);
+      d_tags_cap_ = std::max<std::size_t>(tags.size() * sizeof(kvx_block_tag), 65536);
+      kvx_check(kvx_malloc(opts_.device, d_tags_cap_, &d_tags_), "tag scratch");
+    }
+    kvx_check(kvx_memcpy_async(d_tags_, tags.data(), tags.size() * sizeof(kvx_block_tag), stream_), "tags upload");
+    kvx_check(kvx_fill_pages(pools_[kDevicePool], d_pages, static_cast<const kvx_block_tag*>(d_tags_), pages.size(),
+                             opts_.seed, &opts_.layout, opts_.fill_mode, stream_),
+              "fill");
+    kvx_check(kvx_stream_synchronize(stream_), "sync");
+    return;
+  }
+
+  // Where the new copy lives, and where its bytes come from.
+  Pool dest = kDevicePool;
+  NodePayload* src_node = this;
+  bool push = false;
+  if (tier == Tier::Host) dest = why == BlockEvent::NetArrive ? kLandingPool : kHostPool;
+  if (tier == Tier::Disk) dest = kDiskPool;
+  if (why == BlockEvent::NetArrive) {
+    const auto it = import_src_.find(session);
+    if (it == import_src_.end() || !cluster_ || !cluster_->node(it->second))
+      throw std::runtime_error("payload: migration layer arrived with no known source node");
+    src_node = cluster_->node(it->second);
+    push = true;
+  }
+
+  std::vector<Ref> src, dst;
+  for (std::uint32_t b : blocks) {
+    const Ref from = src_node->best_source(session, layer, b, src_node == this ? t : -1);
+    if (from.pool < 0)
+      throw std::runtime_error("payload: no source copy for session " + std::to_string(session) + " layer " +
+                               std::to_string(layer) + " block " + std::to_string(b) + " (" +
+                               block_event_name(why) + ")");
+    Copies& c = blocks_[key(session, layer, b)];
+    release(c.tier[t]);
+    c.tier[t] = Ref{static_cast<std::int8_t>(dest), alloc(dest)};
+    src.push_back(from);
+    dst.push_back(c.tier[t]);
+  }
+  move(src, dst, *src_node, push);
+}
+
+void NodePayload::tier_lost(std::uint32_t session, std::uint16_t layer, Tier tier,
+                            const std::vector<std::uint32_t>& blocks) {
+  const int t = static_cast<int>(tier);
+  for (std::uint32_t b : blocks) {
+    const auto it = blocks_.find(key(session, layer, b));
+    if (it == blocks_.end()) continue;
+    release(it->second.tier[t]);
+    it->second.tier[t] = Ref{};
+    const Copies& c = it->second;
+    if (c.tier[0].pool < 0 && c.tier[1].pool < 0 && c.tier[2].pool < 0) blocks_.erase(it);
+  }
+}
+
+void NodePayload::migrating_out(std::uint32_t session) {
+  if (cluster_) cluster_->note_source(session, node_);
+}
+
+void NodePayload::importing(std::uint32_t session, std::int64_t /*tokens*/) {
+  const int src = cluster_ ? cluster_->take_source(session) : -1;
+  if (src >= 0) import_src_[session] = src;
+  if (src >= 0 && cluster_->node(src) && cluster_->node(src)->device() != opts_.device)
+    kvx_check(kvx_enable_peer_access(cluster_->node(src)->device(), opts_.device), "peer access");
+}
+
+bool NodePayload::read_block(std::uint32_t session, std::uint16_t layer, std::uint32_t block, Tier tier, void* out) {
+  const auto it = blocks_.find(key(session, layer, block));
+  if (it == blocks_.end()) return false;
+  const Ref r = it->second.tier[static_cast<int>(tier)];
+  if (r.pool < 0) return false;
+  kvx_check(kvx_read_page(pools_[r.pool], r.page, out), "read page");
+  return true;
+}
+
+}  // namespace symsim

@@ -177,3 +177,60 @@ int kvx_enable_peer_access(int device, int peer) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int kvx_stream_create(int device, void** out) {
+  if (!out) return kvx::fail_arg("kvx_stream_create: null out");
+  int prev = 0;
+  KVX_CUDA_TRY(cudaGetDevice(&prev), "kvx_stream_create: cudaGetDevice");
+  KVX_CUDA_TRY(cudaSetDevice(device), "kvx_stream_create: cudaSetDevice");
+  cudaStream_t s = nullptr;
+  const cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return kvx::fail_cuda(e, "kvx_stream_create");
+  *out = s;
+  return KVX_OK;
+}
+
+int kvx_stream_destroy(void* stream) {
+  if (stream) KVX_CUDA_TRY(cudaStreamDestroy(static_cast<cudaStream_t>(stream)), "kvx_stream_destroy");
+  return KVX_OK;
+}
+
+int kvx_stream_synchronize(void* stream) {
+  KVX_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "kvx_stream_synchronize");
+  return KVX_OK;
+}
+
+int kvx_malloc(int device, uint64_t bytes, void** out) {
+  if (!out) return kvx::fail_arg("kvx_malloc: null out");
+  int prev = 0;
+  KVX_CUDA_TRY(cudaGetDevice(&prev), "kvx_malloc: cudaGetDevice");
+  KVX_CUDA_TRY(cudaSetDevice(device), "kvx_malloc: cudaSetDevice");
+  const cudaError_t e = cudaMalloc(out, bytes ? bytes : 1);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return kvx::fail_cuda(e, "kvx_malloc");
+  return KVX_OK;
+}
+
+int kvx_free(void* ptr) {
+  if (ptr) KVX_CUDA_TRY(cudaFree(ptr), "kvx_free");
+  return KVX_OK;
+}
+
+int kvx_memcpy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
+  if (bytes == 0) return KVX_OK;
+  KVX_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)),
+               "kvx_memcpy_async");
+  return KVX_OK;
+}
+
+int kvx_read_page(const kvx_pool* pool, uint64_t page, void* host_out) {
+  if (!pool || !host_out || page >= pool->num_pages) return kvx::fail_arg("kvx_read_page: bad page");
+  KVX_CUDA_TRY(cudaMemcpy(host_out, pool->base + page * pool->page_bytes, pool->page_bytes, cudaMemcpyDefault),
+               "kvx_read_page");
+  return KVX_OK;
+}
+
+}  // extern "C"
