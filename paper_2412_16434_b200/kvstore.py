@@ -108,6 +108,13 @@ class _Meta(C.Structure):
                 ("pinned", C.c_int32), ("pad_", C.c_int32)]
 
 
+class _PayloadOpts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("block_tokens", C.c_int32), ("dtype", C.c_int32), ("fill_mode", C.c_int32),
+                ("device_pages", C.c_uint64), ("host_pages", C.c_uint64), ("landing_pages", C.c_uint64),
+                ("disk_pages", C.c_uint64), ("seed", C.c_uint64)]
+
+
 @dataclass
 class GpuProfile:
     """reference costmodel.hpp:17-27 (same defaults)."""
@@ -254,6 +261,17 @@ def load_kvs_library(path: Optional[str] = None) -> C.CDLL:
         "kvs_prefill_time": ([C.c_int64, P(_Gpu), P(C.c_int64)], C.c_int),
         "kvs_kv_bytes_per_layer": ([C.c_int64, P(_Gpu), P(C.c_int64)], C.c_int),
         "kvs_residency": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, P(C.c_uint8)], C.c_int),
+        "kvs_cluster_create": ([P(C.c_void_p)], C.c_int),
+        "kvs_cluster_destroy": ([C.c_void_p], None),
+        "kvs_payload_create": ([C.c_void_p, C.c_int32, P(_PayloadOpts), P(C.c_void_p)], C.c_int),
+        "kvs_payload_destroy": ([C.c_void_p], None),
+        "kvs_attach_payload": ([C.c_void_p, C.c_void_p], C.c_int),
+        "kvs_payload_read_block": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, C.c_int32, C.c_void_p], C.c_int),
+        "kvs_payload_pages_in_use": ([C.c_void_p, C.c_int32, P(C.c_uint64)], C.c_int),
+        "kvs_payload_pool_of": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, C.c_int32, P(C.c_int32)], C.c_int),
+        "kvs_payload_bytes_moved": ([C.c_void_p, P(C.c_uint64)], C.c_int),
+        "kvs_set_default_payload": ([C.c_void_p, P(_PayloadOpts), C.c_int32], C.c_int),
+        "kvs_cluster_node": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -521,3 +539,107 @@ def decode_step_time(batch: int, gpu: Optional[GpuProfile] = None, lib: Optional
     out = C.c_int64()
     _check(h, h.kvs_decode_step_time(batch, C.byref(g), C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------------------
+# Physical payload (include/symsim/payload.hpp through kvs.h)
+
+POOL_DEVICE, POOL_HOST, POOL_LANDING, POOL_DISK = range(4)
+BLOCK_EVENTS = ("created", "load_h2d", "load_disk_host", "host_copy", "disk_write", "swap_out", "net_arrive")
+
+
+@dataclass
+class PayloadOptions:
+    """Page pools of one node (symsim::PayloadOptions)."""
+    device: int = 0
+    num_kv_heads: int = 8
+    head_dim: int = 128
+    block_tokens: int = 16
+    dtype: int = 1  # KVX_DTYPE_BF16
+    fill_mode: int = 1  # KVX_FILL_VALUES
+    device_pages: int = 0
+    host_pages: int = 0
+    landing_pages: int = 0
+    disk_pages: int = 0
+    seed: int = 0
+
+    def _c(self) -> "_PayloadOpts":
+        return _PayloadOpts(self.device, self.num_kv_heads, self.head_dim, self.block_tokens, self.dtype,
+                            self.fill_mode, self.device_pages, self.host_pages, self.landing_pages,
+                            self.disk_pages, self.seed)
+
+    def page_bytes(self) -> int:
+        return 2 * self.num_kv_heads * self.block_tokens * self.head_dim * (2 if self.dtype == 1 else 4)
+
+
+class PayloadCluster:
+    """Registry of payload nodes (migration sources are looked up here)."""
+
+    def __init__(self):
+        self._lib = load_kvs_library()
+        h = C.c_void_p()
+        _check(self._lib, self._lib.kvs_cluster_create(C.byref(h)))
+        self._h = h
+        self.nodes: Dict[int, "NodePayload"] = {}
+
+    def node(self, node_id: int) -> "NodePayload":
+        if node_id not in self.nodes:
+            h = C.c_void_p()
+            _check(self._lib, self._lib.kvs_cluster_node(self._h, node_id, C.byref(h)))
+            self.nodes[node_id] = NodePayload(None, node_id, None, _handle=h.value, _cluster=self)
+        return self.nodes[node_id]
+
+    def set_default(self, template: Optional[PayloadOptions], num_devices: int = 1) -> None:
+        """Every KvStore constructed afterwards (in any caller) gets a node."""
+        if template is None:
+            _check(self._lib, self._lib.kvs_set_default_payload(None, None, 0))
+        else:
+            _check(self._lib, self._lib.kvs_set_default_payload(self._h, C.byref(template._c()), num_devices))
+
+
+class NodePayload:
+    """Real pages behind one store's DEVICE/HOST/DISK copies."""
+
+    def __init__(self, cluster: Optional[PayloadCluster], node_id: int, opts: Optional[PayloadOptions],
+                 _handle: Optional[int] = None, _cluster=None):
+        self._lib = load_kvs_library()
+        self.node_id = node_id
+        self.cluster = cluster or _cluster
+        if _handle is not None:
+            self._h = C.c_void_p(_handle)
+            self.opts = opts
+        else:
+            h = C.c_void_p()
+            _check(self._lib, self._lib.kvs_payload_create(cluster._h if cluster else None, node_id,
+                                                           C.byref(opts._c()), C.byref(h)))
+            self._h = h
+            self.opts = opts
+            if cluster is not None:
+                cluster.nodes[node_id] = self
+
+    def attach(self, store: KvStore) -> None:
+        _check(self._lib, self._lib.kvs_attach_payload(store._h, self._h))
+
+    def read_block(self, session: int, layer: int, block: int, tier: int, page_bytes: int):
+        import numpy as np
+        out = np.empty(page_bytes, np.uint8)
+        rc = self._lib.kvs_payload_read_block(self._h, session, layer, block, tier, out.ctypes.data)
+        if rc == 1:
+            return None
+        _check(self._lib, rc)
+        return out
+
+    def pages_in_use(self, pool: int) -> int:
+        out = C.c_uint64()
+        _check(self._lib, self._lib.kvs_payload_pages_in_use(self._h, pool, C.byref(out)))
+        return out.value
+
+    def pool_of(self, session: int, layer: int, block: int, tier: int) -> int:
+        out = C.c_int32()
+        _check(self._lib, self._lib.kvs_payload_pool_of(self._h, session, layer, block, tier, C.byref(out)))
+        return out.value
+
+    def bytes_moved(self) -> Dict[str, int]:
+        out = (C.c_uint64 * 7)()
+        _check(self._lib, self._lib.kvs_payload_bytes_moved(self._h, out))
+        return dict(zip(BLOCK_EVENTS, list(out)))

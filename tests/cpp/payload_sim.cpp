@@ -1,0 +1,187 @@
+// Config-1 parity run through the reference's UNCHANGED cluster simulator.
+// TEST INFRASTRUCTURE (built by tests/cpp/build_payload_sim.sh into
+// oracle/_ref/, because it links the reference's Simulation/Engine/
+// NodeManager/ClusterScheduler sources compiled from /root/reference).
+//
+// Two builds of this one file:
+//   payload_sim      this repo's KvStore + NodePayload: every store the
+//                    reference Simulation constructs gets real pages on the
+//                    GPU (via set_default_tier_backend_factory), so the trace's
+//                    appends, write-behind persists, advisory promotions and
+//                    node-to-node migrations move real bytes with the kvx
+//                    kernels. At the end every copy of every block on every
+//                    node is read back and checked bit-exact against the CPU
+//                    restatement's content for its (session, layer, block).
+//   payload_sim_ref  the reference KvStore, no payload: the state oracle.
+// Both print the full transfer ledger and per-request records; the test
+// requires the two outputs to be identical.
+//
+// Trace: tiny Llama-style KV (2 layers, 4 KV heads, head_dim 64, fp32: 32 KiB
+// pages), 8 sessions x 4 turns on 2 nodes, closed-loop chat with advisories
+// leading each turn by more than a migration takes; first turns are staggered
+// so least-loaded routing piles them onto node 0 and advisory re-planning
+// then migrates sessions to node 1 (the trick of
+// /root/reference/proj/tests/acceptance.cpp:172-188).
+//
+// usage: payload_sim [--device-pages N] [--policy symphony|swap|retain|recompute]
+
+#include <cinttypes>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "symsim/simcore.hpp"
+
+#ifdef WITH_PAYLOAD
+#include "../../oracle/kvx_oracle.h"
+#include "symsim/payload.hpp"
+#endif
+
+using namespace symsim;
+
+namespace {
+
+constexpr int kLayers = 2, kHeads = 4, kDim = 64, kBlockTokens = 16;
+constexpr std::uint64_t kSeed = 0x5EEDC0DE;
+
+Trace chat_trace(std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  auto draw = [&rng](Ns lo, Ns hi) { return std::uniform_int_distribution<Ns>(lo, hi)(rng); };
+  Trace t;
+  t.seed = seed;
+  t.concurrency_target = 8;
+  for (int s = 0; s < 8; ++s) {
+    SessionScript sc;
+    sc.session_id = "chat" + std::to_string(s);
+    for (int k = 0; k < 4; ++k) {
+      const std::int64_t prompt = 24 + 8 * ((s + k) % 5), resp = 6 + (s * 3 + k) % 9;
+      sc.turns.push_back({prompt, resp, prompt, resp});
+    }
+    t.sessions.push_back(sc);
+    for (std::uint32_t k = 0; k < 4; ++k) {
+      TraceEvent e;
+      e.session_index = static_cast<std::uint32_t>(s);
+      e.turn_index = k;
+      if (k == 0) {
+        e.anchor = AnchorPoint::SlotOpen;
+        e.delta = s < 5 ? ns_from_ms(1) * s : ns_from_ms(400) + ns_from_ms(3) * s;  // pile onto node 0 first
+      } else {
+        e.anchor = AnchorPoint::PrevCompletion;
+        e.anchor_turn = k - 1;
+        e.delta = draw(ns_from_ms(200), ns_from_ms(900));
+        TraceEvent adv = e;
+        adv.kind = EventKind::Advisory;
+        adv.delta = std::max<Ns>(0, e.delta - ns_from_ms(150));  // lead >> per-layer transfer time
+        t.events.push_back(adv);
+      }
+      e.kind = EventKind::Inference;
+      t.events.push_back(e);
+    }
+  }
+  return t;
+}
+
+const char* tier_s(Tier t) { return tier_name(t); }
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  std::int64_t device_pages = 0;
+  std::string policy = "symphony";
+  for (int i = 1; i < argc; ++i) {
+    if (!std::strcmp(argv[i], "--device-pages") && i + 1 < argc) device_pages = std::atoll(argv[++i]);
+    if (!std::strcmp(argv[i], "--policy") && i + 1 < argc) policy = argv[++i];
+  }
+  RunConfig cfg;
+  cfg.policy = policy_from(policy);
+  cfg.num_nodes = 2;
+  cfg.gpu.num_layers = kLayers;
+  cfg.gpu.kv_bytes_per_token = static_cast<std::int64_t>(kLayers) * 2 * kHeads * kDim * 4;
+  cfg.gpu.hbm_capacity = 80'000'000'000;
+  const std::int64_t page = cfg.gpu.kv_bytes_per_token / kLayers * kBlockTokens;
+  if (device_pages > 0) cfg.device_capacity = device_pages * page;  // force cooperative purges
+  cfg.host_capacity = 4096 * page;
+  cfg.sample_period = ns_from_sec(5);
+  const Trace trace = chat_trace(20260417);
+
+#ifdef WITH_PAYLOAD
+  PayloadCluster cluster;
+  std::vector<std::unique_ptr<NodePayload>> nodes;
+  PayloadOptions po;
+  po.device = 0;  // both nodes on the one visible GPU (peer path = local HBM)
+  po.layout = kvx_page_layout{kHeads, kDim, kBlockTokens, KVX_DTYPE_F32};
+  po.device_pages = static_cast<std::uint64_t>(device_pages > 0 ? device_pages + 64 : 2048);
+  po.host_pages = 4096;
+  po.landing_pages = 4096;
+  po.disk_pages = 8192;
+  po.seed = kSeed;
+  set_default_tier_backend_factory([&](int node_id) -> TierBackend* {
+    nodes.push_back(std::make_unique<NodePayload>(&cluster, node_id, po));
+    return nodes.back().get();
+  });
+#endif
+
+  Simulation sim(trace, cfg);
+  const RunReport rep = sim.run();
+
+  std::printf("policy %s nodes %d transfers %zu records %zu\n", rep.policy.c_str(), rep.num_nodes,
+              rep.transfers.size(), rep.records.size());
+  std::size_t migrate_rows = 0;
+  for (const auto& r : rep.transfers) {
+    if (r.reason == TransferReason::Migrate) ++migrate_rows;
+    std::printf("T %" PRId64 " n%d s%u l%u-%u %s>%s %" PRId64 " %s\n", r.time, r.node, r.session, r.layer_lo,
+                r.layer_hi, tier_s(r.from), tier_s(r.to), r.bytes, reason_name(r.reason));
+  }
+  for (const auto& r : rep.records)
+    std::printf("R s%u t%u n%d arr %" PRId64 " adm %" PRId64 " ft %" PRId64 " fin %" PRId64 " stall %" PRId64 "\n",
+                r.session, r.turn, r.node, r.arrival, r.admit, r.first_token, r.finish, r.load_stall);
+  std::printf("migrate_rows %zu\n", migrate_rows);
+
+#ifdef WITH_PAYLOAD
+  // Every copy on every node, bit-exact against the CPU restatement.
+  std::vector<std::uint8_t> got(static_cast<std::size_t>(page)), want(static_cast<std::size_t>(page));
+  const kvxo_layout ol{kHeads, kDim, kBlockTokens, 0};
+  std::size_t copies = 0, bad = 0, pages_held[4] = {0, 0, 0, 0};
+  for (int n = 0; n < cfg.num_nodes; ++n) {
+    const KvStore& st = sim.node(n).store();
+    NodePayload* node = cluster.node(n);
+    for (std::uint32_t s = 0; s < trace.sessions.size(); ++s)
+      for (int l = 0; l < kLayers; ++l)
+        for (std::uint32_t b = 0; b < st.blocks_in_layer(s, static_cast<std::uint16_t>(l)); ++b) {
+          const std::uint8_t res = st.residency(s, static_cast<std::uint16_t>(l), b);
+          for (int t = 0; t < 3; ++t) {
+            const int pool = node->pool_of(s, static_cast<std::uint16_t>(l), b, static_cast<Tier>(t));
+            if (!(res & (1u << t))) {
+              if (pool >= 0) ++bad;
+              continue;
+            }
+            ++copies;
+            if (pool < 0 || !node->read_block(s, static_cast<std::uint16_t>(l), b, static_cast<Tier>(t), got.data())) {
+              ++bad;
+              continue;
+            }
+            ++pages_held[pool];
+            const std::uint32_t id0 = 0;
+            const kvxo_tag tag{s, static_cast<std::uint32_t>(l), b};
+            kvxo_fill_pages(want.data(), static_cast<std::uint64_t>(page), &id0, &tag, 1, kSeed, &ol, 1);
+            if (std::memcmp(got.data(), want.data(), got.size()) != 0) ++bad;
+          }
+        }
+    for (int p = 0; p < 4; ++p)
+      if (node->pages_in_use(static_cast<NodePayload::Pool>(p)) != pages_held[p]) ++bad;  // leak or loss
+    const std::uint64_t* mv = node->bytes_moved();
+    std::printf("payload node %d pages dev %zu host %zu landing %zu disk %zu moved created %" PRIu64
+                " h2d %" PRIu64 " host_copy %" PRIu64 " disk_write %" PRIu64 " net_arrive %" PRIu64 "\n",
+                n, pages_held[0], pages_held[1], pages_held[2], pages_held[3], mv[0], mv[1], mv[3], mv[4], mv[6]);
+    for (auto& h : pages_held) h = 0;
+  }
+  std::printf("payload verified_copies %zu mismatches %zu\n", copies, bad);
+  set_default_tier_backend_factory({});
+  return bad == 0 ? 0 : 1;
+#else
+  return 0;
+#endif
+}
