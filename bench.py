@@ -240,8 +240,36 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
                 attention=attention, e2e=e2e, gpu_launches=launches, session_bytes=session_bytes)
 
 
+def graph_time_ms(torch, launch, reps, replays, warmup=2):
+    """Per-launch device time of `launch(i)` captured `reps` times into one
+    CUDA graph (decode loops replay graphs; this keeps host launch overhead
+    out of a microsecond-scale kernel's number), replayed `replays` times."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for i in range(warmup):
+            launch(i)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            launch(i)
+    g.replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(replays):
+        g.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / (replays * reps)
+
+
 def bench_attention(args, torch, np, kvx, dev, hbm_peak):
-    """K4 over one layer of Llama-3.1-8B KV at ctx 8192 (GQA 32/8)."""
+    """K4 over one layer of Llama-3.1-8B KV at ctx 8192 (GQA 32/8), launches
+    replayed from a CUDA graph, rotating request sets so consecutive launches
+    read >= 256 MiB (> L2)."""
     cfg = CFG_8B
     blocks = cfg["ctx"] // cfg["block_tokens"]
     layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
@@ -254,33 +282,30 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
     tags = torch.stack([torch.zeros_like(ids), torch.zeros_like(ids), ids], -1).contiguous()
     kvx.fill_pages(pool, ids, tags, pages, 5, layout, kvx.FILL_VALUES)
     perm = torch.from_numpy(rng.permutation(pages).astype(np.int32)).to(dev)
-    stream = torch.cuda.current_stream(dev)
     res = {}
     for batch in (1, 8, 64):
-        sets = max(1, min(pages // (batch * blocks), -(-256 // (batch * 32))))  # >= 256 MiB rotated > L2
+        sets = max(1, min(pages // (batch * blocks), -(-256 // (batch * 32))))
         tables = [perm[s * batch * blocks:(s + 1) * batch * blocks].view(batch, blocks).contiguous()
                   for s in range(sets)]
         ctx = torch.full((batch,), cfg["ctx"], dtype=torch.int32, device=dev)
         q = (torch.randn(batch, 32, 128, device=dev) * 0.5).to(torch.bfloat16)
         out = torch.empty(batch, 32, 128, dtype=torch.float32, device=dev)
-        att = kvx.Attention(layout, 32, blocks)
-        wsb = att.workspace_bytes(batch, cfg["ctx"])
-        ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
-
-        def run(i, ev):
-            if ev:
-                ev[0].record(stream)
-            att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws, stream)
-            if ev:
-                ev[1].record(stream)
-
-        steps = max(10, args.steps)
-        _, (ms,) = time_events(torch, run, steps, 3)
-        t = statistics.mean(ms)
         kv_bytes = batch * cfg["ctx"] * 2 * cfg["kv_heads"] * cfg["head_dim"] * 2
+        reps = max(sets, 16 if batch < 64 else 4)
+
+        def timed(splits):
+            att = kvx.Attention(layout, 32, blocks, num_splits=splits)
+            ws = torch.zeros(max(att.workspace_bytes(batch, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
+            return graph_time_ms(torch, lambda i: att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws),
+                                 reps, max(3, min(args.steps, 20)))
+
+        t = timed(0)
         gbs = kv_bytes / (t * 1e-3) / GB
         res[f"batch{batch}"] = {"ms_per_layer": t, "hbm_gbs": gbs, "frac": gbs / hbm_peak,
-                                "kv_bytes": kv_bytes, "rotating_sets": sets}
+                                "kv_bytes": kv_bytes, "rotating_sets": sets, "timing": "cuda-graph replay"}
+        if args.attn_sweep:  # diagnostic: fixed split-K factors
+            res[f"batch{batch}"]["split_sweep_gbs"] = {
+                s: round(kv_bytes / (timed(s) * 1e-3) / GB, 1) for s in (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)}
     return res
 
 
@@ -342,27 +367,39 @@ def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):
 
 
 def bench_multi(args, torch, np, kvx, dev, rank, world):
-    """Ring migration of one 70B@32K session per rank to rank+1 over NVLink."""
+    """Ring migration of one 70B@32K session per rank to rank+1 over NVLink:
+    K3 (kvx_copy_pages) on the source GPU stores straight into the receiver's
+    page pool, opened through CUDA IPC. No collective on the data path."""
     import torch.distributed as dist
-    cfg = CFG_70B
+    from paper_2412_16434_b200 import cluster
+    cfg = dict(CFG_70B)
+    if args.layers:
+        cfg["layers"] = args.layers
     blocks, n = session_pages(cfg)
-    layout, pool, d_src, d_dst, _, _ = make_session(torch, kvx, np, cfg, 100 + rank, dev)
+    layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
     pb = layout.page_bytes()
-    handle = pool.ipc_export()
-    handles = [None] * world
-    dist.all_gather_object(handles, (handle, pool.num_pages, torch.cuda.get_device_properties(dev).uuid.hex
-                                     if hasattr(torch.cuda.get_device_properties(dev), "uuid") else ""))
-    nxt = (rank + 1) % world
-    peer = kvx.Pool.ipc_open(handles[nxt][0], handles[nxt][1], pb, dev.index)
+    pool = kvx.Pool(2 * n, pb, device=dev.index)
+    src_ids, _ = cluster.session_layout(rank, 2 * n, n)
+    d_src = torch.from_numpy(src_ids.view(np.int32)).to(dev)
+    seed = cluster.session_seed(rank)
+
+    def tags_for(seed_):
+        layer = np.repeat(np.arange(cfg["layers"], dtype=np.uint32), blocks)
+        block = np.tile(np.arange(blocks, dtype=np.uint32), cfg["layers"])
+        return torch.from_numpy(np.stack([np.full(n, seed_, np.uint32), layer, block], -1).view(np.int32)).to(dev)
+
+    kvx.fill_pages(pool, d_src, tags_for(seed), n, seed, layout, kvx.FILL_VALUES)
+    torch.cuda.synchronize()
+    peers = cluster.exchange_pool_handles(dist, rank, pool.ipc_export(), 2 * n, pb)
+    nxt = cluster.ring_peer(rank, world)
+    peer = kvx.Pool.ipc_open(peers[nxt].handle, peers[nxt].num_pages, pb, dev.index)
+    _, peer_dst = cluster.session_layout(nxt, 2 * n, n)  # the receiver's landing pages
+    d_peer_dst = torch.from_numpy(peer_dst.view(np.int32)).to(dev)
     stream = torch.cuda.current_stream(dev)
     mode = {"auto": kvx.COPY_AUTO, "sm": kvx.COPY_SM, "tma": kvx.COPY_TMA}[args.copy_mode]
-    # receiver-side destinations: the peer's second half (its own dst ids are
-    # the same permutation recipe, seeded by the peer's rank)
-    rng = np.random.default_rng(100 + nxt)
-    perm = rng.permutation(2 * n).astype(np.uint32)
-    d_peer_dst = torch.from_numpy(perm[n:2 * n].view(np.int32)).to(dev)
+    red_dev = dev if dist.get_backend() == "nccl" else None
 
-    def step(i, ev):
+    def step(ev):
         if ev:
             ev[0].record(stream)
         kvx.copy_pages(pool, d_src, peer, d_peer_dst, n, mode, stream)
@@ -370,28 +407,39 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
             ev[1].record(stream)
 
     for _ in range(args.warmup):
-        step(0, None)
+        step(None)
     torch.cuda.synchronize()
     dist.barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     with ClockSampler(dev.index) as clocks:
-        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        start.record(stream)
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
         for i in range(args.steps):
-            step(i, evs[i])
-        end.record(stream)
+            step(evs[i])
         torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([start.elapsed_time(end)], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    dist.barrier()  # peers finished writing before anyone reads / frees
-    ms_per_step = ms.item() / args.steps
+    dist.barrier()  # every sender has finished writing into its receiver
+    my_ms = evs[0][0].elapsed_time(evs[-1][-1])
+    ms = cluster.max_over_ranks(dist, my_ms, red_dev)
+    # what landed here is the ring source's session, bit for bit
+    src_rank = cluster.ring_source(rank, world)
+    _, my_dst = cluster.session_layout(rank, 2 * n, n)
+    expect = kvx.Pool(n, pb, device=dev.index)
+    kvx.fill_pages(expect, torch.arange(n, dtype=torch.int32, device=dev), tags_for(cluster.session_seed(src_rank)),
+                   n, cluster.session_seed(src_rank), layout, kvx.FILL_VALUES)
+    torch.cuda.synchronize()
+    probe = torch.randint(0, n, (min(n, 4096),), device=dev)
+    got = pool.as_tensor()[torch.from_numpy(my_dst.view(np.int32)).to(dev)[probe].long()]
+    ok = bool(torch.equal(got, expect.as_tensor()[probe]))
+    oks = [None] * world
+    dist.all_gather_object(oks, ok)
+    assert all(oks), f"migrated pages differ on ranks {[i for i, o in enumerate(oks) if not o]}"
+    ms_per_step = ms / args.steps
     session_bytes = n * pb
     value = world * session_bytes / (ms_per_step * 1e-3) / GB
     kern = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
     achieved = session_bytes / (kern * 1e-3) / GB
     peer.close()
+    dist.barrier()
     return dict(value=value, ms_per_step=ms_per_step, clocks=clocks.summary(), session_bytes=session_bytes,
+                cfg=cfg, verified=True,
                 roofline={"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                           "frac": achieved / NVLINK_PEAK_GBS, "traffic": None, "kernel": "kvx_copy_pages(peer)",
                           "algorithmic_bytes_per_launch": session_bytes, "peak_kind": "measured peer copy"},
@@ -510,6 +558,10 @@ def main():
     ap.add_argument("--skip-attention", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--attn-sweep", action="store_true", help="diagnostic: time fixed split-K factors")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help="N>1 control plane")
+    ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
+    ap.add_argument("--layers", type=int, default=0, help="test mode: shrink the N>1 session")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -522,6 +574,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.same_device:  # test mode: every rank on cuda:0 (IPC between processes, one GPU)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     kvx.lib()
@@ -529,9 +583,12 @@ def main():
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         res = bench_multi(args, torch, np, kvx, dev, rank, world)
-        cfg = CFG_70B
+        cfg = res["cfg"]
         workload = "llama-3.1-70b-kv @32K session ring migration over NVLink (kvx_copy_pages into peer pool)"
     else:
         res = bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind)

@@ -148,7 +148,10 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
 /* out[b][hq][d] (fp32) = softmax(scale * q[b][hq] . K^T) V over the first
  * ctx_lens[b] tokens of request b, whose block table row is
  * d_block_tables[b * max_blocks ...]. q has the layout dtype. Workspace of
- * kvx_decode_attention_workspace() bytes (may be 0 -> NULL allowed). */
+ * kvx_decode_attention_workspace() bytes (may be 0 -> NULL allowed): split-K
+ * partials plus per-(request, kv head) arrival counters; it must be
+ * zero-filled before its first use, and every launch leaves the counters
+ * zeroed again (the last split of each group merges all splits in-kernel). */
 uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx_attn_params* params,
                                         int32_t batch, int32_t max_ctx);
 int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,

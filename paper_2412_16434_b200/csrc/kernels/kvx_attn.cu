@@ -34,6 +34,7 @@ constexpr int kStages = 3;       // cp.async ring depth per warp
 constexpr int kTileBytes = kT * kD * 2;  // one kv head's K (or V) in a page: 4 KiB
 constexpr int kStageBytes = 2 * kTileBytes;
 constexpr int kSmemBytes = kWarps * kStages * kStageBytes;  // 96 KiB
+constexpr int kMaxPagesPerCta = 1024;  // block-table slice staged in smem (4 KiB)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -77,6 +78,7 @@ struct AttnArgs {
   float* out;         // [B][Hq][128]
   float* part_o;      // [B][Hq][S][128]
   float* part_ml;     // [B][Hq][S][2]
+  uint32_t* arrivals; // [B][H] split counters; zero between launches
   int heads;          // kv heads
   int group;          // q heads per kv head
   int max_blocks;
@@ -86,6 +88,8 @@ struct AttnArgs {
 
 __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t s_pages[kMaxPagesPerCta];
+  __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int ctx = a.ctx_lens[b];
@@ -95,8 +99,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
   const int p_end = min(n_pages, p_begin + per_split);
   const uint32_t* table = a.tables + static_cast<uint64_t>(b) * a.max_blocks;
   const int hq0 = h * a.group;
-
-  // Q as mma A fragments (rows = the group's query heads, zero-padded to 16).
+  // Q as mma A fragments (issued first: its latency overlaps the table read)
+  // Rows = the group's query heads, zero-padded to 16.
   uint32_t qa[kD / 16][4];
   {
     const int r0 = lane >> 2, c = (lane & 3) * 2;
@@ -112,6 +116,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
     }
   }
 
+  // Stage this CTA's slice of the block table once (one coalesced read
+  // instead of a dependent global load in front of every page fetch).
+  for (int i = threadIdx.x; i < p_end - p_begin; i += blockDim.x) s_pages[i] = __ldg(table + p_begin + i);
+  __syncthreads();
+
   float o[kD / 8][4];
 #pragma unroll
   for (int i = 0; i < kD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
@@ -126,7 +135,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
   auto issue = [&](int i) {  // page i of this warp -> stage i % kStages
     if (i < my_count) {
       const int p = my_first + i * kWarps;
-      const uint8_t* page = a.pool + static_cast<uint64_t>(__ldg(table + p)) * a.page_bytes;
+      const uint8_t* page = a.pool + static_cast<uint64_t>(s_pages[p - p_begin]) * a.page_bytes;
       const uint8_t* k_src = page + static_cast<uint64_t>(h) * kTileBytes;
       const uint8_t* v_src = page + static_cast<uint64_t>(a.heads + h) * kTileBytes;
       uint8_t* st = ring + (i % kStages) * kStageBytes;
@@ -152,18 +161,23 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
     const int tok0 = (my_first + i * kWarps) * kT;
 
     // S^T[head][tok] = Q . K^T, two n-tiles of 8 tokens.
-    float s[2][4];
+    // Even and odd k-steps accumulate separately: four independent mma
+    // chains of depth 4 instead of two of depth 8 (shorter per-page latency).
+    float s[2][4], s_odd[2][4];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+      s_odd[j][0] = s_odd[j][1] = s_odd[j][2] = s_odd[j][3] = 0.f;
       const int row = j * 8 + (lane & 7);
 #pragma unroll
       for (int kk = 0; kk < kD / 16; kk += 2) {
         uint32_t b0, b1, b2, b3;
         ldsm_x4(ks + swz(row, 2 * kk + (lane >> 3)), b0, b1, b2, b3);
         mma_bf16(s[j], qa[kk], b0, b1);
-        mma_bf16(s[j], qa[kk + 1], b2, b3);
+        mma_bf16(s_odd[j], qa[kk + 1], b2, b3);
       }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) s[j][e] += s_odd[j][e];
     }
     // Online softmax (base 2), rows lane/4 and lane/4 + 8.
     float mx = -INFINITY, mx8 = -INFINITY;
@@ -274,24 +288,66 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
       }
     }
   }
-}
+  if (a.splits == 1) return;
 
-// Log-sum-exp merge of the split partials: one CTA per (request, q head).
-__global__ void attn_combine(const float* part_o, const float* part_ml, float* out, int splits, int d) {
-  const uint64_t row = blockIdx.x;
-  const float* ml = part_ml + row * splits * 2;
-  float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, ml[2 * s]);
-  const float Mb = M == -INFINITY ? 0.f : M;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float L = 0.f, O = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const float f = exp2f(ml[2 * s] - Mb);
-      L += f * ml[2 * s + 1];
-      O += f * part_o[(row * splits + s) * d + j];
-    }
-    out[row * d + j] = L > 0.f ? O / L : 0.f;
+  // Split-K merge fused in: the last CTA of this (request, kv head) to finish
+  // merges every split's partial (L2-resident) — no second launch.
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(a.arrivals + static_cast<uint64_t>(b) * a.heads + h, 1u);
+    s_last = prev == static_cast<uint32_t>(a.splits - 1);
   }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // Stage every split's (m, l) in shared memory with one load per thread,
+  // turn them into per-row weights, then stream the partial O rows with
+  // 8 independent L2 loads in flight per thread.
+  float* sm_m = reinterpret_cast<float*>(smem);  // [splits][16]
+  float* sm_l = sm_m + a.splits * 16;            // [splits][16] -> weights
+  float* sm_inv = sm_l + a.splits * 16;          // [16] 1 / L
+  const uint64_t row0 = static_cast<uint64_t>(b) * a.heads * a.group + hq0;
+  for (int i = threadIdx.x; i < rows * a.splits; i += blockDim.x) {
+    const int r = i / a.splits, s = i - r * a.splits;
+    const float* ml = a.part_ml + ((row0 + r) * a.splits + s) * 2;
+    sm_m[s * 16 + r] = __ldcg(ml);
+    sm_l[s * 16 + r] = __ldcg(ml + 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < rows) {
+    const int r = threadIdx.x;
+    float M = -INFINITY;
+    for (int s = 0; s < a.splits; ++s) M = fmaxf(M, sm_m[s * 16 + r]);
+    const float Mb = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+    for (int s = 0; s < a.splits; ++s) {
+      const float f = exp2f(sm_m[s * 16 + r] - Mb);
+      L += f * sm_l[s * 16 + r];
+      sm_l[s * 16 + r] = f;
+    }
+    sm_inv[r] = L > 0.f ? 1.f / L : 0.f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
+    const int r = e / kD, d = e - r * kD;
+    const float* po = a.part_o + (row0 + r) * a.splits * kD + d;
+    float acc0 = 0.f, acc1 = 0.f;
+    int s = 0;
+    for (; s + 8 <= a.splits; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(po + (s + j) * kD);
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        acc0 += sm_l[(s + j) * 16 + r] * v[j];
+        acc1 += sm_l[(s + j + 1) * 16 + r] * v[j + 1];
+      }
+    }
+    for (; s < a.splits; ++s) acc0 += sm_l[s * 16 + r] * __ldcg(po + s * kD);
+    a.out[(row0 + r) * kD + d] = (acc0 + acc1) * sm_inv[r];
+  }
+  if (threadIdx.x == 0) a.arrivals[static_cast<uint64_t>(b) * a.heads + h] = 0;  // ready for the next launch
 }
 
 // Generic path (any head_dim <= 256 that is a multiple of 32, fp32 or bf16,
@@ -345,26 +401,24 @@ bool fast_path(const kvx_page_layout* l) {
   return l->dtype == KVX_DTYPE_BF16 && l->head_dim == kD && l->block_tokens == kT;
 }
 
-// Splits over the context so that (requests x kv heads x splits) CTAs fill
-// the machine in whole waves while each warp still streams >= 4 pages.
+// Split-K factor. Measured on B200 (profiles/r01_summary.md, split sweep at
+// ctx 8192): the best choice puts about one CTA per SM — batch 1 x 8 kv heads
+// -> 16 splits, batch 8 -> 2, batch 64 -> 1 — so the rule is the largest
+// split count with (requests x kv heads x splits) <= SM count, bounded by
+// the block-table staging limit and by >= 16 pages per CTA.
 int choose_splits(int batch, int heads, int max_ctx, int requested, int sms) {
-  if (requested > 0) return requested;
   const int pages = std::max(1, (max_ctx + kT - 1) / kT);
-  const int max_splits = std::max(1, pages / (kWarps * 4));
-  const long base = static_cast<long>(batch) * heads;
-  const long slots = 2L * sms;  // 2 CTAs per SM (96 KiB smem each)
-  int best = 1;
-  double best_cost = 1e300;
-  for (int s = 1; s <= std::min(max_splits, 256); ++s) {
-    const long ctas = base * s;
-    const double waves = std::ceil(static_cast<double>(ctas) / slots);
-    const double cost = waves * std::ceil(static_cast<double>(pages) / s) + 0.02 * s;  // merge overhead
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = s;
-    }
-  }
-  return best;
+  const int min_splits = (pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
+  if (requested > 0) return std::max(requested, min_splits);
+  const int max_splits = std::max(min_splits, pages / (kWarps * 4));
+  const long base = std::max(1L, static_cast<long>(batch) * heads);
+  const int fill = static_cast<int>(std::max(1L, sms / base));
+  return std::max(min_splits, std::min(max_splits, std::min(fill, 256)));
+}
+
+uint64_t workspace_for(uint64_t batch, uint64_t hq, uint64_t heads, int splits) {
+  if (splits <= 1) return 0;
+  return batch * hq * splits * (kD + 2) * sizeof(float) + batch * heads * sizeof(uint32_t);
 }
 
 }  // namespace
@@ -376,9 +430,7 @@ uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx
                                         int32_t max_ctx) {
   if (!layout || !params || batch <= 0 || !kvx::fast_path(layout)) return 0;
   const int splits = kvx::choose_splits(batch, layout->num_kv_heads, max_ctx, params->num_splits, kvx::sm_count(0));
-  if (splits <= 1) return 0;
-  const uint64_t rows = static_cast<uint64_t>(batch) * params->num_q_heads;
-  return rows * splits * (kvx::kD + 2) * sizeof(float);
+  return kvx::workspace_for(batch, params->num_q_heads, layout->num_kv_heads, splits);
 }
 
 int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
@@ -417,19 +469,15 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     a.scale_log2 = scale * kvx::kLog2e;
     if (splits > 1) {
       const uint64_t rows = static_cast<uint64_t>(batch) * Hq;
-      const uint64_t need = rows * splits * (kvx::kD + 2) * sizeof(float);
-      if (!d_workspace || workspace_bytes < need) return kvx::fail_arg("kvx_decode_attention: workspace too small");
+      if (!d_workspace || workspace_bytes < kvx::workspace_for(batch, Hq, H, splits))
+        return kvx::fail_arg("kvx_decode_attention: workspace too small");
       a.part_o = static_cast<float*>(d_workspace);
       a.part_ml = a.part_o + rows * splits * kvx::kD;
+      a.arrivals = reinterpret_cast<uint32_t*>(a.part_ml + rows * splits * 2);
     }
     dim3 grid(splits, H, batch);
     kvx::attn_bf16_d128<<<grid, kvx::kWarps * 32, kvx::kSmemBytes, st>>>(a);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");
-    if (splits > 1) {
-      kvx::attn_combine<<<static_cast<unsigned>(static_cast<uint64_t>(batch) * Hq), kvx::kD, 0, st>>>(
-          a.part_o, a.part_ml, d_out, splits, kvx::kD);
-      KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention(combine)");
-    }
     return KVX_OK;
   }
 

@@ -1,0 +1,42 @@
+"""The N>1 migration path of bench.py, exercised with two ranks on the one
+available GPU: real CUDA IPC between two processes, the K3 kernel storing
+into the peer process's page pool, max-over-ranks timing, and the receivers'
+bit-exact check of what landed. (On an 8-GPU box the same code runs one rank
+per GPU with NCCL as the control plane; here the control plane is gloo.)"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_process_ring_migration_on_one_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--same-device", "--dist-backend", "gloo", "--layers", "2"]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                          env={**os.environ, "OMP_NUM_THREADS": "1"})
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-5000:]
+    lines = [ln for ln in proc.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, proc.stdout
+    res = json.loads(lines[0])
+    assert res["n_gpus"] == 2 and res["value"] > 0
+    assert res["roofline"]["bound"] == "nvlink"
+    assert res["config"]["layers"] == 2
