@@ -232,12 +232,13 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
 
     attention = None if args.skip_attention else bench_attention(args, torch, np, kvx, dev, hbm_peak)
     e2e = None if args.skip_e2e else bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst)
+    overlap = None if args.skip_overlap else bench_overlap(args, torch, np, kvx, dev, hbm_peak)
     launches = 2 * args.steps
     return dict(value=value, ms_per_step=ms_per_step, extra=extra, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": ncu_traffic(dom_name), "kernel": dom_name,
                           "algorithmic_bytes_per_launch": 2 * session_bytes, "peak_kind": peak_kind},
-                attention=attention, e2e=e2e, gpu_launches=launches, session_bytes=session_bytes)
+                attention=attention, e2e=e2e, overlap=overlap, gpu_launches=launches, session_bytes=session_bytes)
 
 
 def graph_time_ms(torch, launch, reps, replays, warmup=2):
@@ -306,6 +307,138 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
         if args.attn_sweep:  # diagnostic: fixed split-K factors
             res[f"batch{batch}"]["split_sweep_gbs"] = {
                 s: round(kv_bytes / (timed(s) * 1e-3) / GB, 1) for s in (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)}
+    return res
+
+
+def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
+    """Migration overlapped with decode, on one GPU (free-running streams).
+
+    decode : one decode step of Llama-3.1-8B KV at batch 16 x ctx 8192 — 32
+             layers of K4 on the main stream (17 GB of KV read per step)
+    migrate: one 8B@8K session (1 GiB) moved layer by layer with K3 on a side
+             stream (SM mover, or copy engines), one event per layer
+    Both are CUDA graphs; the concurrent case is one graph that forks the side
+    stream. Reported: decode slowdown and the hidden fraction of the
+    migration. Then the physical pipeline gate: a batch-1 decode of the
+    migrating session whose layer l waits on layer l's arrival event,
+    against pipeline_gate()'s prediction from the measured arrivals
+    (reference kvstore.cpp:46-59)."""
+    from paper_2412_16434_b200 import kvstore as K
+    cfg = CFG_8B
+    L, blocks = cfg["layers"], cfg["ctx"] // cfg["block_tokens"]
+    layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
+    pb = layout.page_bytes()
+    B = 16
+    dec_pages = B * L * blocks
+    dpool = kvx.Pool(dec_pages, pb, device=dev.index)
+    ids = torch.arange(dec_pages, dtype=torch.int32, device=dev)
+    kvx.fill_pages(dpool, ids, torch.stack([ids * 0, ids * 0, ids], -1).contiguous(), dec_pages, 11, layout,
+                   kvx.FILL_VALUES)
+    perm = torch.randperm(dec_pages, device=dev, dtype=torch.int64).to(torch.int32)
+    tables = [perm[l * B * blocks:(l + 1) * B * blocks].view(B, blocks).contiguous() for l in range(L)]
+    ctx = torch.full((B,), cfg["ctx"], dtype=torch.int32, device=dev)
+    q = (torch.randn(B, 32, 128, device=dev) * 0.5).to(torch.bfloat16)
+    out = torch.empty(B, 32, 128, dtype=torch.float32, device=dev)
+    att = kvx.Attention(layout, 32, blocks)
+    ws = torch.zeros(max(att.workspace_bytes(B, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
+
+    n = L * blocks
+    spool = kvx.Pool(2 * n, pb, device=dev.index)
+    sp = torch.randperm(2 * n, device=dev, dtype=torch.int64).to(torch.int32)
+    src, dst = sp[:n].contiguous(), sp[n:].contiguous()
+    kvx.fill_pages(spool, src, torch.stack([src * 0 + 3, src // blocks, src % blocks], -1).contiguous(), n, 3,
+                   layout, kvx.FILL_VALUES)
+    h_src = src.cpu().numpy().view(np.uint32)
+    h_dst = dst.cpu().numpy().view(np.uint32)
+    q1 = q[:1].contiguous()
+    out1 = torch.empty(1, 32, 128, dtype=torch.float32, device=dev)
+    ctx1 = ctx[:1].contiguous()
+    att1 = kvx.Attention(layout, 32, blocks)
+    ws1 = torch.zeros(max(att1.workspace_bytes(1, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
+    mig_tables = [dst[l * blocks:(l + 1) * blocks].view(1, blocks).contiguous() for l in range(L)]
+    torch.cuda.synchronize()
+
+    side = torch.cuda.Stream(dev)
+
+    def decode(st):
+        for l in range(L):
+            att(dpool, tables[l], ctx, q, out, B, cfg["ctx"], ws, st.cuda_stream)
+
+    def migrate(st, mode, events=None):
+        for l in range(L):
+            sl = slice(l * blocks, (l + 1) * blocks)
+            if mode == kvx.COPY_CE:
+                kvx.copy_pages(spool, h_src[sl], spool, h_dst[sl], blocks, mode, st.cuda_stream)
+            else:
+                kvx.copy_pages(spool, src[sl], spool, dst[sl], blocks, mode, st.cuda_stream)
+            if events is not None:
+                events[l].record(st)
+
+    def capture(body):
+        cap = torch.cuda.Stream(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            body(cap)
+        return g
+
+    def time_graph(g, reps=10):
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(reps):
+            g.replay()
+        t1.record()
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1) / reps
+
+    def fork(cap, fn):
+        side.wait_stream(cap)
+        with torch.cuda.stream(side):
+            fn(side)
+        cap.wait_stream(side)
+
+    res = {"decode": f"batch {B} x ctx {cfg['ctx']} x {L} layers (K4)", "migration": "1 GiB session, 32 layer moves"}
+    t_dec = time_graph(capture(lambda c: decode(c)))
+    res["decode_alone_ms"] = t_dec
+    for name, mode in (("sm", kvx.COPY_AUTO), ("ce", kvx.COPY_CE)):
+        t_mig = time_graph(capture(lambda c: migrate(c, mode)))
+        t_both = time_graph(capture(lambda c: (fork(c, lambda st: migrate(st, mode)), decode(c))))
+        res[name] = {"migrate_alone_ms": t_mig, "concurrent_ms": t_both,
+                     "decode_slowdown": t_both / t_dec - 1.0,
+                     "hidden_fraction": max(0.0, min(1.0, (t_dec + t_mig - t_both) / t_mig)),
+                     "migrate_gbs_alone": n * pb / (t_mig * 1e-3) / GB}
+
+    # Physical pipeline gate: per-layer arrival events gate a batch-1 decode of
+    # the migrating session; compare with the reference recurrence.
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(L)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(side)
+    migrate(side, kvx.COPY_AUTO, ev)
+    torch.cuda.synchronize()
+    ready_us = [t0.elapsed_time(e) * 1e3 for e in ev]
+    t_layer = time_graph(capture(lambda c: [att1(spool, mig_tables[l], ctx1, q1, out1, 1, cfg["ctx"], ws1,
+                                                 c.cuda_stream) for l in range(L)])) / L
+
+    def gated(c):
+        evs = [torch.cuda.Event() for _ in range(L)]
+        side.wait_stream(c)
+        with torch.cuda.stream(side):
+            migrate(side, kvx.COPY_AUTO, evs)
+        for l in range(L):
+            c.wait_event(evs[l])
+            att1(spool, mig_tables[l], ctx1, q1, out1, 1, cfg["ctx"], ws1, c.cuda_stream)
+        c.wait_stream(side)
+
+    t_gated = time_graph(capture(gated))
+    ns = [int(r * 1e3) for r in ready_us]
+    first_end, gate_start, stall = K.pipeline_gate(ns, 0, int(L * t_layer * 1e6))
+    res["pipeline_gate"] = {"layer_arrival_us_first_last": [ready_us[0], ready_us[-1]],
+                            "layer_decode_us": t_layer * 1e3, "measured_first_step_end_us": t_gated * 1e3,
+                            "predicted_first_step_end_us": first_end / 1e3, "predicted_stall_us": stall / 1e3,
+                            "unpipelined_us": ready_us[-1] + L * t_layer * 1e3}
     return res
 
 
@@ -558,6 +691,7 @@ def main():
     ap.add_argument("--skip-attention", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-overlap", action="store_true")
     ap.add_argument("--attn-sweep", action="store_true", help="diagnostic: time fixed split-K factors")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help="N>1 control plane")
     ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
@@ -609,6 +743,7 @@ def main():
         if world == 1:
             line["e2e"] = res["e2e"]
             line["decode_attention"] = res["attention"]
+            line["overlap"] = res["overlap"]
             line["detail"] = res["extra"]
             if not args.skip_cpu:
                 v, cores, sample = cpu_migrate(np, cfg, 8.0, layers=8, repeat_min=3)

@@ -30,10 +30,14 @@ namespace {
 constexpr int kD = 128;          // head_dim of the fast path
 constexpr int kT = 16;           // block_tokens of the fast path
 constexpr int kWarps = 4;        // warps per CTA, each streams its own pages
-constexpr int kStages = 3;       // cp.async ring depth per warp
+// cp.async ring depth per warp: 3 stages (96 KiB/CTA, 2 CTAs/SM). A 6-stage
+// variant (1 CTA/SM, 5 pages in flight per warp) was measured slower at
+// batch 1 and 8 (profiles/r01_summary.md): small batches are bound by the
+// per-warp instruction latency chain, not by bytes in flight.
+constexpr int kStagesWide = 3;
 constexpr int kTileBytes = kT * kD * 2;  // one kv head's K (or V) in a page: 4 KiB
 constexpr int kStageBytes = 2 * kTileBytes;
-constexpr int kSmemBytes = kWarps * kStages * kStageBytes;  // 96 KiB
+constexpr int smem_bytes(int stages) { return kWarps * stages * kStageBytes; }
 constexpr int kMaxPagesPerCta = 1024;  // block-table slice staged in smem (4 KiB)
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -86,6 +90,7 @@ struct AttnArgs {
   float scale_log2;
 };
 
+template <int kStages>
 __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t s_pages[kMaxPagesPerCta];
@@ -449,8 +454,9 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
   if (kvx::fast_path(layout) && group <= 16) {
     static bool configured = false;
     if (!configured) {
-      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kvx::kSmemBytes),
+      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kvx::smem_bytes(kvx::kStagesWide)),
                    "kvx_decode_attention: smem attribute");
       configured = true;
     }
@@ -476,7 +482,7 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
       a.arrivals = reinterpret_cast<uint32_t*>(a.part_ml + rows * splits * 2);
     }
     dim3 grid(splits, H, batch);
-    kvx::attn_bf16_d128<<<grid, kvx::kWarps * 32, kvx::kSmemBytes, st>>>(a);
+    kvx::attn_bf16_d128<kvx::kStagesWide><<<grid, kvx::kWarps * 32, kvx::smem_bytes(kvx::kStagesWide), st>>>(a);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");
     return KVX_OK;
   }

@@ -253,7 +253,11 @@ int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, 
     sizes.push_back((j - i) * src->page_bytes);
     i = j;
   }
-  if (st == nullptr) {  // batch API needs an explicit stream
+  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
+  if (st != nullptr) KVX_CUDA_TRY(cudaStreamIsCapturing(st, &capturing), "kvx_copy_pages(CE)");
+  // The batch API needs an explicit stream and cannot be graph-captured; one
+  // memcpy node per run of consecutive pages can.
+  if (st == nullptr || capturing != cudaStreamCaptureStatusNone) {
     for (size_t r = 0; r < srcs.size(); ++r)
       KVX_CUDA_TRY(cudaMemcpyAsync(dsts[r], srcs[r], sizes[r], cudaMemcpyDefault, st), "kvx_copy_pages(CE)");
     return KVX_OK;
