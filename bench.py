@@ -628,6 +628,22 @@ def reference_state_ops(np):
     return time.perf_counter() - t0
 
 
+def arm_config(cfg, world):
+    """The workload both arms report (identical for --impl b200 / reference)."""
+    blocks, n = session_pages(cfg)
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    if world == 1:
+        workload = (f"{cfg['model']} @{cfg['ctx']} session ({cfg['layers']} layers x {blocks} pages): pack every "
+                    "page into the migration buffer + unpack into a second page permutation")
+    else:
+        workload = (f"{cfg['model']} @{cfg['ctx']} session per rank, ring migration rank r -> r+1 "
+                    "(page-to-page into the receiver's pool)")
+    return {"workload": workload, "model_shape": cfg["model"], "seq_len": cfg["ctx"], "layers": cfg["layers"],
+            "kv_heads": cfg["kv_heads"], "head_dim": cfg["head_dim"], "kv_dtype": "bf16", "page_bytes": pb,
+            "session_bytes": n * pb, "parallelism": "single" if world == 1 else f"ring-p2p{world}",
+            "l2": "inputs larger than the 126 MB L2 (1 GiB / 10.7 GB per step); no flush"}
+
+
 def run_reference(args):
     import numpy as np
     rank = int(os.environ.get("RANK", "0"))
@@ -673,8 +689,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{cfg['model']} @{cfg['ctx']} session migration (CPU)", "seq_len": cfg["ctx"],
-                       "layers": cfg["layers"], "parallelism": f"replicas{world}"},
+            "config": arm_config(cfg, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -723,22 +738,15 @@ def main():
             dist.init_process_group("gloo")
         res = bench_multi(args, torch, np, kvx, dev, rank, world)
         cfg = res["cfg"]
-        workload = "llama-3.1-70b-kv @32K session ring migration over NVLink (kvx_copy_pages into peer pool)"
     else:
         res = bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind)
         cfg = CFG_8B
-        workload = "llama-3.1-8b-kv @8K session: kvx_pack all pages + kvx_unpack into a second permutation"
 
     if rank == 0:
         line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": workload, "model_shape": cfg["model"], "seq_len": cfg["ctx"],
-                           "layers": cfg["layers"], "kv_heads": cfg["kv_heads"], "head_dim": cfg["head_dim"],
-                           "kv_dtype": "bf16", "page_bytes": 2 * cfg["kv_heads"] * 16 * cfg["head_dim"] * 2,
-                           "session_bytes": res["session_bytes"],
-                           "parallelism": "single" if world == 1 else f"ring-p2p{world}",
-                           "l2": "inputs (1 GiB / 10.7 GB per step) larger than the 126 MB L2; no flush"},
+                "config": arm_config(cfg, world),
                 "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["gpu_launches"]}
         if world == 1:
             line["e2e"] = res["e2e"]

@@ -47,10 +47,11 @@ def build_oracle(ref: bool = True) -> None:
     ref_src = Path(os.environ.get("REF", "/root/reference/proj")) / "src" / "kvstore.cpp"
     if ref and ref_src.exists():
         _make(ORACLE_DIR, "ref")
-        script = ROOT / "tests" / "cpp" / "build_payload_sim.sh"
-        proc = subprocess.run(["bash", str(script)], capture_output=True, text=True)
-        if proc.returncode != 0:
-            raise RuntimeError(f"build failed: {script}\n{proc.stdout}\n{proc.stderr}")
+        for name in ("build_payload_sim.sh", "build_serve_sim.sh"):
+            script = ROOT / "tests" / "cpp" / name
+            proc = subprocess.run(["bash", str(script)], capture_output=True, text=True)
+            if proc.returncode != 0:
+                raise RuntimeError(f"build failed: {script}\n{proc.stdout}\n{proc.stderr}")
 
 
 def ensure_built() -> None:
