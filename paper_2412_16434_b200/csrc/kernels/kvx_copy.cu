@@ -15,6 +15,7 @@
 // shared-memory stages (no register staging at all).
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "kvx_common.cuh"
@@ -26,9 +27,28 @@ constexpr int kVecThreads = 256;
 constexpr int kVecUnroll = 4;
 constexpr uint32_t kVecChunk = kVecThreads * kVecUnroll * 16;  // 16 KiB per work item
 
-constexpr int kBulkStages = 6;
-constexpr uint32_t kBulkChunk = 32768;  // 32 KiB per TMA transfer
-constexpr uint32_t kBulkSmem = kBulkStages * kBulkChunk;
+// TMA mover geometry, measured on B200 (profiles/r01_summary.md sweep):
+//   gather OR scatter (pack/unpack; one side contiguous): 32 KiB x 4 stages,
+//     one CTA per SM -> 6.40 / 6.47 TB/s (98-99% of the measured copy peak)
+//   gather AND scatter (page -> page copy): 64 KiB x 3 stages -> 6.25 TB/s
+// KVX_BULK_CHUNK / KVX_BULK_STAGES / KVX_BULK_CTAS_PER_SM override both (sweeps).
+constexpr int kBulkMaxStages = 16;
+struct BulkGeometry {
+  uint32_t chunk;
+  int stages;
+  int ctas_per_sm;
+};
+
+BulkGeometry bulk_geometry(bool both_scattered) {
+  BulkGeometry b = both_scattered ? BulkGeometry{65536, 3, 1} : BulkGeometry{32768, 4, 1};
+  if (const char* e = std::getenv("KVX_BULK_CHUNK")) b.chunk = static_cast<uint32_t>(std::atoi(e));
+  if (const char* e = std::getenv("KVX_BULK_STAGES")) b.stages = std::atoi(e);
+  if (const char* e = std::getenv("KVX_BULK_CTAS_PER_SM")) b.ctas_per_sm = std::atoi(e);
+  b.chunk = std::max<uint32_t>(1024, std::min<uint32_t>(b.chunk, 65536)) & ~15u;
+  b.stages = std::max(2, std::min(b.stages, kBulkMaxStages));
+  b.ctas_per_sm = std::max(1, std::min(b.ctas_per_sm, 8));
+  return b;
+}
 
 struct MoveArgs {
   const uint8_t* src;
@@ -39,6 +59,7 @@ struct MoveArgs {
   uint64_t page_bytes;
   uint32_t chunk_bytes;
   uint32_t chunks_per_page;
+  int stages;  // TMA ring depth (bulk mover only)
 };
 
 __device__ __forceinline__ void item_addr(const MoveArgs& a, uint64_t item, const uint8_t*& s, uint8_t*& d,
@@ -79,16 +100,18 @@ __global__ void __launch_bounds__(kVecThreads) page_move_vec(MoveArgs a) {
 }
 
 // TMA bulk variant: lane 0 of a single warp per SM streams chunks through a
-// kBulkStages-deep shared-memory ring. Load k+S-1 is issued as soon as the
+// a.stages-deep shared-memory ring. Load k+S-1 is issued as soon as the
 // bulk store of chunk k-1 has finished READING its stage.
 __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
   extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[kBulkStages];
+  __shared__ __align__(8) uint64_t full[kBulkMaxStages];
+  const int S = a.stages;
+  const uint32_t slot = a.chunk_bytes;
   if (threadIdx.x != 0) return;
   const uint64_t items = a.n_pages * a.chunks_per_page;
   if (blockIdx.x >= items) return;
   const uint64_t mine = (items - blockIdx.x + gridDim.x - 1) / gridDim.x;
-  for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+  for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
 
   auto load = [&](uint64_t k) {
@@ -96,24 +119,24 @@ __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
     uint8_t* d;
     uint32_t bytes;
     item_addr(a, blockIdx.x + k * gridDim.x, s, d, bytes);
-    const int st = static_cast<int>(k % kBulkStages);
+    const int st = static_cast<int>(k % S);
     mbar_arrive_expect_tx(&full[st], bytes);
-    bulk_g2s(ring + st * kBulkChunk, s, bytes, &full[st]);
+    bulk_g2s(ring + st * slot, s, bytes, &full[st]);
   };
-  const uint64_t prologue = mine < kBulkStages ? mine : kBulkStages;
+  const uint64_t prologue = mine < static_cast<uint64_t>(S) ? mine : S;
   for (uint64_t k = 0; k < prologue; ++k) load(k);
   for (uint64_t k = 0; k < mine; ++k) {
-    const int st = static_cast<int>(k % kBulkStages);
-    mbar_wait(&full[st], static_cast<uint32_t>((k / kBulkStages) & 1));
+    const int st = static_cast<int>(k % S);
+    mbar_wait(&full[st], static_cast<uint32_t>((k / S) & 1));
     const uint8_t* s;
     uint8_t* d;
     uint32_t bytes;
     item_addr(a, blockIdx.x + k * gridDim.x, s, d, bytes);
-    bulk_s2g(d, ring + st * kBulkChunk, bytes);
+    bulk_s2g(d, ring + st * slot, bytes);
     bulk_commit();
-    if (k >= 1 && k - 1 + kBulkStages < mine) {
+    if (k >= 1 && k - 1 + S < mine) {
       bulk_wait_read<1>();  // store k-1 has drained its stage
-      load(k - 1 + kBulkStages);
+      load(k - 1 + S);
     }
   }
   bulk_wait<0>();
@@ -129,17 +152,21 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
   const int sms = sm_count(device);
   if (mode == KVX_COPY_AUTO) mode = tma_ok ? KVX_COPY_TMA : KVX_COPY_SM;
   if (mode == KVX_COPY_TMA) {
-    a.chunk_bytes = static_cast<uint32_t>(std::min<uint64_t>(a.page_bytes, kBulkChunk));
+    const BulkGeometry geo = bulk_geometry(a.src_ids != nullptr && a.dst_ids != nullptr);
+    a.chunk_bytes = static_cast<uint32_t>(std::min<uint64_t>(a.page_bytes, geo.chunk));
     a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + a.chunk_bytes - 1) / a.chunk_bytes);
-    static bool configured[64] = {};
+    a.stages = geo.stages;
+    const uint32_t smem = static_cast<uint32_t>(geo.stages) * a.chunk_bytes;
+    static uint32_t configured[64] = {};
     const int dev = device < 0 ? 0 : device;
-    if (!configured[dev]) {
-      KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem), who);
-      configured[dev] = true;
+    if (configured[dev] < smem) {
+      KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), who);
+      configured[dev] = smem;
     }
     const uint64_t items = a.n_pages * a.chunks_per_page;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms)));
-    page_move_bulk<<<grid, 32, kBulkSmem, stream>>>(a);
+    const unsigned grid =
+        static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * geo.ctas_per_sm));
+    page_move_bulk<<<grid, 32, smem, stream>>>(a);
   } else if (mode == KVX_COPY_SM) {
     a.chunk_bytes = kVecChunk;
     a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + kVecChunk - 1) / kVecChunk);
