@@ -60,8 +60,11 @@ Ns think_ns_like_reference(std::int64_t words, double wpm) {
   return ns_from_sec(static_cast<double>(words) * 60.0 / wpm);
 }
 
+int g_sessions = 0;  // --sessions override (0: config default)
+
 Trace config4(int users, double miss, double mean_think_s, std::uint64_t seed) {
   SyntheticSpec spec;  // reference defaults: 1000 sessions, 73.4% multi-turn
+  if (g_sessions > 0) spec.sessions = g_sessions;
   auto scripts = synthesize_corpus(spec, seed);
   Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1);
   std::mt19937_64 rng(seed + 2);
@@ -76,7 +79,7 @@ Trace config4(int users, double miss, double mean_think_s, std::uint64_t seed) {
 
 Trace config5(int users, double miss, double mean_think_s, std::uint64_t seed) {
   SyntheticSpec spec;
-  spec.sessions = 600;
+  spec.sessions = g_sessions > 0 ? g_sessions : 600;
   spec.multi_turn_fraction = 1.0;
   auto scripts = synthesize_corpus(spec, seed);
   // Zipf(1.2) popularity over a seeded permutation of sessions: rank r gets
@@ -108,6 +111,8 @@ struct Calibration {
   double network_gbs = 12.5;
   double pcie_gbs = 25.0;
   double prefill_tps = 8192.0;
+  double think_s = 0.0;           // 0: config default
+  std::vector<int> users;         // sweep loads; empty: default list
   std::int64_t kv_bytes_per_token = 131'072;  // Llama-3.1-8B, bf16
   std::int64_t hbm_capacity = 160'000'000'000;
 };
@@ -182,6 +187,18 @@ Calibration parse_calibration(int argc, char** argv, int from) {
       c.pcie_gbs = std::atof(argv[++i]);
     } else if (!std::strcmp(argv[i], "--prefill-tps") && i + 1 < argc) {
       c.prefill_tps = std::atof(argv[++i]);
+    } else if (!std::strcmp(argv[i], "--sessions") && i + 1 < argc) {
+      g_sessions = std::atoi(argv[++i]);
+    } else if (!std::strcmp(argv[i], "--think-s") && i + 1 < argc) {
+      c.think_s = std::atof(argv[++i]);
+    } else if (!std::strcmp(argv[i], "--users") && i + 1 < argc) {
+      std::string u = argv[++i];
+      for (std::size_t pos = 0; pos < u.size();) {
+        const std::size_t comma = u.find(',', pos);
+        c.users.push_back(std::atoi(u.substr(pos, comma - pos).c_str()));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+      }
     }
   }
   return c;
@@ -196,8 +213,10 @@ int main(int argc, char** argv) {
   }
   const std::string mode = argv[1];
   const int config = std::atoi(argv[2]);
+  double think_override = 0.0;
   auto make_trace = [&](int users, double miss) {
-    return config == 5 ? config5(users, miss, 6.0, 505) : config4(users, miss, 10.0, 404);
+    return config == 5 ? config5(users, miss, think_override > 0 ? think_override : 6.0, 505)
+                       : config4(users, miss, think_override > 0 ? think_override : 10.0, 404);
   };
 
   if (mode == "digest") {
@@ -205,6 +224,7 @@ int main(int argc, char** argv) {
     const int users = std::atoi(argv[4]);
     const double miss = argc > 5 && argv[5][0] != '-' ? std::atof(argv[5]) : 0.0;
     const Calibration cal = parse_calibration(argc, argv, 5);
+    think_override = cal.think_s;
     const Trace tr = make_trace(users, miss);
     const RunReport rep = run_simulation(tr, make_cfg(cal, p));
     std::uint64_t h = 1469598103934665603ULL;
@@ -236,13 +256,14 @@ int main(int argc, char** argv) {
 
   if (mode == "sweep") {
     const Calibration cal = parse_calibration(argc, argv, 3);
-    const int loads[] = {32, 64, 128, 256, 384, 512};
+    think_override = cal.think_s;
+    const std::vector<int> loads = cal.users.empty() ? std::vector<int>{32, 64, 128, 256, 384, 512} : cal.users;
     const Policy policies[] = {Policy::Symphony, Policy::Retain, Policy::Swap, Policy::Recompute};
     std::printf("{\"config\": %d, \"cells\": [", config);
     bool first = true;
     for (Policy p : policies)
       for (int users : loads) {
-        if (config == 5 && users > 512) continue;
+        if (users > (g_sessions > 0 ? g_sessions : (config == 5 ? 600 : 1000))) continue;
         Cell c;
         try {
           c = summarize(run_simulation(make_trace(users, 0.0), make_cfg(cal, p)));
