@@ -226,6 +226,8 @@ typedef struct {
   uint64_t landing_pages;
   uint64_t disk_pages;
   uint64_t seed;
+  int32_t free_running; /* 0: lockstep (move at apply); 1: issue at schedule, complete at apply */
+  int32_t pad_;
 } kvs_payload_options;
 
 int kvs_cluster_create(kvs_cluster** out);
@@ -243,6 +245,10 @@ int kvs_payload_pages_in_use(kvs_payload* p, int32_t pool, uint64_t* out);
 int kvs_payload_pool_of(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t block, int32_t tier,
                         int32_t* out);
 int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7);
+/* out[0] = host ns blocked in apply waiting for the GPU (free-running),
+ * out[1] = transfers issued at schedule time, out[2..5] = pages of each pool
+ * held by moves issued but not yet applied. */
+int kvs_payload_stats(kvs_payload* p, uint64_t* out6);
 /* Process-wide default: every KvStore constructed afterwards gets a payload
  * node (node_id -> device node_id % num_devices) in cluster `c`, built from
  * `tmpl`. Lets unchanged caller stacks (the reference Simulation) run with

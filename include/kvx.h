@@ -121,6 +121,15 @@ int kvx_free(void* ptr);
 int kvx_memcpy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 /* Synchronous copy of one page to host memory (verification / debugging). */
 int kvx_read_page(const kvx_pool* pool, uint64_t page, void* host_out);
+/* Events (timing disabled) for stream-ordered completion of page moves.
+ * kvx_event_query returns KVX_OK when complete, KVX_NOT_READY otherwise. */
+#define KVX_NOT_READY 4
+int kvx_event_create(void** out);
+int kvx_event_destroy(void* event);
+int kvx_event_record(void* event, void* stream);
+int kvx_event_synchronize(void* event);
+int kvx_event_query(void* event);
+int kvx_stream_wait_event(void* stream, void* event);
 
 /* ---- page movement (K1-K3) ---------------------------------------------- */
 /* dst[i * page_bytes ...] = page(ids[i]) for i < n. ids in device memory. */

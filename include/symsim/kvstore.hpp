@@ -132,6 +132,26 @@ class TierBackend {
   // `blocks` lost their copy in `tier`; the backend frees the pages.
   virtual void tier_lost(std::uint32_t session, std::uint16_t layer, Tier tier,
                          const std::vector<std::uint32_t>& blocks) = 0;
+  // Free-running backends start a transfer's physical move when the store
+  // schedules it (its completion time is fixed by the cost model at that
+  // point) and finish it when the store applies it; `transfer_retired` comes
+  // first in apply_transfer, before the tier_gained/tier_lost reports of that
+  // transfer. Lockstep backends ignore both and move at tier_gained time.
+  struct TransferInfo {
+    std::uint64_t id = 0;
+    std::uint32_t session = 0;
+    std::uint16_t layer = 0;
+    std::uint32_t block_lo = 0, block_hi = 0;  // inclusive
+    BlockEvent kind = BlockEvent::LoadH2D;
+    Tier to = Tier::Device;
+    std::int64_t bytes = 0;
+    Ns complete_at = 0;
+  };
+  virtual void transfer_posted(const TransferInfo& t) { (void)t; }
+  virtual void transfer_retired(std::uint64_t id, bool voided) {
+    (void)id;
+    (void)voided;
+  }
   // Migration endpoints: the source froze `session`; this node imports it.
   virtual void migrating_out(std::uint32_t session) { (void)session; }
   virtual void importing(std::uint32_t session, std::int64_t tokens) {

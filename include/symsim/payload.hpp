@@ -3,8 +3,7 @@
 //
 // NodePayload implements TierBackend (kvstore.hpp): it gives every block
 // copy the state machine creates a real page and moves the bytes with the
-// kvx_* kernels / copy engines (include/kvx.h) at the moment the reference
-// semantics say the copy comes into existence:
+// kvx_* kernels / copy engines (include/kvx.h):
 //
 //   DEVICE copy  -> a page of this node's HBM pool
 //                   Created   : allocated + filled (K5 / the engine's writes)
@@ -19,13 +18,21 @@
 //   DISK copy    -> a page of the disk pool (pinned host memory standing in
 //                   for the SSD tier; copy engines)
 //
-// This is the "lockstep" mode of SURVEY.md §7 hard part 1: the event order is
-// the reference clock's (apply_transfer in (complete_at, id) order) and every
-// physical move is complete before the call returns, so block-table state is
-// bit-identical to the reference and every copy's bytes can be verified.
-// Migrated layers land in receiver-GPU memory while the ledger still says
-// Host (kvstore.cpp:914-923), which keeps ledger parity exact (SURVEY.md §7
-// hard part 2, option 1): the follow-up LoadH2D becomes an HBM->HBM copy.
+// Two modes (SURVEY.md §7 hard part 1):
+//   lockstep      every move happens inside apply_transfer, synchronously:
+//                 the simplest proof that bytes follow the state.
+//   free-running  a move is issued on the node's stream when the store
+//                 SCHEDULES it (transfer_posted), chained behind in-flight
+//                 sources with CUDA events, and completed when the store
+//                 applies it (the apply waits on the transfer's event —
+//                 "apply_transfer on CUDA-event completion").
+//                 The host only blocks if the GPU is behind the cost model's
+//                 clock; that wait is accounted in apply_wait_ns().
+// In both modes the event order is the reference clock's (apply in
+// (complete_at, id) order), so block-table state is bit-identical to the
+// reference and every copy's bytes can be verified. Migrated layers land in
+// receiver-GPU memory while the ledger still says Host (kvstore.cpp:914-923),
+// which keeps ledger parity exact (SURVEY.md §7 hard part 2, option 1).
 
 #include <cstdint>
 #include <map>
@@ -46,6 +53,7 @@ struct PayloadOptions {
   std::uint64_t disk_pages = 0;     // DISK tier stand-in (pinned host)
   std::uint64_t seed = 0;           // content of Created blocks
   int fill_mode = KVX_FILL_VALUES;
+  bool free_running = false;
 };
 
 class NodePayload;
@@ -78,6 +86,8 @@ class NodePayload final : public TierBackend {
                    const std::vector<std::uint32_t>& blocks) override;
   void tier_lost(std::uint32_t session, std::uint16_t layer, Tier tier,
                  const std::vector<std::uint32_t>& blocks) override;
+  void transfer_posted(const TransferInfo& t) override;
+  void transfer_retired(std::uint64_t id, bool voided) override;
   void migrating_out(std::uint32_t session) override;
   void importing(std::uint32_t session, std::int64_t tokens) override;
 
@@ -93,8 +103,15 @@ class NodePayload final : public TierBackend {
   int pool_of(std::uint32_t session, std::uint16_t layer, std::uint32_t block, Tier tier) const;
   // Bytes moved per BlockEvent kind since construction.
   const std::uint64_t* bytes_moved() const { return moved_; }
+  // Free-running: host nanoseconds spent waiting in apply for the GPU, and
+  // the number of transfers issued at schedule time.
+  std::uint64_t apply_wait_ns() const { return apply_wait_ns_; }
+  std::uint64_t transfers_posted() const { return posted_; }
+  // Free-running: pages of `p` held by moves issued but not yet applied.
+  std::uint64_t pages_in_flight(Pool p) const;
   kvx_pool* pool(Pool p) const { return pools_[p]; }
   void* stream() const { return stream_; }
+  void synchronize();
 
  private:
   struct Ref {
@@ -104,14 +121,28 @@ class NodePayload final : public TierBackend {
   struct Copies {
     Ref tier[3];  // indexed by Tier
   };
+  struct InFlight {  // a free-running move: pages being written by `event`
+    int tier = 0;
+    std::uint32_t session = 0;
+    std::uint16_t layer = 0;
+    std::vector<std::uint32_t> blocks;
+    std::vector<Ref> pages;
+    void* event = nullptr;
+  };
   static std::uint64_t key(std::uint32_t s, std::uint16_t l, std::uint32_t b) {
     return (static_cast<std::uint64_t>(s) << 36) | (static_cast<std::uint64_t>(l) << 20) | b;
   }
   std::uint32_t alloc(Pool p);
   void release(const Ref& r);
   Ref best_source(std::uint32_t s, std::uint16_t l, std::uint32_t b, int exclude_tier) const;
-  // Copies src pages -> dst pages (grouped by source pool) and waits.
-  void move(std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push_from_source);
+  // In-flight copy of a block (fastest tier first): page + the event that
+  // completes it; returns false if none.
+  bool inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_t b, int exclude_tier, Ref* page,
+                       void** event) const;
+  // Issues src[i] -> dst[i] copies on the runner's stream, grouped by pools.
+  void issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push);
+  void move_now(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
+                const std::vector<std::uint32_t>& blocks);
   std::uint32_t* device_ids(const std::vector<std::uint32_t>& ids, int slot);
 
   PayloadCluster* cluster_;
@@ -123,11 +154,20 @@ class NodePayload final : public TierBackend {
   std::unordered_map<std::uint64_t, Copies> blocks_;
   std::map<std::uint32_t, int> import_src_;
   void* stream_ = nullptr;
+  // Device id scratch (source / destination ids). Reuse is safe without host
+  // syncs: uploads and the kernels reading them are ordered on stream_.
   std::uint32_t* d_ids_[2] = {nullptr, nullptr};
   std::size_t d_ids_cap_[2] = {0, 0};
   void* d_tags_ = nullptr;
   std::size_t d_tags_cap_ = 0;
   std::uint64_t moved_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // free-running state
+  std::unordered_map<std::uint64_t, InFlight> inflight_;        // by transfer id
+  std::unordered_map<std::uint64_t, std::uint64_t> inflight_by_block_;  // key*4+tier -> transfer id
+  std::uint64_t applying_ = 0;
+  bool applying_valid_ = false;
+  std::uint64_t apply_wait_ns_ = 0;
+  std::uint64_t posted_ = 0;
 };
 
 }  // namespace symsim

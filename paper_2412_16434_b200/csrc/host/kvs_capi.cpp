@@ -422,6 +422,7 @@ symsim::PayloadOptions to_payload_opts(const kvs_payload_options* o) {
   p.landing_pages = o->landing_pages;
   p.disk_pages = o->disk_pages;
   p.seed = o->seed;
+  p.free_running = o->free_running != 0;
   return p;
 }
 std::map<const symsim::NodePayload*, kvs_payload> g_handles;
@@ -477,6 +478,14 @@ int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7) {
   });
 }
 
+int kvs_payload_stats(kvs_payload* p, uint64_t* out6) {
+  return guarded([&] {
+    out6[0] = p->node->apply_wait_ns();
+    out6[1] = p->node->transfers_posted();
+    for (int i = 0; i < 4; ++i) out6[2 + i] = p->node->pages_in_flight(static_cast<symsim::NodePayload::Pool>(i));
+  });
+}
+
 int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices) {
   return guarded([&] {
     if (!c || !tmpl) {
@@ -522,6 +531,7 @@ KVS_NO_PAYLOAD(kvs_payload_read_block, kvs_payload*, uint32_t, uint16_t, uint32_
 KVS_NO_PAYLOAD(kvs_payload_pages_in_use, kvs_payload*, int32_t, uint64_t*)
 KVS_NO_PAYLOAD(kvs_payload_pool_of, kvs_payload*, uint32_t, uint16_t, uint32_t, int32_t, int32_t*)
 KVS_NO_PAYLOAD(kvs_payload_bytes_moved, kvs_payload*, uint64_t*)
+KVS_NO_PAYLOAD(kvs_payload_stats, kvs_payload*, uint64_t*)
 KVS_NO_PAYLOAD(kvs_set_default_payload, kvs_cluster*, const kvs_payload_options*, int32_t)
 KVS_NO_PAYLOAD(kvs_cluster_node, kvs_cluster*, int32_t, kvs_payload**)
 }  // extern "C"

@@ -174,6 +174,22 @@ std::uint64_t KvStore::post(const Move& m, std::vector<ScheduledTransfer>& sched
   const std::uint64_t id = next_id_++;
   scheduled.push_back(ScheduledTransfer{id, m.complete_at});
   inflight_.emplace(id, m);
+  if (backend_) {
+    static const BlockEvent kEvent[] = {BlockEvent::LoadH2D,   BlockEvent::LoadDiskHost, BlockEvent::HostCopy,
+                                        BlockEvent::DiskWrite, BlockEvent::SwapOut,      BlockEvent::NetArrive};
+    static const Tier kTo[] = {Tier::Device, Tier::Host, Tier::Host, Tier::Disk, Tier::Host, Tier::Host};
+    TierBackend::TransferInfo info;
+    info.id = id;
+    info.session = m.session;
+    info.layer = m.layer;
+    info.block_lo = m.lo;
+    info.block_hi = m.hi;
+    info.kind = kEvent[static_cast<int>(m.kind)];
+    info.to = kTo[static_cast<int>(m.kind)];
+    info.bytes = m.bytes;
+    info.complete_at = m.complete_at;
+    backend_->transfer_posted(info);
+  }
   return id;
 }
 
@@ -199,7 +215,10 @@ void KvStore::clear_drop_marks(Session& s) {
 
 void KvStore::report_gain(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
                           const std::vector<std::uint32_t>& blocks) {
-  if (backend_ && !blocks.empty()) backend_->tier_gained(session, layer, tier, why, blocks);
+  // Reported even when empty for applied transfers: a free-running backend
+  // must learn that none of its in-flight pages were wanted.
+  if (backend_ && (!blocks.empty() || why != BlockEvent::Created))
+    backend_->tier_gained(session, layer, tier, why, blocks);
 }
 
 void KvStore::report_loss(std::uint32_t session, std::uint16_t layer, Tier tier,
@@ -838,6 +857,7 @@ KvStore::ApplyResult KvStore::apply_transfer(std::uint64_t id, Ns now) {
   ApplyResult res;
   res.session = m.session;
   res.layer = m.layer;
+  if (backend_) backend_->transfer_retired(id, m.voided);
   if (m.voided) {  // return the schedule-time reservation; the bytes are discarded
     if (m.kind == Kind::LoadH2D) used_[0] -= m.bytes;
     else if (m.kind != Kind::DiskWrite) used_[1] -= m.bytes;

@@ -1,6 +1,7 @@
-// NodePayload: physical pages behind KvStore's tier residency (lockstep).
-// See include/symsim/payload.hpp for the tier -> pool mapping. All CUDA work
-// goes through the kvx C ABI (include/kvx.h); this file has no CUDA headers.
+// NodePayload: physical pages behind KvStore's tier residency.
+// See include/symsim/payload.hpp for the tier -> pool mapping and the two
+// modes. All CUDA work goes through the kvx C ABI (include/kvx.h); this file
+// has no CUDA headers.
 //
 // Reference anchors for when each copy comes into existence (the hooks fire
 // from the re-implemented state machine at exactly these points):
@@ -12,10 +13,13 @@
 //   LoadH2D      demand / prefetch load   kvstore.cpp:852-861
 //   NetArrive    migration layer landing  kvstore.cpp:914-923
 //   tier_lost    purge / evict / release  kvstore.cpp:388-393, 293-295, 710-736
+// Free-running mode issues each move when the transfer is scheduled
+// (add_transfer, kvstore.cpp:180-185) and completes it at apply.
 
 #include "symsim/payload.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <stdexcept>
 #include <string>
 
@@ -25,6 +29,12 @@ namespace {
 
 void kvx_check(int rc, const char* what) {
   if (rc != KVX_OK) throw std::runtime_error(std::string("payload: ") + what + ": " + kvx_last_error());
+}
+
+std::uint64_t now_ns() {
+  return static_cast<std::uint64_t>(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+          .count());
 }
 
 }  // namespace
@@ -50,7 +60,7 @@ int PayloadCluster::take_source(std::uint32_t session) {
 }
 
 // ---------------------------------------------------------------------------
-// node
+// node: pools, pages, scratch
 
 NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOptions& opts)
     : cluster_(cluster), node_(node_id), opts_(opts) {
@@ -73,6 +83,10 @@ NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOpti
 
 NodePayload::~NodePayload() {
   if (stream_) kvx_stream_synchronize(stream_);
+  for (auto& entry : inflight_) {
+    kvx_event_synchronize(entry.second.event);
+    kvx_event_destroy(entry.second.event);
+  }
   for (auto*& p : pools_)
     if (p) kvx_pool_destroy(p);
   for (auto* d : d_ids_) kvx_free(d);
@@ -80,9 +94,18 @@ NodePayload::~NodePayload() {
   kvx_stream_destroy(stream_);
 }
 
+void NodePayload::synchronize() { kvx_check(kvx_stream_synchronize(stream_), "sync"); }
+
 std::uint64_t NodePayload::pages_in_use(Pool p) const {
   const std::uint64_t total = pools_[p] ? kvx_pool_num_pages(pools_[p]) : 0;
   return total - free_[p].size();
+}
+
+std::uint64_t NodePayload::pages_in_flight(Pool p) const {
+  std::uint64_t n = 0;
+  for (const auto& entry : inflight_)
+    for (const Ref& r : entry.second.pages) n += r.pool == p;
+  return n;
 }
 
 std::uint32_t NodePayload::alloc(Pool p) {
@@ -96,13 +119,19 @@ std::uint32_t NodePayload::alloc(Pool p) {
   return page;
 }
 
+// A freed page may still be read by work queued on this node's stream; any
+// later writer of the page is ordered behind it on the same stream (or waits
+// on a marker of it, see transfer_posted), so no host sync is needed.
 void NodePayload::release(const Ref& r) {
   if (r.pool >= 0) free_[r.pool].push_back(r.page);
 }
 
 std::uint32_t* NodePayload::device_ids(const std::vector<std::uint32_t>& ids, int slot) {
   if (ids.size() > d_ids_cap_[slot]) {
-    kvx_free(d_ids_[slot]);
+    if (d_ids_[slot]) {
+      synchronize();  // the old buffer may still be read by queued kernels
+      kvx_free(d_ids_[slot]);
+    }
     d_ids_[slot] = nullptr;
     const std::size_t cap = std::max<std::size_t>(ids.size(), 4096);
     void* p = nullptr;
@@ -125,19 +154,35 @@ NodePayload::Ref NodePayload::best_source(std::uint32_t s, std::uint16_t l, std:
   return Ref{};
 }
 
+bool NodePayload::inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_t b, int exclude_tier, Ref* page,
+                                  void** event) const {
+  for (int t = 0; t < 3; ++t) {
+    if (t == exclude_tier) continue;
+    const auto it = inflight_by_block_.find(key(s, l, b) * 4 + t);
+    if (it == inflight_by_block_.end()) continue;
+    const InFlight& f = inflight_.at(it->second);
+    for (std::size_t i = 0; i < f.blocks.size(); ++i)
+      if (f.blocks[i] == b) {
+        *page = f.pages[i];
+        *event = f.event;
+        return true;
+      }
+  }
+  return false;
+}
+
 int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier tier) const {
   const auto it = blocks_.find(key(s, l, b));
   return it == blocks_.end() ? -1 : it->second.tier[static_cast<int>(tier)].pool;
 }
 
-// Copies src[i] -> dst[i] (dst all in this node's pools), grouped by
-// (source pool, destination pool). Device-resident pairs use the SM/TMA page
-// mover; anything touching pinned host memory uses the copy engines.
-// `src_node` owns the source pools; with push_from_source the kernel runs on
-// the source node's stream and stores into this node's memory (NVLink / peer
-// path of a migration).
-void NodePayload::move(std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node,
-                       bool push_from_source) {
+// Queues src[i] -> dst[i] (dst in this node's pools) grouped by (source pool,
+// destination pool). HBM<->HBM pairs use the SM/TMA page mover with device
+// id lists; anything touching pinned host memory uses the copy engines.
+// With `push` the work runs on the source node's stream and stores into this
+// node's memory (the NVLink / peer path of a migration).
+void NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push) {
+  NodePayload& runner = push ? src_node : *this;
   for (int sp = 0; sp < 4; ++sp)
     for (int dp = 0; dp < 4; ++dp) {
       std::vector<std::uint32_t> s_ids, d_ids;
@@ -150,7 +195,6 @@ void NodePayload::move(std::vector<Ref>& src, const std::vector<Ref>& dst, NodeP
       kvx_pool* from = src_node.pools_[sp];
       kvx_pool* to = pools_[dp];
       const bool on_device = (sp == kDevicePool || sp == kLandingPool) && (dp == kDevicePool || dp == kLandingPool);
-      NodePayload& runner = push_from_source ? src_node : *this;
       if (on_device) {
         const std::uint32_t* ds = runner.device_ids(s_ids, 0);
         const std::uint32_t* dd = runner.device_ids(d_ids, 1);
@@ -159,9 +203,11 @@ void NodePayload::move(std::vector<Ref>& src, const std::vector<Ref>& dst, NodeP
         kvx_check(kvx_copy_pages(from, s_ids.data(), to, d_ids.data(), s_ids.size(), KVX_COPY_CE, runner.stream_),
                   "copy-engine copy");
       }
-      kvx_check(kvx_stream_synchronize(runner.stream_), "sync");
     }
 }
+
+// ---------------------------------------------------------------------------
+// residency transitions
 
 void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
                               const std::vector<std::uint32_t>& blocks) {
@@ -180,6 +226,7 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
     }
     const std::uint32_t* d_pages = device_ids(pages, 0);
     if (tags.size() * sizeof(kvx_block_tag) > d_tags_cap_) {
+      if (d_tags_) synchronize();
       kvx_free(d_tags_);
       d_tags_cap_ = std::max<std::size_t>(tags.size() * sizeof(kvx_block_tag), 65536);
       kvx_check(kvx_malloc(opts_.device, d_tags_cap_, &d_tags_), "tag scratch");
@@ -188,11 +235,46 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
     kvx_check(kvx_fill_pages(pools_[kDevicePool], d_pages, static_cast<const kvx_block_tag*>(d_tags_), pages.size(),
                              opts_.seed, &opts_.layout, opts_.fill_mode, stream_),
               "fill");
-    kvx_check(kvx_stream_synchronize(stream_), "sync");
+    if (!opts_.free_running) synchronize();
     return;
   }
 
-  // Where the new copy lives, and where its bytes come from.
+  if (!opts_.free_running || !applying_valid_) {
+    move_now(session, layer, tier, why, blocks);
+    return;
+  }
+
+  // Free-running: the move was issued when the transfer was scheduled and
+  // has completed (transfer_retired waited on it). Install the pages of the
+  // blocks the state machine says gained the tier; return the rest.
+  InFlight f = std::move(inflight_.at(applying_));
+  inflight_.erase(applying_);
+  applying_valid_ = false;
+  std::vector<bool> used(f.blocks.size(), false);
+  std::vector<std::uint32_t> missing;
+  for (std::uint32_t b : blocks) {
+    std::size_t i = 0;
+    while (i < f.blocks.size() && f.blocks[i] != b) ++i;
+    if (i == f.blocks.size()) {
+      missing.push_back(b);  // its source appeared only after scheduling
+      continue;
+    }
+    Copies& c = blocks_[key(session, layer, b)];
+    release(c.tier[t]);
+    c.tier[t] = f.pages[i];
+    used[i] = true;
+  }
+  for (std::size_t i = 0; i < f.blocks.size(); ++i)
+    if (!used[i]) release(f.pages[i]);
+  kvx_event_destroy(f.event);
+  if (!missing.empty()) move_now(session, layer, tier, why, missing);
+}
+
+// Lockstep move: choose each block's source now, copy, wait.
+void NodePayload::move_now(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
+                           const std::vector<std::uint32_t>& blocks) {
+  if (blocks.empty()) return;
+  const int t = static_cast<int>(tier);
   Pool dest = kDevicePool;
   NodePayload* src_node = this;
   bool push = false;
@@ -205,7 +287,6 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
     src_node = cluster_->node(it->second);
     push = true;
   }
-
   std::vector<Ref> src, dst;
   for (std::uint32_t b : blocks) {
     const Ref from = src_node->best_source(session, layer, b, src_node == this ? t : -1);
@@ -219,7 +300,12 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
     src.push_back(from);
     dst.push_back(c.tier[t]);
   }
-  move(src, dst, *src_node, push);
+  if (push) {  // queued free-running work on either side lands first
+    src_node->synchronize();
+    synchronize();
+  }
+  issue(src, dst, *src_node, push);
+  (push ? *src_node : *this).synchronize();
 }
 
 void NodePayload::tier_lost(std::uint32_t session, std::uint16_t layer, Tier tier,
@@ -234,6 +320,99 @@ void NodePayload::tier_lost(std::uint32_t session, std::uint16_t layer, Tier tie
     if (c.tier[0].pool < 0 && c.tier[1].pool < 0 && c.tier[2].pool < 0) blocks_.erase(it);
   }
 }
+
+// ---------------------------------------------------------------------------
+// free-running: issue at schedule time, complete at apply
+
+void NodePayload::transfer_posted(const TransferInfo& tr) {
+  if (!opts_.free_running) return;
+  const int t = static_cast<int>(tr.to);
+  Pool dest = kDevicePool;
+  if (tr.to == Tier::Host) dest = tr.kind == BlockEvent::NetArrive ? kLandingPool : kHostPool;
+  if (tr.to == Tier::Disk) dest = kDiskPool;
+  NodePayload* src_node = this;
+  bool push = false;
+  if (tr.kind == BlockEvent::NetArrive) {
+    const auto it = import_src_.find(tr.session);
+    if (it == import_src_.end() || !cluster_ || !cluster_->node(it->second)) return;  // apply falls back
+    src_node = cluster_->node(it->second);
+    push = true;
+  }
+  InFlight f;
+  f.tier = t;
+  f.session = tr.session;
+  f.layer = tr.layer;
+  std::vector<Ref> src, dst;
+  std::vector<void*> waits;
+  for (std::uint64_t b64 = tr.block_lo; b64 <= tr.block_hi; ++b64) {
+    const auto b = static_cast<std::uint32_t>(b64);
+    const auto have = blocks_.find(key(tr.session, tr.layer, b));
+    if (have != blocks_.end() && have->second.tier[t].pool >= 0) continue;  // already there
+    if (inflight_by_block_.count(key(tr.session, tr.layer, b) * 4 + t)) continue;  // already coming
+    const int exclude = src_node == this ? t : -1;
+    Ref from = src_node->best_source(tr.session, tr.layer, b, exclude);
+    if (from.pool < 0) {  // chained behind a move still in flight on the source side
+      void* ev = nullptr;
+      if (!src_node->inflight_source(tr.session, tr.layer, b, exclude, &from, &ev)) continue;
+      waits.push_back(ev);
+    }
+    src.push_back(from);
+    dst.push_back(Ref{static_cast<std::int8_t>(dest), alloc(dest)});
+    f.blocks.push_back(b);
+    f.pages.push_back(dst.back());
+  }
+  if (f.blocks.empty()) return;
+  NodePayload& runner = push ? *src_node : *this;
+  if (push) {  // the source writes our pages: order it after our queued reads of recycled pages
+    void* marker = nullptr;
+    kvx_check(kvx_event_create(&marker), "event");
+    kvx_check(kvx_event_record(marker, stream_), "event record");
+    kvx_check(kvx_stream_wait_event(runner.stream_, marker), "stream wait");
+    kvx_event_destroy(marker);
+  }
+  std::sort(waits.begin(), waits.end());
+  waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
+  for (void* ev : waits) kvx_check(kvx_stream_wait_event(runner.stream_, ev), "stream wait");
+  issue(src, dst, *src_node, push);
+  kvx_check(kvx_event_create(&f.event), "event");
+  kvx_check(kvx_event_record(f.event, runner.stream_), "event record");
+  for (std::uint32_t b : f.blocks) inflight_by_block_[key(tr.session, tr.layer, b) * 4 + t] = tr.id;
+  moved_[7] += f.blocks.size() * page_bytes_;  // bytes issued ahead of their apply
+  inflight_.emplace(tr.id, std::move(f));
+  ++posted_;
+}
+
+void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
+  applying_valid_ = false;
+  if (!opts_.free_running) return;
+  const auto it = inflight_.find(id);
+  if (it == inflight_.end()) return;
+  InFlight& f = it->second;
+  if (kvx_event_query(f.event) == KVX_NOT_READY) {  // the GPU is behind the model clock
+    const std::uint64_t t0 = now_ns();
+    kvx_check(kvx_event_synchronize(f.event), "event sync");
+    apply_wait_ns_ += now_ns() - t0;
+  }
+  // Later work on this node is ordered after the move (it may have run on a
+  // peer's stream).
+  kvx_check(kvx_stream_wait_event(stream_, f.event), "stream wait");
+  for (std::uint32_t b : f.blocks) {
+    const auto k = key(f.session, f.layer, b) * 4 + f.tier;
+    const auto jt = inflight_by_block_.find(k);
+    if (jt != inflight_by_block_.end() && jt->second == id) inflight_by_block_.erase(jt);
+  }
+  if (voided) {
+    for (const Ref& r : f.pages) release(r);
+    kvx_event_destroy(f.event);
+    inflight_.erase(it);
+    return;
+  }
+  applying_ = id;
+  applying_valid_ = true;
+}
+
+// ---------------------------------------------------------------------------
+// migration endpoints, verification
 
 void NodePayload::migrating_out(std::uint32_t session) {
   if (cluster_) cluster_->note_source(session, node_);
@@ -251,6 +430,7 @@ bool NodePayload::read_block(std::uint32_t session, std::uint16_t layer, std::ui
   if (it == blocks_.end()) return false;
   const Ref r = it->second.tier[static_cast<int>(tier)];
   if (r.pool < 0) return false;
+  synchronize();
   kvx_check(kvx_read_page(pools_[r.pool], r.page, out), "read page");
   return true;
 }

@@ -234,3 +234,43 @@ int kvx_read_page(const kvx_pool* pool, uint64_t page, void* host_out) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int kvx_event_create(void** out) {
+  if (!out) return kvx::fail_arg("kvx_event_create: null out");
+  cudaEvent_t e = nullptr;
+  KVX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "kvx_event_create");
+  *out = e;
+  return KVX_OK;
+}
+
+int kvx_event_destroy(void* event) {
+  if (event) KVX_CUDA_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(event)), "kvx_event_destroy");
+  return KVX_OK;
+}
+
+int kvx_event_record(void* event, void* stream) {
+  KVX_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)), "kvx_event_record");
+  return KVX_OK;
+}
+
+int kvx_event_synchronize(void* event) {
+  KVX_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(event)), "kvx_event_synchronize");
+  return KVX_OK;
+}
+
+int kvx_event_query(void* event) {
+  const cudaError_t e = cudaEventQuery(static_cast<cudaEvent_t>(event));
+  if (e == cudaErrorNotReady) return KVX_NOT_READY;
+  KVX_CUDA_TRY(e, "kvx_event_query");
+  return KVX_OK;
+}
+
+int kvx_stream_wait_event(void* stream, void* event) {
+  KVX_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0),
+               "kvx_stream_wait_event");
+  return KVX_OK;
+}
+
+}  // extern "C"

@@ -112,7 +112,8 @@ class _PayloadOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("block_tokens", C.c_int32), ("dtype", C.c_int32), ("fill_mode", C.c_int32),
                 ("device_pages", C.c_uint64), ("host_pages", C.c_uint64), ("landing_pages", C.c_uint64),
-                ("disk_pages", C.c_uint64), ("seed", C.c_uint64)]
+                ("disk_pages", C.c_uint64), ("seed", C.c_uint64), ("free_running", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 @dataclass
@@ -270,6 +271,7 @@ def load_kvs_library(path: Optional[str] = None) -> C.CDLL:
         "kvs_payload_pages_in_use": ([C.c_void_p, C.c_int32, P(C.c_uint64)], C.c_int),
         "kvs_payload_pool_of": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, C.c_int32, P(C.c_int32)], C.c_int),
         "kvs_payload_bytes_moved": ([C.c_void_p, P(C.c_uint64)], C.c_int),
+        "kvs_payload_stats": ([C.c_void_p, P(C.c_uint64)], C.c_int),
         "kvs_set_default_payload": ([C.c_void_p, P(_PayloadOpts), C.c_int32], C.c_int),
         "kvs_cluster_node": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
     }
@@ -562,11 +564,12 @@ class PayloadOptions:
     landing_pages: int = 0
     disk_pages: int = 0
     seed: int = 0
+    free_running: bool = False
 
     def _c(self) -> "_PayloadOpts":
         return _PayloadOpts(self.device, self.num_kv_heads, self.head_dim, self.block_tokens, self.dtype,
                             self.fill_mode, self.device_pages, self.host_pages, self.landing_pages,
-                            self.disk_pages, self.seed)
+                            self.disk_pages, self.seed, int(self.free_running), 0)
 
     def page_bytes(self) -> int:
         return 2 * self.num_kv_heads * self.block_tokens * self.head_dim * (2 if self.dtype == 1 else 4)
@@ -643,3 +646,8 @@ class NodePayload:
         out = (C.c_uint64 * 7)()
         _check(self._lib, self._lib.kvs_payload_bytes_moved(self._h, out))
         return dict(zip(BLOCK_EVENTS, list(out)))
+
+    def stats(self) -> Dict[str, int]:
+        out = (C.c_uint64 * 6)()
+        _check(self._lib, self._lib.kvs_payload_stats(self._h, out))
+        return {"apply_wait_ns": out[0], "transfers_posted": out[1], "in_flight": list(out[2:6])}

@@ -91,10 +91,13 @@ const char* tier_s(Tier t) { return tier_name(t); }
 int main(int argc, char** argv) {
   std::int64_t device_pages = 0;
   std::string policy = "symphony";
+  bool free_running = false;
   for (int i = 1; i < argc; ++i) {
     if (!std::strcmp(argv[i], "--device-pages") && i + 1 < argc) device_pages = std::atoll(argv[++i]);
     if (!std::strcmp(argv[i], "--policy") && i + 1 < argc) policy = argv[++i];
+    if (!std::strcmp(argv[i], "--free-running")) free_running = true;
   }
+  (void)free_running;
   RunConfig cfg;
   cfg.policy = policy_from(policy);
   cfg.num_nodes = 2;
@@ -118,6 +121,7 @@ int main(int argc, char** argv) {
   po.landing_pages = 4096;
   po.disk_pages = 8192;
   po.seed = kSeed;
+  po.free_running = free_running;
   set_default_tier_backend_factory([&](int node_id) -> TierBackend* {
     nodes.push_back(std::make_unique<NodePayload>(&cluster, node_id, po));
     return nodes.back().get();
@@ -173,6 +177,8 @@ int main(int argc, char** argv) {
     for (int p = 0; p < 4; ++p)
       if (node->pages_in_use(static_cast<NodePayload::Pool>(p)) != pages_held[p]) ++bad;  // leak or loss
     const std::uint64_t* mv = node->bytes_moved();
+    std::printf("payload node %d posted %" PRIu64 " apply_wait_us %.1f\n", n, node->transfers_posted(),
+                node->apply_wait_ns() / 1e3);
     std::printf("payload node %d pages dev %zu host %zu landing %zu disk %zu moved created %" PRIu64
                 " h2d %" PRIu64 " host_copy %" PRIu64 " disk_write %" PRIu64 " net_arrive %" PRIu64 "\n",
                 n, pages_held[0], pages_held[1], pages_held[2], pages_held[3], mv[0], mv[1], mv[3], mv[4], mv[6]);

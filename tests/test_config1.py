@@ -31,6 +31,7 @@ VARIANTS = {
     "dev40": ["--device-pages", "40"],
     "swap": ["--policy", "swap"],
 }
+MODES = {"lockstep": [], "free-running": ["--free-running"]}
 
 
 def _state_lines(text):
@@ -53,11 +54,13 @@ def test_golden_has_migrations_and_purges():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", list(MODES))
 @pytest.mark.parametrize("variant", list(VARIANTS))
-def test_config1_trace_with_real_pages(variant):
+def test_config1_trace_with_real_pages(variant, mode):
     if not PROD_BIN.exists():
         pytest.skip("oracle/_ref/payload_sim not built (needs the reference sources; build here and ship)")
-    proc = subprocess.run([str(PROD_BIN), *VARIANTS[variant]], capture_output=True, text=True, timeout=600)
+    proc = subprocess.run([str(PROD_BIN), *VARIANTS[variant], *MODES[mode]], capture_output=True, text=True,
+                          timeout=600)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     assert _state_lines(proc.stdout) == _state_lines((GOLDEN / f"config1_{variant}.txt").read_text())
     summary = [ln for ln in proc.stdout.splitlines() if ln.startswith("payload verified_copies")][0]

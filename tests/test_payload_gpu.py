@@ -1,4 +1,4 @@
-"""Physical payload behind the store, on the B200 (lockstep mode).
+"""Physical payload behind the store, on the B200 (lockstep and free-running).
 
 A KvStore with a NodePayload attached gives every tier copy a real page; the
 transfers the state machine schedules move real bytes when they are applied
@@ -33,10 +33,13 @@ def tiny_profile():
     return K.GpuProfile(kv_bytes_per_token=LAYERS * 2 * 4 * 64 * 4, num_layers=LAYERS, hbm_capacity=10**12)
 
 
-def payload_opts(device_pages=64, host_pages=64, landing_pages=64, disk_pages=128):
+def payload_opts(device_pages=64, host_pages=64, landing_pages=64, disk_pages=128, free_running=False):
     return K.PayloadOptions(device=0, num_kv_heads=4, head_dim=64, block_tokens=16, dtype=0, fill_mode=1,
                             device_pages=device_pages, host_pages=host_pages, landing_pages=landing_pages,
-                            disk_pages=disk_pages, seed=SEED)
+                            disk_pages=disk_pages, seed=SEED, free_running=free_running)
+
+
+MODES = pytest.mark.parametrize("free_running", [False, True], ids=["lockstep", "free-running"])
 
 
 @pytest.fixture(scope="module")
@@ -82,8 +85,10 @@ def verify(store, node, sessions, landing_ok=True):
                         assert np.array_equal(got, expected(s, l, b, pb)), f"s{s} l{l} b{b} tier {t}: bytes differ"
                     else:
                         assert pool < 0, f"s{s} l{l} b{b}: tier {t} not resident but holds a page"
+    in_flight = node.stats()["in_flight"]  # free-running: moves issued, not yet applied
     for p in range(4):
-        assert node.pages_in_use(p) == held[p], f"pool {p}: {node.pages_in_use(p)} pages in use, {held[p]} accounted"
+        assert node.pages_in_use(p) == held[p] + in_flight[p], \
+            f"pool {p}: {node.pages_in_use(p)} pages in use, {held[p]} resident + {in_flight[p]} in flight"
 
 
 class Pump:
@@ -101,16 +106,18 @@ class Pump:
         return out
 
 
-def make_node(opts_kw=None, **store_kw):
+def make_node(opts_kw=None, free_running=False, **store_kw):
     cluster = K.PayloadCluster()
     store = K.KvStore(gpu=tiny_profile(), opts=K.Options(**store_kw))
-    node = K.NodePayload(cluster, store_kw.get("node_id", 0), payload_opts(**(opts_kw or {})))
+    node = K.NodePayload(cluster, store_kw.get("node_id", 0),
+                         payload_opts(free_running=free_running, **(opts_kw or {})))
     node.attach(store)
     return cluster, store, node
 
 
-def test_write_behind_purge_reload(dev):
-    cluster, store, node = make_node()
+@MODES
+def test_write_behind_purge_reload(dev, free_running):
+    cluster, store, node = make_node(free_running=free_running)
     pump = Pump(store)
     for s in (1, 2):
         store.register_session(s, f"s{s}")
@@ -137,8 +144,9 @@ def test_write_behind_purge_reload(dev):
     assert sum(node.pages_in_use(p) for p in range(4)) == 0
 
 
-def test_swap_offload_and_reactivation(dev):
-    cluster, store, node = make_node(write_behind=False)
+@MODES
+def test_swap_offload_and_reactivation(dev, free_running):
+    cluster, store, node = make_node(free_running=free_running, write_behind=False)
     pump = Pump(store)
     store.register_session(1, "a")
     store.register_session(2, "b")
@@ -158,7 +166,8 @@ def test_swap_offload_and_reactivation(dev):
     assert not store.fully_device_resident(2) and store.has_any_copy(2)
 
 
-def test_migration_lands_in_receiver_hbm(dev):
+@MODES
+def test_migration_lands_in_receiver_hbm(dev, free_running):
     """import_migration on node 1 pulls the frozen session from node 0: each
     layer's NetArrive lands in node 1's HBM landing pool (HOST tier in the
     ledger, reference kvstore.cpp:914-923); the follow-up demand load is an
@@ -167,7 +176,7 @@ def test_migration_lands_in_receiver_hbm(dev):
     stores, nodes, pumps = [], [], []
     for n in range(2):
         st = K.KvStore(gpu=tiny_profile(), opts=K.Options(node_id=n))
-        nd = K.NodePayload(cluster, n, payload_opts())
+        nd = K.NodePayload(cluster, n, payload_opts(free_running=free_running))
         nd.attach(st)
         st.register_session(5, "mig")
         st.finalize_sessions()
@@ -193,12 +202,14 @@ def test_migration_lands_in_receiver_hbm(dev):
     assert nodes[1].bytes_moved()["net_arrive"] == 2 * 5 * stores[1].layer_block_bytes()
 
 
+@MODES
 @pytest.mark.parametrize("seed", [1, 2, 3])
 @pytest.mark.parametrize("write_behind", [True, False])
-def test_randomized_lifecycle_keeps_bytes_and_state_consistent(dev, seed, write_behind):
+def test_randomized_lifecycle_keeps_bytes_and_state_consistent(dev, seed, write_behind, free_running):
     rng = random.Random(seed * 7 + write_behind)
     pb = 2 * 4 * 16 * 64 * 4
     cluster, store, node = make_node(opts_kw=dict(device_pages=96, host_pages=96, disk_pages=400),
+                                     free_running=free_running,
                                      write_behind=write_behind, device_capacity=pb * 2 * 24,
                                      host_capacity=pb * 2 * 20)
     pump = Pump(store)
