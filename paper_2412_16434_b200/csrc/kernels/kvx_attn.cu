@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kD = 128;          // head_dim of the fast path
 constexpr int kT = 16;           // block_tokens of the fast path
-constexpr int kWarps = 4;        // warps per CTA, each streams its own pages
+constexpr int kWarps = 4;        // warps per CTA (wide grids); 8 when the grid is one wave
 // cp.async ring depth per warp: 3 stages (96 KiB/CTA, 2 CTAs/SM). A 6-stage
 // variant (1 CTA/SM, 5 pages in flight per warp) was measured slower at
 // batch 1 and 8 (profiles/r01_summary.md): small batches are bound by the
@@ -37,7 +37,7 @@ constexpr int kWarps = 4;        // warps per CTA, each streams its own pages
 constexpr int kStagesWide = 3;
 constexpr int kTileBytes = kT * kD * 2;  // one kv head's K (or V) in a page: 4 KiB
 constexpr int kStageBytes = 2 * kTileBytes;
-constexpr int smem_bytes(int stages) { return kWarps * stages * kStageBytes; }
+constexpr int smem_bytes(int stages, int warps) { return warps * stages * kStageBytes; }
 constexpr int kMaxPagesPerCta = 1024;  // block-table slice staged in smem (4 KiB)
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -90,8 +90,9 @@ struct AttnArgs {
   float scale_log2;
 };
 
-template <int kStages>
-__global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
+// W warps per CTA, each streaming its own pages through a kStages ring.
+template <int kStages, int W>
+__global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t s_pages[kMaxPagesPerCta];
   __shared__ int s_last;
@@ -133,13 +134,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
 
   uint8_t* ring = smem + warp * (kStages * kStageBytes);
   const uint32_t ring_s = smem_u32(ring);
-  // This warp's pages: p_begin + warp, + kWarps, ...
+  // This warp's pages: p_begin + warp, + W, ...
   const int my_first = p_begin + warp;
-  const int my_count = my_first < p_end ? (p_end - my_first + kWarps - 1) / kWarps : 0;
+  const int my_count = my_first < p_end ? (p_end - my_first + W - 1) / W : 0;
 
   auto issue = [&](int i) {  // page i of this warp -> stage i % kStages
     if (i < my_count) {
-      const int p = my_first + i * kWarps;
+      const int p = my_first + i * W;
       const uint8_t* page = a.pool + static_cast<uint64_t>(s_pages[p - p_begin]) * a.page_bytes;
       const uint8_t* k_src = page + static_cast<uint64_t>(h) * kTileBytes;
       const uint8_t* v_src = page + static_cast<uint64_t>(a.heads + h) * kTileBytes;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
     __syncwarp();
     const uint32_t ks = ring_s + (i % kStages) * kStageBytes;
     const uint32_t vs = ks + kTileBytes;
-    const int tok0 = (my_first + i * kWarps) * kT;
+    const int tok0 = (my_first + i * W) * kT;
 
     // S^T[head][tok] = Q . K^T, two n-tiles of 8 tokens.
     // Even and odd k-steps accumulate separately: four independent mma
@@ -215,12 +216,16 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
     }
     l_r = l_r * corr + (p[0][0] + p[0][1] + p[1][0] + p[1][1]);
     l_r8 = l_r8 * corr8 + (p[0][2] + p[0][3] + p[1][2] + p[1][3]);
+    // Rescale O only when some row's running max moved (corr == 1 exactly
+    // otherwise): after the first pages the max rarely changes.
+    if (__any_sync(0xffffffffu, corr != 1.f || corr8 != 1.f)) {
 #pragma unroll
-    for (int n = 0; n < kD / 8; ++n) {
-      o[n][0] *= corr;
-      o[n][1] *= corr;
-      o[n][2] *= corr8;
-      o[n][3] *= corr8;
+      for (int n = 0; n < kD / 8; ++n) {
+        o[n][0] *= corr;
+        o[n][1] *= corr;
+        o[n][2] *= corr8;
+        o[n][3] *= corr8;
+      }
     }
     // O[head][d] += P[head][tok] . V[tok][d]; P straight from the S fragments.
     uint32_t pa[4];
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
   // Combine the 4 warps of the CTA through shared memory (reusing the rings).
   __syncthreads();
   float* so = reinterpret_cast<float*>(smem);                   // [warp][16][128]
-  float* sml = so + kWarps * 16 * kD;                           // [warp][16][2]
+  float* sml = so + W * 16 * kD;                                // [warp][16][2]
   {
     const int r = lane >> 2, c = (lane & 3) * 2;
     float* ow = so + warp * 16 * kD;
@@ -273,11 +278,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) attn_bf16_d128(AttnArgs a) {
     const int r = e / kD, d = e - r * kD;
     float M = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
+    for (int w = 0; w < W; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
     const float Mb = M == -INFINITY ? 0.f : M;
     float L = 0.f, O = 0.f;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < W; ++w) {
       const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
       L += f * sml[(w * 16 + r) * 2 + 1];
       O += f * so[(w * 16 + r) * kD + d];
@@ -406,18 +411,19 @@ bool fast_path(const kvx_page_layout* l) {
   return l->dtype == KVX_DTYPE_BF16 && l->head_dim == kD && l->block_tokens == kT;
 }
 
-// Split-K factor. Measured on B200 (profiles/r01_summary.md, split sweep at
-// ctx 8192): the best choice puts about one CTA per SM — batch 1 x 8 kv heads
-// -> 16 splits, batch 8 -> 2, batch 64 -> 1 — so the rule is the largest
-// split count with (requests x kv heads x splits) <= SM count, bounded by
-// the block-table staging limit and by >= 16 pages per CTA.
+// Split-K factor, from the B200 split sweeps (profiles/r01_summary.md, ctx
+// 8192): the largest split count with (requests x kv heads x splits) <= half
+// the SM count, bounded by the block-table staging limit and by >= 16 pages
+// per CTA.
 int choose_splits(int batch, int heads, int max_ctx, int requested, int sms) {
   const int pages = std::max(1, (max_ctx + kT - 1) / kT);
   const int min_splits = (pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
   if (requested > 0) return std::max(requested, min_splits);
   const int max_splits = std::max(min_splits, pages / (kWarps * 4));
   const long base = std::max(1L, static_cast<long>(batch) * heads);
-  const int fill = static_cast<int>(std::max(1L, sms / base));
+  // One-wave grids run 8 warps per CTA; measured best there at ~half an SM
+  // count of CTAs (batch 1 -> 9 splits, batch 8 -> 1).
+  const int fill = static_cast<int>(std::max(1L, sms / (2 * base)));
   return std::max(min_splits, std::min(max_splits, std::min(fill, 256)));
 }
 
@@ -454,9 +460,13 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
   if (kvx::fast_path(layout) && group <= 16) {
     static bool configured = false;
     if (!configured) {
-      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide>,
+      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide, 4>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kvx::smem_bytes(kvx::kStagesWide)),
+                                        kvx::smem_bytes(kvx::kStagesWide, 4)),
+                   "kvx_decode_attention: smem attribute");
+      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide, 8>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kvx::smem_bytes(kvx::kStagesWide, 8)),
                    "kvx_decode_attention: smem attribute");
       configured = true;
     }
@@ -482,7 +492,13 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
       a.arrivals = reinterpret_cast<uint32_t*>(a.part_ml + rows * splits * 2);
     }
     dim3 grid(splits, H, batch);
-    kvx::attn_bf16_d128<kvx::kStagesWide><<<grid, kvx::kWarps * 32, kvx::smem_bytes(kvx::kStagesWide), st>>>(a);
+    // One wave or less: 8 warps per CTA (two per scheduler) halve each warp's
+    // serial page chain; otherwise 4 warps and 2 CTAs per SM.
+    const long ctas = static_cast<long>(splits) * H * batch;
+    if (ctas <= kvx::sm_count(pool->device))
+      kvx::attn_bf16_d128<kvx::kStagesWide, 8><<<grid, 8 * 32, kvx::smem_bytes(kvx::kStagesWide, 8), st>>>(a);
+    else
+      kvx::attn_bf16_d128<kvx::kStagesWide, 4><<<grid, 4 * 32, kvx::smem_bytes(kvx::kStagesWide, 4), st>>>(a);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");
     return KVX_OK;
   }
