@@ -263,7 +263,7 @@ bool KvStore::evict_host_lru(std::int64_t bytes_needed, Ns now) {
         if ((lay[b] & kBacked) == kBacked) {
           lay[b] = static_cast<std::uint8_t>(lay[b] & ~kOnHost);
           got += page_bytes_;
-          dropped.push_back(static_cast<std::uint32_t>(b));
+          if (backend_) dropped.push_back(static_cast<std::uint32_t>(b));
         }
       report_loss(idx, static_cast<std::uint16_t>(l), Tier::Host, dropped);
     }
@@ -364,18 +364,21 @@ std::vector<BlockKey> KvStore::append_blocks(std::uint32_t session, std::int64_t
     throw std::logic_error("append_blocks: device capacity exceeded (missing reservation)");
 
   created.reserve(static_cast<std::size_t>(fresh * layers));
-  std::vector<std::uint32_t> range(fresh);
-  for (std::uint32_t i = 0; i < fresh; ++i) range[i] = first + i;
+  std::vector<std::uint32_t> range;
+  if (backend_)
+    for (std::uint32_t b = first; b < last; ++b) range.push_back(b);
   for (int l = 0; l < layers; ++l) {
     Layer& lay = s.layers[static_cast<std::size_t>(l)];
     lay.resize(last);
     std::vector<std::uint32_t> lost[3];
     for (std::uint32_t b = first; b < last; ++b) {
-      for (unsigned t = 1; t < 3; ++t)
-        if (lay[b] & (1u << t)) lost[t].push_back(b);
+      if (backend_)
+        for (unsigned t = 1; t < 3; ++t)
+          if (lay[b] & (1u << t)) lost[t].push_back(b);
       lay[b] = static_cast<std::uint8_t>((lay[b] & ~kResidency) | kOnDev);
       created.push_back(BlockKey{session, static_cast<std::uint16_t>(l), b});
     }
+    if (!backend_) continue;
     report_loss(session, static_cast<std::uint16_t>(l), Tier::Host, lost[1]);
     report_loss(session, static_cast<std::uint16_t>(l), Tier::Disk, lost[2]);
     report_gain(session, static_cast<std::uint16_t>(l), Tier::Device, BlockEvent::Created, range);
@@ -490,7 +493,7 @@ std::int64_t KvStore::purge_from_device(std::int64_t bytes_needed, Ns now, bool 
           used_[0] -= page_bytes_;
           freed += page_bytes_;
           instant[k - head] += page_bytes_;
-          dropped[k - head].push_back(static_cast<std::uint32_t>(b));
+          if (backend_) dropped[k - head].push_back(static_cast<std::uint32_t>(b));
         } else if (opts_.write_behind) {
           f |= kDropOnPersist;  // its persist is in flight; drop when it lands
         } else {
@@ -512,8 +515,10 @@ std::int64_t KvStore::purge_from_device(std::int64_t bytes_needed, Ns now, bool 
     for (std::size_t k = head; k < tail; ++k) {
       if (instant[k - head] == 0) continue;
       const Layer& lay = sessions_[runs[k].session].layers[runs[k].layer];
-      std::vector<std::uint32_t> ascending(dropped[k - head].rbegin(), dropped[k - head].rend());
-      report_loss(runs[k].session, runs[k].layer, Tier::Device, ascending);
+      if (backend_) {
+        std::vector<std::uint32_t> ascending(dropped[k - head].rbegin(), dropped[k - head].rend());
+        report_loss(runs[k].session, runs[k].layer, Tier::Device, ascending);
+      }
       const bool on_host = std::any_of(lay.begin(), lay.end(), [](std::uint8_t f) { return (f & kOnHost) != 0; });
       log(now, runs[k].session, runs[k].layer, runs[k].layer, Tier::Device, on_host ? Tier::Host : Tier::Disk,
           instant[k - head], TransferReason::Purge);
@@ -542,17 +547,19 @@ std::optional<LoadPlan> KvStore::plan_layerwise_load(std::uint32_t session, Ns n
   clear_drop_marks(s);
 
   // Dry run: bytes to reserve, and every block with no source at all.
-  std::int64_t need = 0;
+  // (Counters are locals: stores through uint8_t flags alias any member.)
+  std::int64_t need_blocks = 0;
   std::string missing;
   for (int l = 0; l < layers; ++l) {
     const Layer& lay = s.layers[static_cast<std::size_t>(l)];
+    const bool inbound = s.inbound_eta[static_cast<std::size_t>(l)] != 0;
     for (std::size_t b = 0; b < lay.size(); ++b) {
       if (lay[b] & (kOnDev | kLoadPending)) continue;
-      need += page_bytes_;
-      if (!(lay[b] & kBacked) && s.inbound_eta[static_cast<std::size_t>(l)] == 0)
-        missing += " " + std::to_string(l) + ":" + std::to_string(b);
+      ++need_blocks;
+      if (!(lay[b] & kBacked) && !inbound) missing += " " + std::to_string(l) + ":" + std::to_string(b);
     }
   }
+  const std::int64_t need = need_blocks * page_bytes_;
   if (!missing.empty())
     throw std::runtime_error("plan_layerwise_load: session " + s.name + " missing layer:block" + missing);
   if (need > device_cap_ - used_[0]) return std::nullopt;
@@ -562,7 +569,7 @@ std::optional<LoadPlan> KvStore::plan_layerwise_load(std::uint32_t session, Ns n
     const auto li = static_cast<std::size_t>(l);
     Layer& lay = s.layers[li];
     const Ns ready = s.load_eta[li] > 0 ? std::max(now, s.load_eta[li]) : now;
-    std::int64_t src_bytes[3] = {0, 0, 0};  // [host, disk, inbound]
+    std::int64_t src_blocks[3] = {0, 0, 0};  // [host, disk, inbound]
     std::uint32_t lo = 0, hi = 0;
     bool any = false;
     for (std::size_t b = 0; b < lay.size(); ++b) {
@@ -572,8 +579,10 @@ std::optional<LoadPlan> KvStore::plan_layerwise_load(std::uint32_t session, Ns n
       hi = static_cast<std::uint32_t>(b);
       any = true;
       f |= kLoadPending;
-      src_bytes[(f & kOnHost) ? 0 : (f & kOnDisk) ? 1 : 2] += page_bytes_;
+      ++src_blocks[(f & kOnHost) ? 0 : (f & kOnDisk) ? 1 : 2];
     }
+    const std::int64_t src_bytes[3] = {src_blocks[0] * page_bytes_, src_blocks[1] * page_bytes_,
+                                       src_blocks[2] * page_bytes_};
     if (!any) {
       plan.layer_ready[li] = ready;
       continue;
@@ -625,7 +634,7 @@ PromoteResult KvStore::promote(std::uint32_t session, Ns now, std::vector<Schedu
   for (int l = 0; l < gpu_.num_layers; ++l) {
     const auto li = static_cast<std::size_t>(l);
     Layer& lay = s.layers[li];
-    std::int64_t host_bytes = 0, disk_bytes = 0;
+    std::int64_t host_blocks = 0, disk_blocks = 0;
     std::uint32_t lo = 0, hi = 0;
     bool any = false;
     for (std::size_t b = 0; b < lay.size(); ++b) {
@@ -634,8 +643,9 @@ PromoteResult KvStore::promote(std::uint32_t session, Ns now, std::vector<Schedu
       if (!any) lo = static_cast<std::uint32_t>(b);
       hi = static_cast<std::uint32_t>(b);
       any = true;
-      ((f & kOnHost) ? host_bytes : disk_bytes) += page_bytes_;
+      ++((f & kOnHost) ? host_blocks : disk_blocks);
     }
+    const std::int64_t host_bytes = host_blocks * page_bytes_, disk_bytes = disk_blocks * page_bytes_;
     if (!any) {
       if (!device_full) ++res.device_layers;
       continue;
@@ -692,10 +702,10 @@ PromoteResult KvStore::promote(std::uint32_t session, Ns now, std::vector<Schedu
 void KvStore::offload_session(std::uint32_t session, Ns now, std::vector<ScheduledTransfer>& scheduled) {
   Session& s = sess(session);
   s.last_use = now;
-  std::int64_t unbacked = 0;
+  std::int64_t unbacked_blocks = 0;
   for (const Layer& lay : s.layers)
-    for (std::uint8_t f : lay)
-      if ((f & kOnDev) && !(f & kBacked)) unbacked += page_bytes_;
+    for (std::uint8_t f : lay) unbacked_blocks += (f & kOnDev) && !(f & kBacked);
+  const std::int64_t unbacked = unbacked_blocks * page_bytes_;
   if (unbacked > 0 && !make_host_room(unbacked, now)) {
     // HOST cannot take it: drop the cache outright (from == to marks a drop).
     const std::int64_t dropped = footprint(s);
@@ -716,7 +726,7 @@ void KvStore::offload_session(std::uint32_t session, Ns now, std::vector<Schedul
         f = static_cast<std::uint8_t>(f & ~kOnDev);
         used_[0] -= page_bytes_;
         demoted += page_bytes_;
-        gone.push_back(static_cast<std::uint32_t>(b));
+        if (backend_) gone.push_back(static_cast<std::uint32_t>(b));
       } else {
         if (!any) lo = static_cast<std::uint32_t>(b);
         hi = static_cast<std::uint32_t>(b);
@@ -753,14 +763,21 @@ void KvStore::release_session(std::uint32_t session, Ns now) {
     if (entry.second.session == session) entry.second.voided = true;
   std::int64_t held[3] = {0, 0, 0};
   for (std::size_t l = 0; l < s.layers.size(); ++l) {
+    std::int64_t count[3] = {0, 0, 0};
     std::vector<std::uint32_t> lost[3];
-    for (std::size_t b = 0; b < s.layers[l].size(); ++b)
-      for (unsigned t = 0; t < 3; ++t)
-        if (s.layers[l][b] & (1u << t)) {
-          held[t] += page_bytes_;
-          lost[t].push_back(static_cast<std::uint32_t>(b));
-        }
-    for (unsigned t = 0; t < 3; ++t) report_loss(session, static_cast<std::uint16_t>(l), Tier(t), lost[t]);
+    for (std::size_t b = 0; b < s.layers[l].size(); ++b) {
+      const std::uint8_t f = s.layers[l][b];
+      count[0] += f & kOnDev;
+      count[1] += (f & kOnHost) >> 1;
+      count[2] += (f & kOnDisk) >> 2;
+      if (backend_)
+        for (unsigned t = 0; t < 3; ++t)
+          if (f & (1u << t)) lost[t].push_back(static_cast<std::uint32_t>(b));
+    }
+    for (unsigned t = 0; t < 3; ++t) {
+      held[t] += count[t] * page_bytes_;
+      report_loss(session, static_cast<std::uint16_t>(l), Tier(t), lost[t]);
+    }
     s.layers[l].clear();
   }
   for (unsigned t = 0; t < 3; ++t) used_[t] -= held[t];
@@ -872,21 +889,26 @@ KvStore::ApplyResult KvStore::apply_transfer(std::uint64_t id, Ns now) {
   const std::uint64_t stop = std::min<std::uint64_t>(static_cast<std::uint64_t>(m.hi) + 1, lay.size());
 
   std::vector<std::uint32_t> gained, dev_dropped;
+  const bool track = backend_ != nullptr;  // hoisted: flag stores alias members
+  std::uint8_t* const flags = lay.data();
   // Sets `bit` on every block of the range, remembering which ones are new.
   auto gain_bit = [&](std::uint8_t bit, std::uint8_t clear) {
-    for (std::uint64_t b = m.lo; b < stop; ++b) {
-      if (!(lay[b] & bit)) gained.push_back(static_cast<std::uint32_t>(b));
-      lay[b] = static_cast<std::uint8_t>((lay[b] | bit) & ~clear);
-    }
+    if (track)
+      for (std::uint64_t b = m.lo; b < stop; ++b)
+        if (!(flags[b] & bit)) gained.push_back(static_cast<std::uint32_t>(b));
+    const std::uint8_t keep = static_cast<std::uint8_t>(~clear);
+    for (std::uint64_t b = m.lo; b < stop; ++b) flags[b] = static_cast<std::uint8_t>((flags[b] | bit) & keep);
   };
   // Completes a deferred drop: DEVICE residency leaves once a persist lands.
   auto settle_drop = [&]() {
+    std::int64_t n = 0;
     for (std::uint64_t b = m.lo; b < stop; ++b)
-      if ((lay[b] & kDropOnPersist) && (lay[b] & kOnDev)) {
-        lay[b] = static_cast<std::uint8_t>(lay[b] & ~(kOnDev | kDropOnPersist));
-        used_[0] -= page_bytes_;
-        dev_dropped.push_back(static_cast<std::uint32_t>(b));
+      if ((flags[b] & kDropOnPersist) && (flags[b] & kOnDev)) {
+        flags[b] = static_cast<std::uint8_t>(flags[b] & ~(kOnDev | kDropOnPersist));
+        ++n;
+        if (track) dev_dropped.push_back(static_cast<std::uint32_t>(b));
       }
+    used_[0] -= n * page_bytes_;
   };
 
   switch (m.kind) {
@@ -924,12 +946,16 @@ KvStore::ApplyResult KvStore::apply_transfer(std::uint64_t id, Ns now) {
     case Kind::SwapOut:
       gain_bit(kOnHost, kHostPending);
       report_gain(m.session, m.layer, Tier::Host, BlockEvent::SwapOut, gained);
-      for (std::uint64_t b = m.lo; b < stop; ++b) {
-        if (lay[b] & kOnDev) {
-          used_[0] -= page_bytes_;
-          dev_dropped.push_back(static_cast<std::uint32_t>(b));
+      {
+        std::int64_t n = 0;
+        for (std::uint64_t b = m.lo; b < stop; ++b) {
+          if (flags[b] & kOnDev) {
+            ++n;
+            if (track) dev_dropped.push_back(static_cast<std::uint32_t>(b));
+          }
+          flags[b] = static_cast<std::uint8_t>(flags[b] & ~(kOnDev | kDropOnPersist));
         }
-        lay[b] = static_cast<std::uint8_t>(lay[b] & ~(kOnDev | kDropOnPersist));
+        used_[0] -= n * page_bytes_;
       }
       report_loss(m.session, m.layer, Tier::Device, dev_dropped);
       log(now, m.session, m.layer, m.layer, Tier::Device, Tier::Host, m.bytes, m.reason);

@@ -260,3 +260,36 @@ def test_attention_split_merge_reuses_workspace(dev):
     torch.cuda.synchronize()
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+def test_full_70b_session_migration_property(dev):
+    """Config 3 at full size on one GPU (10.7 GB, Llama-3.1-70B KV @ 32K):
+    every layer's 2,048 pages move page->page (K3, the migration kernel) into
+    a second pool standing in for the receiver; every landed page must equal a
+    fresh fill of its (session, layer, block) tag."""
+    layout = LLAMA8B  # 70B KV page shape is the same: 8 kv heads x d128 bf16
+    pb = layout.page_bytes()
+    L, blocks = 80, 2048
+    n = L * blocks
+    if torch.cuda.get_device_properties(0).total_memory < 4 * n * pb:
+        pytest.skip("needs ~43 GB of device memory")
+    gen = torch.Generator(device="cpu").manual_seed(70)
+    src_ids = torch.randperm(n + 1000, generator=gen)[:n].to(torch.int32).to(dev)
+    dst_ids = torch.randperm(n + 1000, generator=gen)[:n].to(torch.int32).to(dev)
+    layer = torch.arange(L, dtype=torch.int32).repeat_interleave(blocks)
+    block = torch.arange(blocks, dtype=torch.int32).repeat(L)
+    tags = torch.stack([torch.full_like(layer, 70), layer, block], -1).contiguous().to(dev)
+    src = kvx.Pool(n + 1000, pb)
+    dst = kvx.Pool(n + 1000, pb)
+    kvx.fill_pages(src, src_ids, tags, n, 700, layout, kvx.FILL_BITS)
+    for l in range(L):
+        sl = slice(l * blocks, (l + 1) * blocks)
+        kvx.copy_pages(src, src_ids[sl], dst, dst_ids[sl], blocks, kvx.COPY_AUTO)
+    del src
+    expect = kvx.Pool(n, pb)
+    kvx.fill_pages(expect, torch.arange(n, dtype=torch.int32, device=dev), tags, n, 700, layout, kvx.FILL_BITS)
+    torch.cuda.synchronize()
+    got, want = dst.as_tensor(), expect.as_tensor()
+    for l in range(0, L, 8):  # compare in chunks to bound temporary memory
+        sl = slice(l * blocks, min(L, l + 8) * blocks)
+        assert torch.equal(got[dst_ids[sl].long()], want[sl])
