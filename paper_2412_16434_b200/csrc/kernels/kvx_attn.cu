@@ -98,6 +98,11 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // Programmatic dependent launch: this CTA may be resident before the
+  // previous kernel on the stream (e.g. the prior layer, or the append of
+  // this step's K/V) has finished; everything we read may be its output, so
+  // wait here — what overlaps is launch, rasterisation and CTA setup.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int ctx = a.ctx_lens[b];
   const int n_pages = (ctx + kT - 1) / kT;
   const int per_split = (n_pages + a.splits - 1) / a.splits;
@@ -244,6 +249,9 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
     __syncwarp();
   }
   cp_async_wait<0>();
+  // All our global reads of the pool are done: let the next kernel's CTAs
+  // start launching into SMs as ours drain.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Full row sums across the 4 lanes sharing a row.
   l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
@@ -495,10 +503,21 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     // One wave or less: 8 warps per CTA (two per scheduler) halve each warp's
     // serial page chain; otherwise 4 warps and 2 CTAs per SM.
     const long ctas = static_cast<long>(splits) * H * batch;
-    if (ctas <= kvx::sm_count(pool->device))
-      kvx::attn_bf16_d128<kvx::kStagesWide, 8><<<grid, 8 * 32, kvx::smem_bytes(kvx::kStagesWide, 8), st>>>(a);
+    const bool narrow = ctas <= kvx::sm_count(pool->device);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(narrow ? 8 * 32 : 4 * 32);
+    cfg.dynamicSmemBytes = kvx::smem_bytes(kvx::kStagesWide, narrow ? 8 : 4);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (narrow)
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 8>, a), "kvx_decode_attention");
     else
-      kvx::attn_bf16_d128<kvx::kStagesWide, 4><<<grid, 4 * 32, kvx::smem_bytes(kvx::kStagesWide, 4), st>>>(a);
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 4>, a), "kvx_decode_attention");
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");
     return KVX_OK;
   }
