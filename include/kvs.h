@@ -253,6 +253,14 @@ int kvs_payload_stats(kvs_payload* p, uint64_t* out6);
  * node (node_id -> device node_id % num_devices) in cluster `c`, built from
  * `tmpl`. Lets unchanged caller stacks (the reference Simulation) run with
  * real pages. NULL clears it. Nodes are owned by the cluster. */
+/* DEVICE page ids of blocks [0, n) of (session, layer) into out[n] — the
+ * block-table row for kvx_decode_attention; KVS_ERR_LOGIC if any block is not
+ * DEVICE-resident. The pool itself: kvs_payload_pool (0 device, 1 host,
+ * 2 landing, 3 disk) returns the kvx_pool* the pages live in. */
+int kvs_payload_block_table(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t n, uint32_t* out);
+int kvs_payload_pool(kvs_payload* p, int32_t pool, void** out);
+/* Waits for everything queued on the node's stream (free-running moves). */
+int kvs_payload_synchronize(kvs_payload* p);
 int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices);
 int kvs_cluster_node(kvs_cluster* c, int32_t node_id, kvs_payload** out);
 

@@ -99,6 +99,10 @@ class NodePayload final : public TierBackend {
   // Copies the bytes of one block's copy in `tier` to host memory; false if
   // this node holds no such copy.
   bool read_block(std::uint32_t session, std::uint16_t layer, std::uint32_t block, Tier tier, void* out);
+  // DEVICE page ids of blocks [0, n) of (session, layer) — the block-table
+  // row a decode-attention launch consumes (kvx_decode_attention). False if
+  // any of them is not DEVICE-resident.
+  bool device_block_table(std::uint32_t session, std::uint16_t layer, std::uint32_t n, std::uint32_t* out) const;
   // Which pool holds the block's `tier` copy (-1: none).
   int pool_of(std::uint32_t session, std::uint16_t layer, std::uint32_t block, Tier tier) const;
   // Bytes moved per BlockEvent kind since construction.

@@ -486,6 +486,24 @@ int kvs_payload_stats(kvs_payload* p, uint64_t* out6) {
   });
 }
 
+int kvs_payload_block_table(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t n, uint32_t* out) {
+  return guarded([&] {
+    if (!p->node->device_block_table(session, layer, n, out))
+      throw std::logic_error("payload: block not DEVICE-resident");
+  });
+}
+
+int kvs_payload_pool(kvs_payload* p, int32_t pool, void** out) {
+  return guarded([&] {
+    if (pool < 0 || pool > 3) throw std::logic_error("payload: pool index out of range");
+    *out = p->node->pool(static_cast<symsim::NodePayload::Pool>(pool));
+  });
+}
+
+int kvs_payload_synchronize(kvs_payload* p) {
+  return guarded([&] { p->node->synchronize(); });
+}
+
 int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices) {
   return guarded([&] {
     if (!c || !tmpl) {
@@ -533,6 +551,9 @@ KVS_NO_PAYLOAD(kvs_payload_pool_of, kvs_payload*, uint32_t, uint16_t, uint32_t, 
 KVS_NO_PAYLOAD(kvs_payload_bytes_moved, kvs_payload*, uint64_t*)
 KVS_NO_PAYLOAD(kvs_payload_stats, kvs_payload*, uint64_t*)
 KVS_NO_PAYLOAD(kvs_set_default_payload, kvs_cluster*, const kvs_payload_options*, int32_t)
+KVS_NO_PAYLOAD(kvs_payload_block_table, kvs_payload*, uint32_t, uint16_t, uint32_t, uint32_t*)
+KVS_NO_PAYLOAD(kvs_payload_pool, kvs_payload*, int32_t, void**)
+KVS_NO_PAYLOAD(kvs_payload_synchronize, kvs_payload*)
 KVS_NO_PAYLOAD(kvs_cluster_node, kvs_cluster*, int32_t, kvs_payload**)
 }  // extern "C"
 #endif

@@ -171,6 +171,16 @@ bool NodePayload::inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_
   return false;
 }
 
+bool NodePayload::device_block_table(std::uint32_t session, std::uint16_t layer, std::uint32_t n,
+                                     std::uint32_t* out) const {
+  for (std::uint32_t b = 0; b < n; ++b) {
+    const auto it = blocks_.find(key(session, layer, b));
+    if (it == blocks_.end() || it->second.tier[0].pool != kDevicePool) return false;
+    out[b] = it->second.tier[0].page;
+  }
+  return true;
+}
+
 int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier tier) const {
   const auto it = blocks_.find(key(s, l, b));
   return it == blocks_.end() ? -1 : it->second.tier[static_cast<int>(tier)].pool;

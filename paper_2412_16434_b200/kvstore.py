@@ -272,6 +272,9 @@ def load_kvs_library(path: Optional[str] = None) -> C.CDLL:
         "kvs_payload_pool_of": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, C.c_int32, P(C.c_int32)], C.c_int),
         "kvs_payload_bytes_moved": ([C.c_void_p, P(C.c_uint64)], C.c_int),
         "kvs_payload_stats": ([C.c_void_p, P(C.c_uint64)], C.c_int),
+        "kvs_payload_block_table": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, P(C.c_uint32)], C.c_int),
+        "kvs_payload_pool": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
+        "kvs_payload_synchronize": ([C.c_void_p], C.c_int),
         "kvs_set_default_payload": ([C.c_void_p, P(_PayloadOpts), C.c_int32], C.c_int),
         "kvs_cluster_node": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
     }
@@ -651,3 +654,20 @@ class NodePayload:
         out = (C.c_uint64 * 6)()
         _check(self._lib, self._lib.kvs_payload_stats(self._h, out))
         return {"apply_wait_ns": out[0], "transfers_posted": out[1], "in_flight": list(out[2:6])}
+
+    def device_block_table(self, session: int, layer: int, n: int):
+        """uint32 DEVICE page ids of blocks [0, n) — a decode block-table row."""
+        import numpy as np
+        out = np.empty(n, np.uint32)
+        _check(self._lib, self._lib.kvs_payload_block_table(self._h, session, layer, n,
+                                                            out.ctypes.data_as(C.POINTER(C.c_uint32))))
+        return out
+
+    def pool_handle(self, pool: int) -> int:
+        """The kvx_pool* behind one of this node's pools (for kvx calls)."""
+        out = C.c_void_p()
+        _check(self._lib, self._lib.kvs_payload_pool(self._h, pool, C.byref(out)))
+        return out.value
+
+    def synchronize(self) -> None:
+        _check(self._lib, self._lib.kvs_payload_synchronize(self._h))

@@ -125,6 +125,13 @@ class Pool:
         self.device = -1 if host else device
 
     @classmethod
+    def borrow(cls, handle: int, num_pages: int, page_bytes: int, device: int = 0) -> "Pool":
+        """A non-owning view of a kvx_pool* owned elsewhere (e.g. a NodePayload)."""
+        p = cls(num_pages, page_bytes, device, _handle=handle)
+        p._borrowed = True
+        return p
+
+    @classmethod
     def wrap(cls, tensor, num_pages: int, page_bytes: int, device: int = 0) -> "Pool":
         h = C.c_void_p()
         check(lib().kvx_pool_wrap(device, tensor.data_ptr(), num_pages, page_bytes, C.byref(h)))
@@ -159,6 +166,9 @@ class Pool:
         return _device_view(self.base, n, self.device).view(self.num_pages, self.page_bytes)
 
     def close(self) -> None:
+        if getattr(self, "_borrowed", False):
+            self.handle = None
+            return
         if self.handle:
             check(lib().kvx_pool_destroy(self.handle))
             self.handle = None
