@@ -464,10 +464,12 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
   const int group = Hq / H;
   const float scale = params->scale > 0.f ? params->scale : 1.0f / std::sqrt(static_cast<float>(layout->head_dim));
   const cudaStream_t st = kvx::as_stream(stream);
+  kvx::DeviceGuard guard(pool->device);
 
   if (kvx::fast_path(layout) && group <= 16) {
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[64] = {};
+    const int dev_slot = pool->device < 0 ? 0 : pool->device % 64;
+    if (!configured[dev_slot]) {
       KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide, 4>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kvx::smem_bytes(kvx::kStagesWide, 4)),
@@ -476,7 +478,7 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         kvx::smem_bytes(kvx::kStagesWide, 8)),
                    "kvx_decode_attention: smem attribute");
-      configured = true;
+      configured[dev_slot] = true;
     }
     const int splits = kvx::choose_splits(batch, H, max_ctx, params->num_splits, kvx::sm_count(pool->device));
     kvx::AttnArgs a{};

@@ -26,6 +26,22 @@ int fail_cuda(cudaError_t e, const char* what);
 int fail_arg(const char* what);
 int sm_count(int device);
 
+// Makes `device` current for the scope (kernels must launch on the device
+// that owns the stream and the pool); no-op for host pools (device < 0).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (device < 0) return;
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != device && cudaSetDevice(device) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 #define KVX_CUDA_TRY(expr, what)                  \
   do {                                            \
     cudaError_t kvx_e_ = (expr);                  \

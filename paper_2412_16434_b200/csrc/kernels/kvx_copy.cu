@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
 // mover for peer (NVLink) or mapped-host (PCIe) endpoints.
 int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const char* who, bool tma_ok) {
   if (a.n_pages == 0) return KVX_OK;
+  DeviceGuard guard(device);
   if (a.page_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(a.src) % 16 || reinterpret_cast<uintptr_t>(a.dst) % 16)
     return fail_arg("page movers need 16-byte aligned pages");
   const int sms = sm_count(device);
@@ -307,6 +308,7 @@ int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_t
     return kvx::fail_arg("kvx_fill_pages: layout does not match the pool's page size");
   if (n == 0) return KVX_OK;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, kvx::sm_count(pool->device) * 8ull));
+  kvx::DeviceGuard guard(pool->device);
   kvx::fill_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(pool->base, pool->page_bytes, d_page_ids, d_tags,
                                                                      n, seed, fill_mode, dtype);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_fill_pages");
@@ -322,6 +324,7 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
   const int row_bytes = layout->head_dim * elt;
   if (row_bytes % 16 != 0) return kvx::fail_arg("kvx_append_kv: head_dim * sizeof(dtype) must be a multiple of 16");
   if (n == 0) return KVX_OK;
+  kvx::DeviceGuard guard(pool->device);
   kvx::append_kv_kernel<<<static_cast<unsigned>(n), 128, 0, kvx::as_stream(stream)>>>(
       pool->base, pool->page_bytes, d_page_ids, d_slots, static_cast<const uint8_t*>(d_k),
       static_cast<const uint8_t*>(d_v), layout->num_kv_heads, layout->block_tokens, row_bytes);
