@@ -233,12 +233,14 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
     attention = None if args.skip_attention else bench_attention(args, torch, np, kvx, dev, hbm_peak)
     e2e = None if args.skip_e2e else bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst)
     overlap = None if args.skip_overlap else bench_overlap(args, torch, np, kvx, dev, hbm_peak)
+    store_cycle = None if args.skip_e2e else bench_store_cycle(args, torch, np, kvx, dev)
     launches = 2 * args.steps
     return dict(value=value, ms_per_step=ms_per_step, extra=extra, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": ncu_traffic(dom_name), "kernel": dom_name,
                           "algorithmic_bytes_per_launch": 2 * session_bytes, "peak_kind": peak_kind},
-                attention=attention, e2e=e2e, overlap=overlap, gpu_launches=launches, session_bytes=session_bytes)
+                attention=attention, e2e=e2e, overlap=overlap, store_cycle=store_cycle, gpu_launches=launches,
+                session_bytes=session_bytes)
 
 
 def graph_time_ms(torch, launch, reps, replays, warmup=2):
@@ -440,6 +442,59 @@ def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
                             "predicted_first_step_end_us": first_end / 1e3, "predicted_stall_us": stall / 1e3,
                             "unpipelined_us": ready_us[-1] + L * t_layer * 1e3}
     return res
+
+
+def bench_store_cycle(args, torch, np, kvx, dev):
+    """The store-driven tier cycle of one 8B @8K session through the kvs C ABI
+    (KvStore + NodePayload, free-running): offload_session (32 per-layer
+    SwapOut moves DEVICE -> pinned HOST, copy engines) then
+    plan_layerwise_load (32 LoadH2D moves back to fresh DEVICE pages), with
+    the cost model calibrated to the measured PCIe rate. Every move is issued
+    when the store schedules it and completed when the transfer is applied in
+    (complete_at, id) order; the host only waits if the GPU is behind."""
+    from paper_2412_16434_b200 import kvstore as K
+    cfg = CFG_8B
+    blocks, n = session_pages(cfg)
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    gpu = K.GpuProfile(kv_bytes_per_token=cfg["layers"] * pb // cfg["block_tokens"], num_layers=cfg["layers"],
+                       hbm_capacity=100 * n * pb)
+    links = K.LinkProfile(pcie_bandwidth=55e9)
+    st = K.KvStore(gpu=gpu, links=links, opts=K.Options(write_behind=False, host_capacity=4 * n * pb))
+    node = K.NodePayload(K.PayloadCluster(), 0, K.PayloadOptions(
+        device=dev.index, num_kv_heads=cfg["kv_heads"], head_dim=cfg["head_dim"], dtype=kvx.BF16,
+        device_pages=2 * n, host_pages=n, landing_pages=1, disk_pages=1, seed=9, free_running=True))
+    node.attach(st)
+    steps = max(3, min(args.steps, 8))
+    for i in range(steps + 1):  # a fresh session per cycle: its only copy starts on DEVICE
+        st.register_session(i, f"s{i}")
+    st.finalize_sessions()
+
+    def pump(sched):
+        for tid, at in sorted(sched, key=lambda t: (t[1], t[0])):
+            st.apply_transfer(tid, at)
+
+    now = 1_000_000
+    times = []
+    for i in range(steps + 1):
+        _, sched = st.append_blocks(i, cfg["ctx"], now)  # untimed: creation fills the pages
+        pump(sched)
+        node.synchronize()
+        t0 = time.perf_counter()
+        pump(st.offload_session(i, now + 1))  # 1 GiB DEVICE -> HOST
+        plan, sched = st.plan_layerwise_load(i, now + 2, 1000, K.DEMAND)  # 1 GiB HOST -> DEVICE
+        pump(sched)
+        node.synchronize()
+        if i:  # first cycle is warm-up
+            times.append(time.perf_counter() - t0)
+        assert st.fully_device_resident(i)
+        st.release_session(i, now + 3)
+        now += 10_000_000_000
+    t = statistics.mean(times)
+    st_ = node.stats()
+    return {"value": 2 * n * pb / t / GB, "unit": "GB/s (D2H + H2D session bytes)", "ms_per_cycle": 1e3 * t,
+            "cycles": steps, "apply_wait_ms_total": st_["apply_wait_ns"] / 1e6,
+            "transfers_issued_at_schedule_time": st_["transfers_posted"],
+            "path": "kvs_offload_session + kvs_plan_layerwise_load, NodePayload free-running (copy engines)"}
 
 
 def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):
@@ -752,6 +807,7 @@ def main():
             line["e2e"] = res["e2e"]
             line["decode_attention"] = res["attention"]
             line["overlap"] = res["overlap"]
+            line["store_cycle"] = res["store_cycle"]
             line["detail"] = res["extra"]
             if not args.skip_cpu:
                 v, cores, sample = cpu_migrate(np, cfg, 8.0, layers=8, repeat_min=3)
