@@ -425,7 +425,6 @@ symsim::PayloadOptions to_payload_opts(const kvs_payload_options* o) {
   p.free_running = o->free_running != 0;
   return p;
 }
-std::map<const symsim::NodePayload*, kvs_payload> g_handles;
 }  // namespace
 
 extern "C" {

@@ -33,8 +33,6 @@ TierBackendFactory& factory_slot() {
   return f;
 }
 
-constexpr std::uint8_t tier_bit(Tier t) { return static_cast<std::uint8_t>(1u << static_cast<unsigned>(t)); }
-
 bool evicts_before(const BlockMeta& a, const BlockMeta& b) {
   if (a.key.layer != b.key.layer) return a.key.layer > b.key.layer;
   if (a.session_bytes != b.session_bytes) return a.session_bytes < b.session_bytes;

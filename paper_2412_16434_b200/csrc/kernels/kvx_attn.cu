@@ -76,6 +76,7 @@ __device__ __forceinline__ uint32_t swz(int row, int col16) {
 struct AttnArgs {
   const uint8_t* pool;
   uint64_t page_bytes;
+  uint64_t pool_pages;  // block-table entries are checked against it
   const uint32_t* tables;
   const int32_t* ctx_lens;
   const uint16_t* q;  // [B][Hq][128] bf16
@@ -129,7 +130,11 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
 
   // Stage this CTA's slice of the block table once (one coalesced read
   // instead of a dependent global load in front of every page fetch).
-  for (int i = threadIdx.x; i < p_end - p_begin; i += blockDim.x) s_pages[i] = __ldg(table + p_begin + i);
+  for (int i = threadIdx.x; i < p_end - p_begin; i += blockDim.x) {
+    const uint32_t page = __ldg(table + p_begin + i);
+    if (page >= a.pool_pages) __trap();  // corrupt block table: fail loudly
+    s_pages[i] = page;
+  }
   __syncthreads();
 
   float o[kD / 8][4];
@@ -484,6 +489,7 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     kvx::AttnArgs a{};
     a.pool = pool->base;
     a.page_bytes = pool->page_bytes;
+    a.pool_pages = pool->num_pages;
     a.tables = d_block_tables;
     a.ctx_lens = d_ctx_lens;
     a.q = static_cast<const uint16_t*>(d_q);

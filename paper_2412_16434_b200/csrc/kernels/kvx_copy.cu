@@ -60,6 +60,7 @@ struct MoveArgs {
   uint32_t chunk_bytes;
   uint32_t chunks_per_page;
   int stages;  // TMA ring depth (bulk mover only)
+  uint64_t src_pages, dst_pages;  // pool sizes: page ids are checked against them
 };
 
 __device__ __forceinline__ void item_addr(const MoveArgs& a, uint64_t item, const uint8_t*& s, uint8_t*& d,
@@ -68,6 +69,7 @@ __device__ __forceinline__ void item_addr(const MoveArgs& a, uint64_t item, cons
   const uint32_t c = static_cast<uint32_t>(item - page * a.chunks_per_page);
   const uint64_t sp = a.src_ids ? __ldg(a.src_ids + page) : page;
   const uint64_t dp = a.dst_ids ? __ldg(a.dst_ids + page) : page;
+  if ((a.src_ids && sp >= a.src_pages) || (a.dst_ids && dp >= a.dst_pages)) __trap();  // bad id: fail loudly
   const uint64_t off = static_cast<uint64_t>(c) * a.chunk_bytes;
   s = a.src + sp * a.page_bytes + off;
   d = a.dst + dp * a.page_bytes + off;
@@ -246,13 +248,15 @@ extern "C" {
 
 int kvx_pack(const kvx_pool* src, const uint32_t* d_page_ids, uint64_t n, void* d_dst, int mode, void* stream) {
   if (!src || (n && (!d_page_ids || !d_dst))) return kvx::fail_arg("kvx_pack: null argument");
-  MoveArgs a{src->base, d_page_ids, static_cast<uint8_t*>(d_dst), nullptr, n, src->page_bytes, 0, 0};
+  MoveArgs a{src->base, d_page_ids, static_cast<uint8_t*>(d_dst), nullptr, n, src->page_bytes, 0, 0, 0,
+             src->num_pages, 0};
   return kvx::launch_move(a, mode, src->device, kvx::as_stream(stream), "kvx_pack", !src->host && !src->ipc);
 }
 
 int kvx_unpack(kvx_pool* dst, const uint32_t* d_page_ids, uint64_t n, const void* d_src, int mode, void* stream) {
   if (!dst || (n && (!d_page_ids || !d_src))) return kvx::fail_arg("kvx_unpack: null argument");
-  MoveArgs a{static_cast<const uint8_t*>(d_src), nullptr, dst->base, d_page_ids, n, dst->page_bytes, 0, 0};
+  MoveArgs a{static_cast<const uint8_t*>(d_src), nullptr, dst->base, d_page_ids, n, dst->page_bytes, 0, 0, 0,
+             0, dst->num_pages};
   return kvx::launch_move(a, mode, dst->device, kvx::as_stream(stream), "kvx_unpack", !dst->host && !dst->ipc);
 }
 
@@ -263,7 +267,7 @@ int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, 
   if (n == 0) return KVX_OK;
   const cudaStream_t st = kvx::as_stream(stream);
   if (mode != KVX_COPY_CE) {
-    MoveArgs a{src->base, src_ids, dst->base, dst_ids, n, src->page_bytes, 0, 0};
+    MoveArgs a{src->base, src_ids, dst->base, dst_ids, n, src->page_bytes, 0, 0, 0, src->num_pages, dst->num_pages};
     const int dev = src->device >= 0 ? src->device : dst->device;
     const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
     return kvx::launch_move(a, mode, dev, st, "kvx_copy_pages", local);

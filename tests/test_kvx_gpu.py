@@ -293,3 +293,28 @@ def test_full_70b_session_migration_property(dev):
     for l in range(0, L, 8):  # compare in chunks to bound temporary memory
         sl = slice(l * blocks, min(L, l + 8) * blocks)
         assert torch.equal(got[dst_ids[sl].long()], want[sl])
+
+
+def test_corrupt_page_id_fails_loudly(dev, tmp_path):
+    """An out-of-range page id in a block table traps the kernel (no silent
+    out-of-bounds copy); run in a child process since a trap poisons the
+    CUDA context."""
+    import subprocess
+    import sys
+    script = tmp_path / "bad_id.py"
+    script.write_text(
+        "import sys, torch\n"
+        f"sys.path.insert(0, {str(ROOT)!r})\n"
+        "from paper_2412_16434_b200 import kvx\n"
+        "pool = kvx.Pool(8, 4096)\n"
+        "ids = torch.tensor([1, 99], dtype=torch.int32, device='cuda')\n"
+        "buf = torch.empty(2 * 4096, dtype=torch.uint8, device='cuda')\n"
+        "try:\n"
+        "    kvx.pack(pool, ids, 2, buf, kvx.COPY_SM)\n"
+        "    torch.cuda.synchronize()\n"
+        "except Exception as e:\n"
+        "    print('raised', type(e).__name__)\n"
+        "    sys.exit(0)\n"
+        "sys.exit(3)\n")
+    proc = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0 and "raised" in proc.stdout, proc.stdout + proc.stderr[-2000:]
