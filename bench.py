@@ -296,8 +296,8 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
         kv_bytes = batch * cfg["ctx"] * 2 * cfg["kv_heads"] * cfg["head_dim"] * 2
         reps = max(sets, 16 if batch < 64 else 4)
 
-        def timed(splits):
-            att = kvx.Attention(layout, 32, blocks, num_splits=splits)
+        def timed(splits, merge=kvx.MERGE_AUTO):
+            att = kvx.Attention(layout, 32, blocks, num_splits=splits, split_merge=merge)
             ws = torch.zeros(max(att.workspace_bytes(batch, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
             return graph_time_ms(torch, lambda i: att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws),
                                  reps, max(3, min(args.steps, 20)))
@@ -308,7 +308,11 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
                                 "kv_bytes": kv_bytes, "rotating_sets": sets, "timing": "cuda-graph replay"}
         if args.attn_sweep:  # diagnostic: fixed split-K factors
             res[f"batch{batch}"]["split_sweep_gbs"] = {
-                s: round(kv_bytes / (timed(s) * 1e-3) / GB, 1) for s in (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)}
+                s: round(kv_bytes / (timed(s, kvx.MERGE_GLOBAL) * 1e-3) / GB, 1)
+                for s in (1, 2, 3, 4, 6, 8, 12, 16, 24, 32)}
+            res[f"batch{batch}"]["cluster_sweep_gbs"] = {
+                s: round(kv_bytes / (timed(s, kvx.MERGE_CLUSTER) * 1e-3) / GB, 1)
+                for s in (2, 3, 4, 6, 8, 9, 12, 16) if batch * cfg["kv_heads"] * s <= 148}
     return res
 
 

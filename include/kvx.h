@@ -83,7 +83,17 @@ typedef struct {
   int32_t max_blocks;  /* row stride of the block table                  */
   int32_t num_splits;  /* split-K over context; 0 = auto                  */
   float scale;         /* softmax scale; 0 = 1/sqrt(head_dim)             */
+  int32_t split_merge; /* KVX_MERGE_*: how split-K partials are combined  */
 } kvx_attn_params;
+
+/* Split-K merge strategies (both in-kernel, one launch). AUTO picks CLUSTER
+ * when the splits of each (request, kv head) fit one thread-block cluster
+ * (<= 16 CTAs) co-resident in a single wave, GLOBAL otherwise. */
+enum {
+  KVX_MERGE_AUTO = 0,
+  KVX_MERGE_GLOBAL = 1,  /* partials in the workspace, last CTA merges (arrival counter) */
+  KVX_MERGE_CLUSTER = 2  /* partials in shared memory, merged over DSMEM              */
+};
 
 const char* kvx_last_error(void);
 int kvx_version(void);
@@ -158,9 +168,10 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
  * ctx_lens[b] tokens of request b, whose block table row is
  * d_block_tables[b * max_blocks ...]. q has the layout dtype. Workspace of
  * kvx_decode_attention_workspace() bytes (may be 0 -> NULL allowed): split-K
- * partials plus per-(request, kv head) arrival counters; it must be
- * zero-filled before its first use, and every launch leaves the counters
- * zeroed again (the last split of each group merges all splits in-kernel). */
+ * partials plus per-(request, kv head) arrival counters for the GLOBAL merge;
+ * it must be zero-filled before its first use, and every launch leaves the
+ * counters zeroed again (the last split of each group merges all splits
+ * in-kernel). The CLUSTER merge does not touch it. */
 uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx_attn_params* params,
                                         int32_t batch, int32_t max_ctx);
 int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,

@@ -35,11 +35,41 @@ constexpr int kWarps = 4;        // warps per CTA (wide grids); 8 when the grid 
 // batch 1 and 8 (profiles/r01_summary.md): small batches are bound by the
 // per-warp instruction latency chain, not by bytes in flight.
 constexpr int kStagesWide = 3;
+// One-wave (narrow) variant: 8 warps x 3 stages = 192 KiB, one CTA per SM.
+#ifndef KVX_NARROW_W
+#define KVX_NARROW_W 8
+#endif
+#ifndef KVX_NARROW_STAGES
+#define KVX_NARROW_STAGES 3
+#endif
+constexpr int kNarrowW = KVX_NARROW_W;
+constexpr int kNarrowStages = KVX_NARROW_STAGES;
 constexpr int kTileBytes = kT * kD * 2;  // one kv head's K (or V) in a page: 4 KiB
 constexpr int kStageBytes = 2 * kTileBytes;
 constexpr int smem_bytes(int stages, int warps) { return warps * stages * kStageBytes; }
 constexpr int kMaxPagesPerCta = 1024;  // block-table slice staged in smem (4 KiB)
+constexpr int kMaxClusterSplits = 16;  // DSMEM split merge: one cluster per (request, kv head)
 constexpr float kLog2e = 1.4426950408889634f;
+
+// Per-CTA timeline stamps (%globaltimer) for tools/attn_trace.cu, which
+// includes this file with KVX_ATTN_TRACE defined; compiled out otherwise.
+#ifdef KVX_ATTN_TRACE
+__device__ __forceinline__ void trace_mark(int slot) {
+  if (threadIdx.x != 0) return;
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const uint64_t cta = (static_cast<uint64_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  kvx_attn_trace[cta * 8 + slot] = t;
+  if (slot == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    kvx_attn_trace[cta * 8 + 7] = sm;
+  }
+}
+#define KVX_TRACE(slot) trace_mark(slot)
+#else
+#define KVX_TRACE(slot) ((void)0)
+#endif
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
@@ -67,6 +97,21 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Address of the same shared-memory variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t map_rank(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 // Byte offset of 16-B chunk `col16` (0..15) of tile row `row` (0..15): rows
 // are 256 B; chunks are XOR-swizzled within each 128-B half by (row & 7).
 __device__ __forceinline__ uint32_t swz(int row, int col16) {
@@ -84,6 +129,7 @@ struct AttnArgs {
   float* part_o;      // [B][Hq][S][128]
   float* part_ml;     // [B][Hq][S][2]
   uint32_t* arrivals; // [B][H] split counters; zero between launches
+  int cluster_merge;  // 1: the splits of a (request, kv head) form one cluster; merge over DSMEM
   int heads;          // kv heads
   int group;          // q heads per kv head
   int max_blocks;
@@ -93,7 +139,7 @@ struct AttnArgs {
 
 // W warps per CTA, each streaming its own pages through a kStages ring.
 template <int kStages, int W>
-__global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
+__global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t s_pages[kMaxPagesPerCta];
   __shared__ int s_last;
@@ -103,7 +149,9 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
   // previous kernel on the stream (e.g. the prior layer, or the append of
   // this step's K/V) has finished; everything we read may be its output, so
   // wait here — what overlaps is launch, rasterisation and CTA setup.
+  KVX_TRACE(0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  KVX_TRACE(1);
   const int ctx = a.ctx_lens[b];
   const int n_pages = (ctx + kT - 1) / kT;
   const int per_split = (n_pages + a.splits - 1) / a.splits;
@@ -136,6 +184,7 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
     s_pages[i] = page;
   }
   __syncthreads();
+  KVX_TRACE(2);
 
   float o[kD / 8][4];
 #pragma unroll
@@ -172,6 +221,7 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
     issue(i + kStages - 1);
     cp_async_wait<kStages - 1>();
     __syncwarp();
+    if (i == 0) KVX_TRACE(3);
     const uint32_t ks = ring_s + (i % kStages) * kStageBytes;
     const uint32_t vs = ks + kTileBytes;
     const int tok0 = (my_first + i * W) * kT;
@@ -254,6 +304,7 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
     __syncwarp();
   }
   cp_async_wait<0>();
+  KVX_TRACE(4);
   // All our global reads of the pool are done: let the next kernel's CTAs
   // start launching into SMs as ours drain.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -287,6 +338,10 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
   }
   __syncthreads();
   const int rows = a.group;
+  // DSMEM merge: this CTA's combined partial stays in its own shared memory
+  // ([16][128] O, [16][2] (m, l)) for the cluster to read.
+  float* cta_o = sml + W * 32;
+  float* cta_ml = cta_o + 16 * kD;
   for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
     const int r = e / kD, d = e - r * kD;
     float M = -INFINITY;
@@ -303,6 +358,12 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
     const uint64_t row = static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r;
     if (a.splits == 1) {
       a.out[row * kD + d] = L > 0.f ? O / L : 0.f;
+    } else if (a.cluster_merge) {
+      cta_o[r * kD + d] = O;
+      if (d == 0) {
+        cta_ml[r * 2] = M;
+        cta_ml[r * 2 + 1] = L;
+      }
     } else {
       a.part_o[(row * a.splits + split) * kD + d] = O;
       if (d == 0) {
@@ -311,7 +372,48 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
       }
     }
   }
+  KVX_TRACE(5);
   if (a.splits == 1) return;
+
+  if (a.cluster_merge) {
+    // The cluster is this (request, kv head)'s `splits` CTAs (cluster rank ==
+    // split). One cluster barrier publishes every CTA's partial; each CTA then
+    // merges a 1/splits slice of the output elements, reading all partials
+    // with one round of independent DSMEM loads; a second barrier keeps every
+    // CTA's shared memory alive until all readers are done.
+    cluster_sync_all();
+    const uint32_t o_s = smem_u32(cta_o), ml_s = smem_u32(cta_ml);
+    const int ns = a.splits;
+    for (int e = split * blockDim.x + threadIdx.x; e < rows * kD; e += ns * blockDim.x) {
+      const int r = e / kD, d = e - r * kD;
+      float m[kMaxClusterSplits], l[kMaxClusterSplits], ov[kMaxClusterSplits];
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxClusterSplits; ++s2) {
+        if (s2 < ns) {
+          m[s2] = ld_dsmem(map_rank(ml_s + r * 8, s2));
+          l[s2] = ld_dsmem(map_rank(ml_s + r * 8 + 4, s2));
+          ov[s2] = ld_dsmem(map_rank(o_s + (r * kD + d) * 4, s2));
+        }
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxClusterSplits; ++s2)
+        if (s2 < ns) M = fmaxf(M, m[s2]);
+      const float Mb = M == -INFINITY ? 0.f : M;
+      float L = 0.f, O = 0.f;
+#pragma unroll
+      for (int s2 = 0; s2 < kMaxClusterSplits; ++s2)
+        if (s2 < ns) {
+          const float f = exp2f(m[s2] - Mb);
+          L += f * l[s2];
+          O += f * ov[s2];
+        }
+      a.out[(static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
+    }
+    cluster_sync_all();
+    KVX_TRACE(6);
+    return;
+  }
 
   // Split-K merge fused in: the last CTA of this (request, kv head) to finish
   // merges every split's partial (L2-resident) — no second launch.
@@ -371,6 +473,7 @@ __global__ void __launch_bounds__(W * 32, 8 / W) attn_bf16_d128(AttnArgs a) {
     a.out[(row0 + r) * kD + d] = (acc0 + acc1) * sm_inv[r];
   }
   if (threadIdx.x == 0) a.arrivals[static_cast<uint64_t>(b) * a.heads + h] = 0;  // ready for the next launch
+  KVX_TRACE(6);
 }
 
 // Generic path (any head_dim <= 256 that is a multiple of 32, fp32 or bf16,
@@ -445,6 +548,81 @@ uint64_t workspace_for(uint64_t batch, uint64_t hq, uint64_t heads, int splits) 
   return batch * hq * splits * (kD + 2) * sizeof(float) + batch * heads * sizeof(uint32_t);
 }
 
+// One-time per-device kernel attributes (dynamic smem, cluster sizes > 8).
+int configure(int device) {
+  static bool configured[64] = {};
+  const int slot = device < 0 ? 0 : device % 64;
+  if (configured[slot]) return KVX_OK;
+  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kStagesWide, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_bytes(kStagesWide, 4)),
+               "kvx_decode_attention: smem attribute");
+  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_bytes(kNarrowStages, kNarrowW)),
+               "kvx_decode_attention: smem attribute");
+  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+               "kvx_decode_attention: cluster attribute");
+  configured[slot] = true;
+  return KVX_OK;
+}
+
+// How many clusters of `splits` one-SM CTAs (8 warps, 192 KiB smem) the
+// device runs at once (cudaOccupancyMaxActiveClusters; GPC-shape dependent).
+int cluster_capacity(int device, int splits) {
+  static int cache[64][kMaxClusterSplits + 1] = {};
+  const int slot = device < 0 ? 0 : device % 64;
+  int& c = cache[slot][splits];
+  if (c == 0) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(splits, 1, 1);
+    cfg.blockDim = dim3(kNarrowW * 32);
+    cfg.dynamicSmemBytes = smem_bytes(kNarrowStages, kNarrowW);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = splits;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    c = cudaOccupancyMaxActiveClusters(&n, attn_bf16_d128<kNarrowStages, kNarrowW>, &cfg) == cudaSuccess ? std::max(n, 0) : 0;
+    if (c == 0) {
+      cudaGetLastError();
+      c = -1;  // cached "does not fit"
+    }
+  }
+  return c;
+}
+
+struct Plan {
+  int splits;
+  bool cluster;  // merge over DSMEM (grid x = splits = cluster size)
+  bool narrow;   // 8 warps per CTA
+};
+
+// Launch plan: the split count from choose_splits; the splits of each
+// (request, kv head) merge over DSMEM when they fit one cluster and all
+// B x H clusters are co-resident (one CTA per SM), else through the
+// workspace. Traced on B200 (tools/attn_trace.cu, profiles/r01_summary.md):
+// the DSMEM merge saves ~1 us per launch at batch 1-4 (12 and 16-CTA
+// clusters do not co-reside 8 at a time on B200's GPCs and run in two
+// waves, which the occupancy check catches). Explicit split counts and
+// merge modes are honoured (tests, sweeps).
+Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge, int device) {
+  const int sms = sm_count(device);
+  const long groups = std::max(1L, static_cast<long>(batch) * heads);
+  const int pages = std::max(1, (max_ctx + kT - 1) / kT);
+  const int min_splits = (pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
+  Plan p{choose_splits(batch, heads, max_ctx, requested, sms), false, false};
+  if (merge != KVX_MERGE_GLOBAL) {
+    const int s = p.splits;
+    const bool ok = s >= 2 && s <= kMaxClusterSplits && s >= min_splits && groups * s <= sms &&
+                    cluster_capacity(device, s) >= (requested > 0 ? 1 : groups);
+    if (ok) p = Plan{s, true, true};
+  }
+  if (!p.cluster) p.narrow = static_cast<long>(p.splits) * groups <= sms;
+  return p;
+}
+
 }  // namespace
 }  // namespace kvx
 
@@ -472,20 +650,14 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
   kvx::DeviceGuard guard(pool->device);
 
   if (kvx::fast_path(layout) && group <= 16) {
-    static bool configured[64] = {};
-    const int dev_slot = pool->device < 0 ? 0 : pool->device % 64;
-    if (!configured[dev_slot]) {
-      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide, 4>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kvx::smem_bytes(kvx::kStagesWide, 4)),
-                   "kvx_decode_attention: smem attribute");
-      KVX_CUDA_TRY(cudaFuncSetAttribute(kvx::attn_bf16_d128<kvx::kStagesWide, 8>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        kvx::smem_bytes(kvx::kStagesWide, 8)),
-                   "kvx_decode_attention: smem attribute");
-      configured[dev_slot] = true;
-    }
-    const int splits = kvx::choose_splits(batch, H, max_ctx, params->num_splits, kvx::sm_count(pool->device));
+    const int dev = pool->device < 0 ? 0 : pool->device;
+    if (int rc = kvx::configure(dev)) return rc;
+    if (params->split_merge < KVX_MERGE_AUTO || params->split_merge > KVX_MERGE_CLUSTER)
+      return kvx::fail_arg("kvx_decode_attention: unknown split_merge");
+    const kvx::Plan plan = kvx::plan_attention(batch, H, max_ctx, params->num_splits, params->split_merge, dev);
+    if (params->split_merge == KVX_MERGE_CLUSTER && !plan.cluster && plan.splits > 1)
+      return kvx::fail_arg("kvx_decode_attention: split_merge=CLUSTER but the splits do not fit one cluster");
+    const int splits = plan.splits;
     kvx::AttnArgs a{};
     a.pool = pool->base;
     a.page_bytes = pool->page_bytes;
@@ -499,7 +671,8 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     a.max_blocks = params->max_blocks;
     a.splits = splits;
     a.scale_log2 = scale * kvx::kLog2e;
-    if (splits > 1) {
+    a.cluster_merge = plan.cluster ? 1 : 0;
+    if (splits > 1 && !plan.cluster) {
       const uint64_t rows = static_cast<uint64_t>(batch) * Hq;
       if (!d_workspace || workspace_bytes < kvx::workspace_for(batch, Hq, H, splits))
         return kvx::fail_arg("kvx_decode_attention: workspace too small");
@@ -510,20 +683,28 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     dim3 grid(splits, H, batch);
     // One wave or less: 8 warps per CTA (two per scheduler) halve each warp's
     // serial page chain; otherwise 4 warps and 2 CTAs per SM.
-    const long ctas = static_cast<long>(splits) * H * batch;
-    const bool narrow = ctas <= kvx::sm_count(pool->device);
+    const bool narrow = plan.narrow;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(narrow ? 8 * 32 : 4 * 32);
-    cfg.dynamicSmemBytes = kvx::smem_bytes(kvx::kStagesWide, narrow ? 8 : 4);
+    cfg.blockDim = dim3(narrow ? kvx::kNarrowW * 32 : 4 * 32);
+    cfg.dynamicSmemBytes = narrow ? kvx::smem_bytes(kvx::kNarrowStages, kvx::kNarrowW) : kvx::smem_bytes(kvx::kStagesWide, 4);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = plan.cluster ? splits : 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    // Cluster launches go without PDL: early-resident dependent clusters cost
+    // 2-15 us per launch at >= 32K context on B200 (tools/attn_trace.cu,
+    // profiles/r01_summary.md); without PDL the cluster merge is at least as
+    // fast as the global merge at every measured shape under graph replay.
+    if (plan.cluster) attr[0].val.programmaticStreamSerializationAllowed = 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = plan.cluster ? 2 : 1;
     if (narrow)
-      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 8>, a), "kvx_decode_attention");
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kNarrowStages, kvx::kNarrowW>, a), "kvx_decode_attention");
     else
       KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 4>, a), "kvx_decode_attention");
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");

@@ -60,13 +60,16 @@ Ns think_ns_like_reference(std::int64_t words, double wpm) {
   return ns_from_sec(static_cast<double>(words) * 60.0 / wpm);
 }
 
-int g_sessions = 0;  // --sessions override (0: config default)
+int g_sessions = 0;           // --sessions override (0: config default)
+double g_typing_wpm = 40.0;   // --typing-wpm (reference SpeedModel default 40)
 
 Trace config4(int users, double miss, double mean_think_s, std::uint64_t seed) {
   SyntheticSpec spec;  // reference defaults: 1000 sessions, 73.4% multi-turn
   if (g_sessions > 0) spec.sessions = g_sessions;
   auto scripts = synthesize_corpus(spec, seed);
-  Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1);
+  SpeedModel speeds;
+  speeds.typing_wpm_mean = g_typing_wpm;
+  Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1, speeds);
   std::mt19937_64 rng(seed + 2);
   std::exponential_distribution<double> think(1.0 / mean_think_s);
   for (auto& e : t.events) {
@@ -96,7 +99,9 @@ Trace config5(int users, double miss, double mean_think_s, std::uint64_t seed) {
     for (int k = 0; k < want; ++k) turns.push_back(sc.turns[static_cast<std::size_t>(k) % sc.turns.size()]);
     sc.turns = std::move(turns);
   }
-  Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1);
+  SpeedModel speeds;
+  speeds.typing_wpm_mean = g_typing_wpm;
+  Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1, speeds);
   std::exponential_distribution<double> think(1.0 / mean_think_s);
   for (auto& e : t.events) {
     if (e.kind != EventKind::Inference || e.turn_index == 0) continue;
@@ -187,6 +192,8 @@ Calibration parse_calibration(int argc, char** argv, int from) {
       c.pcie_gbs = std::atof(argv[++i]);
     } else if (!std::strcmp(argv[i], "--prefill-tps") && i + 1 < argc) {
       c.prefill_tps = std::atof(argv[++i]);
+    } else if (!std::strcmp(argv[i], "--typing-wpm") && i + 1 < argc) {
+      g_typing_wpm = std::atof(argv[++i]);
     } else if (!std::strcmp(argv[i], "--sessions") && i + 1 < argc) {
       g_sessions = std::atoi(argv[++i]);
     } else if (!std::strcmp(argv[i], "--think-s") && i + 1 < argc) {

@@ -158,7 +158,7 @@ def test_append_kv_bit_exact(dev, layout):
     assert np.array_equal(pool.as_tensor().cpu().numpy(), ref)
 
 
-def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0):
+def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0, merge=kvx.MERGE_AUTO):
     rng = np.random.default_rng(seed)
     pb = layout.page_bytes()
     batch = len(ctx_lens)
@@ -175,7 +175,7 @@ def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0):
     else:
         q = rng.standard_normal((batch, hq, layout.head_dim)).astype(np.float32)
     ctx = np.asarray(ctx_lens, np.int32)
-    att = kvx.Attention(layout, hq, max_blocks, num_splits=splits)
+    att = kvx.Attention(layout, hq, max_blocks, num_splits=splits, split_merge=merge)
     ws_bytes = att.workspace_bytes(batch, max_ctx)
     ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev) if ws_bytes else None
     out = torch.full((batch, hq, layout.head_dim), float("nan"), dtype=torch.float32, device=dev)
@@ -192,15 +192,38 @@ def test_attention_tiny_fp32(dev, ctx_lens):
     assert np.all(np.abs(got - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref))), np.abs(got - ref).max()
 
 
+@pytest.mark.parametrize("merge", [kvx.MERGE_AUTO, kvx.MERGE_GLOBAL], ids=["auto", "global"])
 @pytest.mark.parametrize("hq,ctx_lens,splits", [
     (32, [8192], 0), (32, [1, 15, 16, 17, 500, 1031], 0), (64, [4096, 33], 0), (8, [700], 1),
     (32, [3000, 2999, 64], 7), (128, [257], 0), (32, [8192] * 8, 0),
 ])
-def test_attention_bf16_d128(dev, hq, ctx_lens, splits):
-    got, ref = _attention_case(dev, LLAMA8B, hq, ctx_lens, splits, seed=len(ctx_lens) + hq)
+def test_attention_bf16_d128(dev, hq, ctx_lens, splits, merge):
+    got, ref = _attention_case(dev, LLAMA8B, hq, ctx_lens, splits, seed=len(ctx_lens) + hq, merge=merge)
     err = np.abs(got - ref)
     assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (err.max(), err.mean())
     assert err.mean() < 5e-4
+
+
+@pytest.mark.parametrize("hq,ctx_lens,splits", [
+    (32, [8192], 16), (32, [8192], 2), (32, [5000, 16], 9), (32, [100], 16), (64, [1, 2, 3, 4], 4),
+    (4, [16 * 1024 * 16], 16),
+])
+def test_attention_cluster_merge(dev, hq, ctx_lens, splits):
+    """Split-K partials merged over DSMEM inside a thread-block cluster
+    (KVX_MERGE_CLUSTER): split counts up to 16, splits with no pages (ctx 100
+    over 16 splits), and the longest context one cluster covers (16 splits x
+    1,024 staged pages = 262,144 tokens, on a one-kv-head layout)."""
+    layout = LLAMA8B if hq % 8 == 0 else kvx.PageLayout(1, 128, 16, kvx.BF16)
+    got, ref = _attention_case(dev, layout, hq, ctx_lens, splits, seed=splits, merge=kvx.MERGE_CLUSTER)
+    err = np.abs(got - ref)
+    assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (err.max(), err.mean())
+    assert err.mean() < 5e-4
+
+
+def test_attention_cluster_merge_refuses_what_does_not_fit(dev):
+    # 17 splits exceed the largest cluster; asking for CLUSTER must fail, not fall back silently
+    with pytest.raises(kvx.KvxError, match="cluster"):
+        _attention_case(dev, LLAMA8B, 32, [4096], 17, merge=kvx.MERGE_CLUSTER)
 
 
 def test_full_session_migration_property(dev):
@@ -239,7 +262,7 @@ def test_attention_split_merge_reuses_workspace(dev):
     launches on one workspace give identical results, for several split counts."""
     layout = LLAMA8B
     for splits in (2, 5, 32):
-        got0, ref = _attention_case(dev, layout, 32, [2048, 1500, 77], splits, seed=splits)
+        got0, ref = _attention_case(dev, layout, 32, [2048, 1500, 77], splits, seed=splits, merge=kvx.MERGE_GLOBAL)
         err = np.abs(got0 - ref)
         assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (splits, err.max())
     rng = np.random.default_rng(9)
@@ -250,7 +273,7 @@ def test_attention_split_merge_reuses_workspace(dev):
     tables = to_dev(rng.permutation(pages).astype(np.int32).reshape(3, 128), dev)
     ctx = to_dev(np.array([2048, 2000, 1], np.int32), dev)
     q = to_dev(rng.integers(0x3C00, 0x3F80, (3, 32, 128)).astype(np.uint16), dev)
-    att = kvx.Attention(layout, 32, 128, num_splits=7)
+    att = kvx.Attention(layout, 32, 128, num_splits=7, split_merge=kvx.MERGE_GLOBAL)
     ws = torch.zeros(att.workspace_bytes(3, 2048), dtype=torch.uint8, device=dev)
     outs = []
     for _ in range(4):
