@@ -495,10 +495,63 @@ def bench_store_cycle(args, torch, np, kvx, dev):
         now += 10_000_000_000
     t = statistics.mean(times)
     st_ = node.stats()
-    return {"value": 2 * n * pb / t / GB, "unit": "GB/s (D2H + H2D session bytes)", "ms_per_cycle": 1e3 * t,
-            "cycles": steps, "apply_wait_ms_total": st_["apply_wait_ns"] / 1e6,
-            "transfers_issued_at_schedule_time": st_["transfers_posted"],
-            "path": "kvs_offload_session + kvs_plan_layerwise_load, NodePayload free-running (copy engines)"}
+    res = {"value": 2 * n * pb / t / GB, "unit": "GB/s (D2H + H2D session bytes)", "ms_per_cycle": 1e3 * t,
+           "cycles": steps, "apply_wait_ms_total": st_["apply_wait_ns"] / 1e6,
+           "transfers_issued_at_schedule_time": st_["transfers_posted"],
+           "path": "kvs_offload_session + kvs_plan_layerwise_load, NodePayload free-running (copy engines)"}
+    res["swap"] = bench_store_swap(args, K, kvx, cfg, n, pb, dev)
+    return res
+
+
+def bench_store_swap(args, K, kvx, cfg, n, pb, dev):
+    """Symphony's tier swap on one node: while session A is offloaded (SwapOut,
+    DEVICE -> HOST) session B, advised to arrive, is loaded back (LoadH2D,
+    HOST -> DEVICE). Both are posted together and applied in the store's
+    (complete_at, id) order; the payload runs them on its OUT and IN lanes, so
+    the two PCIe directions overlap. Value: session bytes moved per second,
+    both directions counted."""
+    gpu = K.GpuProfile(kv_bytes_per_token=cfg["layers"] * pb // cfg["block_tokens"], num_layers=cfg["layers"],
+                       hbm_capacity=100 * n * pb)
+    st = K.KvStore(gpu=gpu, links=K.LinkProfile(pcie_bandwidth=55e9),
+                   opts=K.Options(write_behind=False, host_capacity=8 * n * pb))
+    node = K.NodePayload(K.PayloadCluster(), 0, K.PayloadOptions(
+        device=dev.index, num_kv_heads=cfg["kv_heads"], head_dim=cfg["head_dim"], dtype=kvx.BF16,
+        device_pages=3 * n, host_pages=3 * n, landing_pages=1, disk_pages=1, seed=13, free_running=True))
+    node.attach(st)
+    cycles = max(3, min(args.steps, 8))
+    for i in range(cycles + 2):
+        st.register_session(i, f"w{i}")
+    st.finalize_sessions()
+
+    def pump(sched):
+        for tid, at in sorted(sched, key=lambda t: (t[1], t[0])):
+            st.apply_transfer(tid, at)
+
+    now = 1_000_000
+    _, sched = st.append_blocks(0, cfg["ctx"], now)  # session 0 starts offloaded
+    pump(sched)
+    pump(st.offload_session(0, now + 1))
+    node.synchronize()
+    times = []
+    for i in range(1, cycles + 2):
+        now += 10_000_000_000
+        _, sched = st.append_blocks(i, cfg["ctx"], now)  # A = i on DEVICE (untimed fill)
+        pump(sched)
+        node.synchronize()
+        t0 = time.perf_counter()
+        out = st.offload_session(i, now + 1)  # A: DEVICE -> HOST
+        _, load = st.plan_layerwise_load(i - 1, now + 1, 1000, K.DEMAND)  # B = i - 1: HOST -> DEVICE
+        pump(out + load)
+        node.synchronize()
+        if i > 1:
+            times.append(time.perf_counter() - t0)
+        assert st.fully_device_resident(i - 1)
+        st.release_session(i - 1, now + 2)
+    t = statistics.mean(times)
+    s = node.stats()
+    return {"value": 2 * n * pb / t / GB, "unit": "GB/s (D2H + H2D session bytes, concurrent)",
+            "ms_per_swap": 1e3 * t, "swaps": len(times), "cross_lane_waits": s["cross_lane_waits"],
+            "path": "kvs_offload_session(A) + kvs_plan_layerwise_load(B) posted together, IN/OUT lanes"}
 
 
 def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):

@@ -247,8 +247,9 @@ int kvs_payload_pool_of(kvs_payload* p, uint32_t session, uint16_t layer, uint32
 int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7);
 /* out[0] = host ns blocked in apply waiting for the GPU (free-running),
  * out[1] = transfers issued at schedule time, out[2..5] = pages of each pool
- * held by moves issued but not yet applied. */
-int kvs_payload_stats(kvs_payload* p, uint64_t* out6);
+ * held by moves issued but not yet applied, out[6] = batches that waited on
+ * another lane's batch touching the same pages (IN / OUT / PEER lanes). */
+int kvs_payload_stats(kvs_payload* p, uint64_t* out7);
 /* Process-wide default: every KvStore constructed afterwards gets a payload
  * node (node_id -> device node_id % num_devices) in cluster `c`, built from
  * `tmpl`. Lets unchanged caller stacks (the reference Simulation) run with
@@ -259,8 +260,13 @@ int kvs_payload_stats(kvs_payload* p, uint64_t* out6);
  * 2 landing, 3 disk) returns the kvx_pool* the pages live in. */
 int kvs_payload_block_table(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t n, uint32_t* out);
 int kvs_payload_pool(kvs_payload* p, int32_t pool, void** out);
-/* Waits for everything queued on the node's stream (free-running moves). */
+/* Waits for everything queued on the node's lanes (free-running moves). */
 int kvs_payload_synchronize(kvs_payload* p);
+/* The cudaStream_t of one of the node's lanes: 0 IN (moves landing in HBM),
+ * 1 OUT (HBM -> pinned host), 2 DISK (disk-tier reads and writes), 3 PEER
+ * (migration pushes into a peer). Callers may order their own work against
+ * a lane with events; the payload never waits on caller streams. */
+int kvs_payload_stream(kvs_payload* p, int32_t lane, void** out);
 int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices);
 int kvs_cluster_node(kvs_cluster* c, int32_t node_id, kvs_payload** out);
 

@@ -28,6 +28,14 @@
 //                 "apply_transfer on CUDA-event completion").
 //                 The host only blocks if the GPU is behind the cost model's
 //                 clock; that wait is accounted in apply_wait_ns().
+// Moves run on four lanes (CUDA streams) per node so independent queues
+// overlap the way the hardware allows: IN (anything landing in this GPU's
+// HBM: fills, LoadH2D), OUT (HBM -> pinned host: SwapOut, HostCopy), DISK
+// (DiskWrite, LoadDiskHost: the reference's separate disk queues) and PEER
+// (migration pushes this node runs into a peer's landing pool). PCIe is full
+// duplex, so an offload and a prefetch proceed at once. Hazards across lanes are tracked per page: every page
+// remembers the last (node, lane, batch) that touched it, and a batch waits
+// on the events of the other lanes' batches that still touch its pages.
 // In both modes the event order is the reference clock's (apply in
 // (complete_at, id) order), so block-table state is bit-identical to the
 // reference and every copy's bytes can be verified. Migrated layers land in
@@ -64,7 +72,9 @@ class NodePayload;
 class PayloadCluster {
  public:
   void add(NodePayload* node);
+  void remove(NodePayload* node);
   NodePayload* node(int id) const;
+  std::vector<NodePayload*> nodes() const;
   void note_source(std::uint32_t session, int node);
   int take_source(std::uint32_t session);
 
@@ -114,7 +124,10 @@ class NodePayload final : public TierBackend {
   // Free-running: pages of `p` held by moves issued but not yet applied.
   std::uint64_t pages_in_flight(Pool p) const;
   kvx_pool* pool(Pool p) const { return pools_[p]; }
-  void* stream() const { return stream_; }
+  enum LaneId : int { kLaneIn = 0, kLaneOut = 1, kLaneDisk = 2, kLanePeer = 3, kLanes = 4 };
+  void* stream(LaneId lane) const { return lanes_[lane].stream; }
+  // Batches that had to wait on another lane's batch (page reuse hazards).
+  std::uint64_t cross_lane_waits() const { return cross_waits_; }
   void synchronize();
 
  private:
@@ -125,6 +138,29 @@ class NodePayload final : public TierBackend {
   struct Copies {
     Ref tier[3];  // indexed by Tier
   };
+  // A stream plus the events of its batches still possibly running; batch
+  // tickets increase by one per batch.
+  struct Lane {
+    void* stream = nullptr;
+    std::uint64_t next = 1;  // ticket of the next batch
+    std::uint64_t done = 0;  // every ticket <= done has completed
+    std::vector<std::pair<std::uint64_t, void*>> pending;  // (ticket, event), ascending
+    std::uint32_t* d_ids[2] = {nullptr, nullptr};           // page-id scratch for this lane's kernels
+    std::size_t d_ids_cap[2] = {0, 0};
+    void retire();
+    void* event_for(std::uint64_t ticket);  // nullptr once complete
+    void drain();                           // after a stream sync: everything complete
+  };
+  struct Fence {  // the last batch that read or wrote a page
+    std::int32_t node = -1;
+    std::int32_t lane = 0;
+    std::uint64_t ticket = 0;
+  };
+  using Touch = std::pair<NodePayload*, Ref>;  // a page of some node's pool
+  void wait_fences(NodePayload& runner, int lane, const std::vector<Touch>& pages);
+  void set_fences(NodePayload& runner, int lane, const std::vector<Touch>& pages);
+  Fence& fence(const Ref& r) { return fences_[r.pool][r.page]; }
+
   struct InFlight {  // a free-running move: pages being written by `event`
     int tier = 0;
     std::uint32_t session = 0;
@@ -144,10 +180,12 @@ class NodePayload final : public TierBackend {
   bool inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_t b, int exclude_tier, Ref* page,
                        void** event) const;
   // Issues src[i] -> dst[i] copies on the runner's stream, grouped by pools.
-  void issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push);
+  // Queues the moves on the lane the destination implies; returns the lane's stream.
+  void* issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push,
+              const std::vector<void*>& waits);
   void move_now(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
                 const std::vector<std::uint32_t>& blocks);
-  std::uint32_t* device_ids(const std::vector<std::uint32_t>& ids, int slot);
+  std::uint32_t* device_ids(Lane& lane, const std::vector<std::uint32_t>& ids, int slot);
 
   PayloadCluster* cluster_;
   int node_;
@@ -157,11 +195,12 @@ class NodePayload final : public TierBackend {
   std::vector<std::uint32_t> free_[4];
   std::unordered_map<std::uint64_t, Copies> blocks_;
   std::map<std::uint32_t, int> import_src_;
-  void* stream_ = nullptr;
-  // Device id scratch (source / destination ids). Reuse is safe without host
-  // syncs: uploads and the kernels reading them are ordered on stream_.
-  std::uint32_t* d_ids_[2] = {nullptr, nullptr};
-  std::size_t d_ids_cap_[2] = {0, 0};
+  Lane lanes_[kLanes];
+  std::vector<Fence> fences_[4];  // per pool page
+  std::uint64_t cross_waits_ = 0;
+  // Device id scratch lives per lane (Lane::d_ids): reuse is safe without
+  // host syncs because uploads and the kernels reading them share the lane's
+  // stream. Tag scratch is used by fills, which run on the IN lane.
   void* d_tags_ = nullptr;
   std::size_t d_tags_cap_ = 0;
   std::uint64_t moved_[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -477,11 +477,12 @@ int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7) {
   });
 }
 
-int kvs_payload_stats(kvs_payload* p, uint64_t* out6) {
+int kvs_payload_stats(kvs_payload* p, uint64_t* out7) {
   return guarded([&] {
-    out6[0] = p->node->apply_wait_ns();
-    out6[1] = p->node->transfers_posted();
-    for (int i = 0; i < 4; ++i) out6[2 + i] = p->node->pages_in_flight(static_cast<symsim::NodePayload::Pool>(i));
+    out7[0] = p->node->apply_wait_ns();
+    out7[1] = p->node->transfers_posted();
+    for (int i = 0; i < 4; ++i) out7[2 + i] = p->node->pages_in_flight(static_cast<symsim::NodePayload::Pool>(i));
+    out7[6] = p->node->cross_lane_waits();
   });
 }
 
@@ -501,6 +502,13 @@ int kvs_payload_pool(kvs_payload* p, int32_t pool, void** out) {
 
 int kvs_payload_synchronize(kvs_payload* p) {
   return guarded([&] { p->node->synchronize(); });
+}
+
+int kvs_payload_stream(kvs_payload* p, int32_t lane, void** out) {
+  return guarded([&] {
+    if (lane < 0 || lane >= symsim::NodePayload::kLanes) throw std::logic_error("payload: lane index out of range");
+    *out = p->node->stream(static_cast<symsim::NodePayload::LaneId>(lane));
+  });
 }
 
 int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices) {
@@ -553,6 +561,7 @@ KVS_NO_PAYLOAD(kvs_set_default_payload, kvs_cluster*, const kvs_payload_options*
 KVS_NO_PAYLOAD(kvs_payload_block_table, kvs_payload*, uint32_t, uint16_t, uint32_t, uint32_t*)
 KVS_NO_PAYLOAD(kvs_payload_pool, kvs_payload*, int32_t, void**)
 KVS_NO_PAYLOAD(kvs_payload_synchronize, kvs_payload*)
+KVS_NO_PAYLOAD(kvs_payload_stream, kvs_payload*, int32_t, void**)
 KVS_NO_PAYLOAD(kvs_cluster_node, kvs_cluster*, int32_t, kvs_payload**)
 }  // extern "C"
 #endif

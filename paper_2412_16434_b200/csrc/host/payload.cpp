@@ -44,6 +44,17 @@ std::uint64_t now_ns() {
 
 void PayloadCluster::add(NodePayload* node) { nodes_[node->node_id()] = node; }
 
+void PayloadCluster::remove(NodePayload* node) {
+  const auto it = nodes_.find(node->node_id());
+  if (it != nodes_.end() && it->second == node) nodes_.erase(it);
+}
+
+std::vector<NodePayload*> PayloadCluster::nodes() const {
+  std::vector<NodePayload*> out;
+  for (const auto& e : nodes_) out.push_back(e.second);
+  return out;
+}
+
 NodePayload* PayloadCluster::node(int id) const {
   const auto it = nodes_.find(id);
   return it == nodes_.end() ? nullptr : it->second;
@@ -60,13 +71,85 @@ int PayloadCluster::take_source(std::uint32_t session) {
 }
 
 // ---------------------------------------------------------------------------
+// lanes and per-page fences
+
+// Retires completed batches from the front (they complete in ticket order).
+void NodePayload::Lane::retire() {
+  std::size_t k = 0;
+  while (k < pending.size() && kvx_event_query(pending[k].second) == KVX_OK) {
+    done = pending[k].first;
+    kvx_event_destroy(pending[k].second);
+    ++k;
+  }
+  pending.erase(pending.begin(), pending.begin() + static_cast<std::ptrdiff_t>(k));
+}
+
+void* NodePayload::Lane::event_for(std::uint64_t ticket) {
+  if (ticket <= done) return nullptr;
+  retire();
+  if (ticket <= done) return nullptr;
+  const auto it = std::lower_bound(pending.begin(), pending.end(), std::make_pair(ticket, static_cast<void*>(nullptr)),
+                                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  return it != pending.end() && it->first == ticket ? it->second : nullptr;
+}
+
+void NodePayload::Lane::drain() {
+  for (auto& e : pending) kvx_event_destroy(e.second);
+  pending.clear();
+  done = next - 1;
+}
+
+// Make `runner`'s lane wait for every other lane's batch still touching
+// `pages` (reads and writes alike: WAR, RAW and WAW are all covered).
+void NodePayload::wait_fences(NodePayload& runner, int lane, const std::vector<Touch>& pages) {
+  // A lane completes its batches in ticket order, so waiting for the newest
+  // ticket seen per foreign lane covers every page fenced by that lane.
+  std::vector<std::pair<Lane*, std::uint64_t>> need;
+  for (const Touch& t : pages) {
+    const Fence& f = t.first->fence(t.second);
+    if (f.ticket == 0 || (f.node == runner.node_ && f.lane == lane)) continue;  // same stream: ordered
+    NodePayload* owner = f.node == runner.node_ ? &runner
+                         : f.node == node_      ? this
+                         : cluster_             ? cluster_->node(f.node)
+                                                : nullptr;
+    if (!owner) continue;  // that node is gone, and synchronized on its way out
+    Lane* L = &owner->lanes_[f.lane];
+    auto it = std::find_if(need.begin(), need.end(), [L](const auto& e) { return e.first == L; });
+    if (it == need.end())
+      need.emplace_back(L, f.ticket);
+    else
+      it->second = std::max(it->second, f.ticket);
+  }
+  bool waited = false;
+  for (const auto& [L, ticket] : need)
+    if (void* ev = L->event_for(ticket)) {  // nullptr: already complete
+      kvx_check(kvx_stream_wait_event(runner.lanes_[lane].stream, ev), "stream wait");
+      waited = true;
+    }
+  if (waited) ++cross_waits_;
+}
+
+// Close the batch just queued on `runner`'s lane: one event, and every page
+// it touched now points at it.
+void NodePayload::set_fences(NodePayload& runner, int lane, const std::vector<Touch>& pages) {
+  Lane& L = runner.lanes_[lane];
+  L.retire();  // keeps the pending list short on lanes nobody waits on
+  void* ev = nullptr;
+  kvx_check(kvx_event_create(&ev), "event");
+  kvx_check(kvx_event_record(ev, L.stream), "event record");
+  const std::uint64_t ticket = L.next++;
+  L.pending.emplace_back(ticket, ev);
+  for (const Touch& t : pages) t.first->fence(t.second) = Fence{runner.node_, lane, ticket};
+}
+
+// ---------------------------------------------------------------------------
 // node: pools, pages, scratch
 
 NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOptions& opts)
     : cluster_(cluster), node_(node_id), opts_(opts) {
   page_bytes_ = kvx_page_bytes(&opts_.layout);
   if (page_bytes_ == 0) throw std::runtime_error("payload: empty page layout");
-  kvx_check(kvx_stream_create(opts_.device, &stream_), "stream");
+  for (Lane& L : lanes_) kvx_check(kvx_stream_create(opts_.device, &L.stream), "stream");
   const std::uint64_t counts[4] = {opts_.device_pages, opts_.host_pages, opts_.landing_pages, opts_.disk_pages};
   for (int p = 0; p < 4; ++p) {
     if (counts[p] == 0) continue;
@@ -75,6 +158,7 @@ NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOpti
     else
       kvx_check(kvx_pool_create_host(counts[p], page_bytes_, &pools_[p]), "host pool");
     free_[p].resize(counts[p]);
+    fences_[p].resize(counts[p]);
     // LIFO free list handing out low page ids first.
     for (std::uint64_t i = 0; i < counts[p]; ++i) free_[p][i] = static_cast<std::uint32_t>(counts[p] - 1 - i);
   }
@@ -82,19 +166,30 @@ NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOpti
 }
 
 NodePayload::~NodePayload() {
-  if (stream_) kvx_stream_synchronize(stream_);
-  for (auto& entry : inflight_) {
-    kvx_event_synchronize(entry.second.event);
-    kvx_event_destroy(entry.second.event);
+  // Peers may have queued pushes into our landing pool: let them land first.
+  if (cluster_) {
+    cluster_->remove(this);
+    for (NodePayload* n : cluster_->nodes()) n->synchronize();
   }
+  for (Lane& L : lanes_)
+    if (L.stream) kvx_stream_synchronize(L.stream);
+  for (auto& entry : inflight_) kvx_event_destroy(entry.second.event);
   for (auto*& p : pools_)
     if (p) kvx_pool_destroy(p);
-  for (auto* d : d_ids_) kvx_free(d);
+  for (Lane& L : lanes_) {
+    L.drain();
+    for (auto* d : L.d_ids) kvx_free(d);
+    kvx_stream_destroy(L.stream);
+  }
   kvx_free(d_tags_);
-  kvx_stream_destroy(stream_);
 }
 
-void NodePayload::synchronize() { kvx_check(kvx_stream_synchronize(stream_), "sync"); }
+void NodePayload::synchronize() {
+  for (Lane& L : lanes_) {
+    kvx_check(kvx_stream_synchronize(L.stream), "sync");
+    L.drain();
+  }
+}
 
 std::uint64_t NodePayload::pages_in_use(Pool p) const {
   const std::uint64_t total = pools_[p] ? kvx_pool_num_pages(pools_[p]) : 0;
@@ -119,28 +214,28 @@ std::uint32_t NodePayload::alloc(Pool p) {
   return page;
 }
 
-// A freed page may still be read by work queued on this node's stream; any
-// later writer of the page is ordered behind it on the same stream (or waits
-// on a marker of it, see transfer_posted), so no host sync is needed.
+// A freed page may still be read by queued work; its fence makes any later
+// writer on another lane wait for that work, so no host sync is needed.
 void NodePayload::release(const Ref& r) {
   if (r.pool >= 0) free_[r.pool].push_back(r.page);
 }
 
-std::uint32_t* NodePayload::device_ids(const std::vector<std::uint32_t>& ids, int slot) {
-  if (ids.size() > d_ids_cap_[slot]) {
-    if (d_ids_[slot]) {
-      synchronize();  // the old buffer may still be read by queued kernels
-      kvx_free(d_ids_[slot]);
+std::uint32_t* NodePayload::device_ids(Lane& lane, const std::vector<std::uint32_t>& ids, int slot) {
+  if (ids.size() > lane.d_ids_cap[slot]) {
+    if (lane.d_ids[slot]) {
+      kvx_check(kvx_stream_synchronize(lane.stream), "sync");  // queued kernels may still read it
+      kvx_free(lane.d_ids[slot]);
     }
-    d_ids_[slot] = nullptr;
+    lane.d_ids[slot] = nullptr;
     const std::size_t cap = std::max<std::size_t>(ids.size(), 4096);
     void* p = nullptr;
     kvx_check(kvx_malloc(opts_.device, cap * sizeof(std::uint32_t), &p), "id scratch");
-    d_ids_[slot] = static_cast<std::uint32_t*>(p);
-    d_ids_cap_[slot] = cap;
+    lane.d_ids[slot] = static_cast<std::uint32_t*>(p);
+    lane.d_ids_cap[slot] = cap;
   }
-  kvx_check(kvx_memcpy_async(d_ids_[slot], ids.data(), ids.size() * sizeof(std::uint32_t), stream_), "ids upload");
-  return d_ids_[slot];
+  kvx_check(kvx_memcpy_async(lane.d_ids[slot], ids.data(), ids.size() * sizeof(std::uint32_t), lane.stream),
+            "ids upload");
+  return lane.d_ids[slot];
 }
 
 // Best existing copy of a block on this node, fastest tier first, skipping
@@ -186,13 +281,30 @@ int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier
   return it == blocks_.end() ? -1 : it->second.tier[static_cast<int>(tier)].pool;
 }
 
-// Queues src[i] -> dst[i] (dst in this node's pools) grouped by (source pool,
-// destination pool). HBM<->HBM pairs use the SM/TMA page mover with device
-// id lists; anything touching pinned host memory uses the copy engines.
-// With `push` the work runs on the source node's stream and stores into this
-// node's memory (the NVLink / peer path of a migration).
-void NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push) {
+// Queues src[i] -> dst[i] (dst in this node's pools, all in one pool)
+// grouped by (source pool, destination pool). HBM<->HBM pairs use the SM/TMA
+// page mover with device id lists; anything touching pinned host memory uses
+// the copy engines. With `push` the work runs on the source node's PEER lane
+// and stores into this node's memory (the NVLink / peer path of a
+// migration); otherwise on this node's IN lane (destination in HBM), DISK
+// lane (disk-tier source or destination) or OUT lane (HBM -> host). The batch first waits on `waits` and on
+// the fences of every page it touches.
+void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push,
+                         const std::vector<void*>& waits) {
   NodePayload& runner = push ? src_node : *this;
+  const int dp0 = dst.empty() ? kDevicePool : dst[0].pool;
+  const bool from_disk = std::any_of(src.begin(), src.end(), [](const Ref& r) { return r.pool == kDiskPool; });
+  const int lane = push                                           ? kLanePeer
+                   : (dp0 == kDevicePool || dp0 == kLandingPool) ? kLaneIn
+                   : (dp0 == kDiskPool || from_disk)             ? kLaneDisk
+                                                                 : kLaneOut;
+  Lane& L = runner.lanes_[lane];
+  std::vector<Touch> touched;
+  touched.reserve(src.size() + dst.size());
+  for (const Ref& r : src) touched.emplace_back(&src_node, r);
+  for (const Ref& r : dst) touched.emplace_back(this, r);
+  for (void* ev : waits) kvx_check(kvx_stream_wait_event(L.stream, ev), "stream wait");
+  wait_fences(runner, lane, touched);
   for (int sp = 0; sp < 4; ++sp)
     for (int dp = 0; dp < 4; ++dp) {
       std::vector<std::uint32_t> s_ids, d_ids;
@@ -206,14 +318,16 @@ void NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& dst
       kvx_pool* to = pools_[dp];
       const bool on_device = (sp == kDevicePool || sp == kLandingPool) && (dp == kDevicePool || dp == kLandingPool);
       if (on_device) {
-        const std::uint32_t* ds = runner.device_ids(s_ids, 0);
-        const std::uint32_t* dd = runner.device_ids(d_ids, 1);
-        kvx_check(kvx_copy_pages(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO, runner.stream_), "page copy");
+        const std::uint32_t* ds = runner.device_ids(L, s_ids, 0);
+        const std::uint32_t* dd = runner.device_ids(L, d_ids, 1);
+        kvx_check(kvx_copy_pages(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO, L.stream), "page copy");
       } else {
-        kvx_check(kvx_copy_pages(from, s_ids.data(), to, d_ids.data(), s_ids.size(), KVX_COPY_CE, runner.stream_),
+        kvx_check(kvx_copy_pages(from, s_ids.data(), to, d_ids.data(), s_ids.size(), KVX_COPY_CE, L.stream),
                   "copy-engine copy");
       }
     }
+  set_fences(runner, lane, touched);
+  return L.stream;
 }
 
 // ---------------------------------------------------------------------------
@@ -227,24 +341,29 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
   if (why == BlockEvent::Created) {
     std::vector<std::uint32_t> pages;
     std::vector<kvx_block_tag> tags;
+    std::vector<Touch> touched;
     for (std::uint32_t b : blocks) {
       Copies& c = blocks_[key(session, layer, b)];
       release(c.tier[t]);
       c.tier[t] = Ref{kDevicePool, alloc(kDevicePool)};
       pages.push_back(c.tier[t].page);
       tags.push_back(kvx_block_tag{session, layer, b});
+      touched.emplace_back(this, c.tier[t]);
     }
-    const std::uint32_t* d_pages = device_ids(pages, 0);
+    Lane& L = lanes_[kLaneIn];
+    wait_fences(*this, kLaneIn, touched);
+    const std::uint32_t* d_pages = device_ids(L, pages, 0);
     if (tags.size() * sizeof(kvx_block_tag) > d_tags_cap_) {
-      if (d_tags_) synchronize();
+      if (d_tags_) kvx_check(kvx_stream_synchronize(L.stream), "sync");
       kvx_free(d_tags_);
       d_tags_cap_ = std::max<std::size_t>(tags.size() * sizeof(kvx_block_tag), 65536);
       kvx_check(kvx_malloc(opts_.device, d_tags_cap_, &d_tags_), "tag scratch");
     }
-    kvx_check(kvx_memcpy_async(d_tags_, tags.data(), tags.size() * sizeof(kvx_block_tag), stream_), "tags upload");
+    kvx_check(kvx_memcpy_async(d_tags_, tags.data(), tags.size() * sizeof(kvx_block_tag), L.stream), "tags upload");
     kvx_check(kvx_fill_pages(pools_[kDevicePool], d_pages, static_cast<const kvx_block_tag*>(d_tags_), pages.size(),
-                             opts_.seed, &opts_.layout, opts_.fill_mode, stream_),
+                             opts_.seed, &opts_.layout, opts_.fill_mode, L.stream),
               "fill");
+    set_fences(*this, kLaneIn, touched);
     if (!opts_.free_running) synchronize();
     return;
   }
@@ -310,11 +429,7 @@ void NodePayload::move_now(std::uint32_t session, std::uint16_t layer, Tier tier
     src.push_back(from);
     dst.push_back(c.tier[t]);
   }
-  if (push) {  // queued free-running work on either side lands first
-    src_node->synchronize();
-    synchronize();
-  }
-  issue(src, dst, *src_node, push);
+  issue(src, dst, *src_node, push, {});
   (push ? *src_node : *this).synchronize();
 }
 
@@ -372,20 +487,13 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
     f.pages.push_back(dst.back());
   }
   if (f.blocks.empty()) return;
-  NodePayload& runner = push ? *src_node : *this;
-  if (push) {  // the source writes our pages: order it after our queued reads of recycled pages
-    void* marker = nullptr;
-    kvx_check(kvx_event_create(&marker), "event");
-    kvx_check(kvx_event_record(marker, stream_), "event record");
-    kvx_check(kvx_stream_wait_event(runner.stream_, marker), "stream wait");
-    kvx_event_destroy(marker);
-  }
+  // Sources still being written by another move are chained explicitly (and
+  // by their fences); recycled destination pages wait on their fences.
   std::sort(waits.begin(), waits.end());
   waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
-  for (void* ev : waits) kvx_check(kvx_stream_wait_event(runner.stream_, ev), "stream wait");
-  issue(src, dst, *src_node, push);
+  void* lane_stream = issue(src, dst, *src_node, push, waits);
   kvx_check(kvx_event_create(&f.event), "event");
-  kvx_check(kvx_event_record(f.event, runner.stream_), "event record");
+  kvx_check(kvx_event_record(f.event, lane_stream), "event record");
   for (std::uint32_t b : f.blocks) inflight_by_block_[key(tr.session, tr.layer, b) * 4 + t] = tr.id;
   moved_[7] += f.blocks.size() * page_bytes_;  // bytes issued ahead of their apply
   inflight_.emplace(tr.id, std::move(f));
@@ -403,9 +511,7 @@ void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
     kvx_check(kvx_event_synchronize(f.event), "event sync");
     apply_wait_ns_ += now_ns() - t0;
   }
-  // Later work on this node is ordered after the move (it may have run on a
-  // peer's stream).
-  kvx_check(kvx_stream_wait_event(stream_, f.event), "stream wait");
+  // Later moves touching these pages are ordered by the pages' fences.
   for (std::uint32_t b : f.blocks) {
     const auto k = key(f.session, f.layer, b) * 4 + f.tier;
     const auto jt = inflight_by_block_.find(k);

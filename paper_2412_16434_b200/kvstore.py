@@ -275,6 +275,7 @@ def load_kvs_library(path: Optional[str] = None) -> C.CDLL:
         "kvs_payload_block_table": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, P(C.c_uint32)], C.c_int),
         "kvs_payload_pool": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
         "kvs_payload_synchronize": ([C.c_void_p], C.c_int),
+        "kvs_payload_stream": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
         "kvs_set_default_payload": ([C.c_void_p, P(_PayloadOpts), C.c_int32], C.c_int),
         "kvs_cluster_node": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
     }
@@ -550,6 +551,7 @@ def decode_step_time(batch: int, gpu: Optional[GpuProfile] = None, lib: Optional
 # Physical payload (include/symsim/payload.hpp through kvs.h)
 
 POOL_DEVICE, POOL_HOST, POOL_LANDING, POOL_DISK = range(4)
+LANE_IN, LANE_OUT, LANE_DISK, LANE_PEER = range(4)
 BLOCK_EVENTS = ("created", "load_h2d", "load_disk_host", "host_copy", "disk_write", "swap_out", "net_arrive")
 
 
@@ -651,9 +653,10 @@ class NodePayload:
         return dict(zip(BLOCK_EVENTS, list(out)))
 
     def stats(self) -> Dict[str, int]:
-        out = (C.c_uint64 * 6)()
+        out = (C.c_uint64 * 7)()
         _check(self._lib, self._lib.kvs_payload_stats(self._h, out))
-        return {"apply_wait_ns": out[0], "transfers_posted": out[1], "in_flight": list(out[2:6])}
+        return {"apply_wait_ns": out[0], "transfers_posted": out[1], "in_flight": list(out[2:6]),
+                "cross_lane_waits": out[6]}
 
     def device_block_table(self, session: int, layer: int, n: int):
         """uint32 DEVICE page ids of blocks [0, n) — a decode block-table row."""
@@ -671,3 +674,9 @@ class NodePayload:
 
     def synchronize(self) -> None:
         _check(self._lib, self._lib.kvs_payload_synchronize(self._h))
+
+    def stream(self, lane: int) -> int:
+        """cudaStream_t of a lane (LANE_IN / LANE_OUT / LANE_DISK / LANE_PEER)."""
+        out = C.c_void_p()
+        _check(self._lib, self._lib.kvs_payload_stream(self._h, lane, C.byref(out)))
+        return out.value

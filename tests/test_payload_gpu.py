@@ -250,3 +250,39 @@ def test_randomized_lifecycle_keeps_bytes_and_state_consistent(dev, seed, write_
             verify(store, node, sessions)
     pump.run()
     verify(store, node, sessions)
+
+
+def test_recycled_pages_wait_for_other_lanes(dev):
+    """Free-running, pages recycled across lanes: session A's write-behind
+    DiskWrites (DISK lane) still read A's DEVICE pages when A is purged from
+    DEVICE (its HOST copy has landed, on the OUT lane) and B's demand load (IN
+    lane) is handed those very pages. The DISK lane is stalled by a 50 ms spin
+    kernel queued ahead of A's writes, so without the page fences B's load
+    would overwrite the pages before the DiskWrites read them and A's DISK
+    copy would hold B's bytes. The load must wait on the DiskWrite batch, and
+    every copy of both sessions stays bit-exact."""
+    cluster, store, node = make_node(opts_kw=dict(device_pages=6), free_running=True)
+    pump = Pump(store)
+    for s in (1, 2):
+        store.register_session(s, f"s{s}")
+    store.finalize_sessions()
+    pump.add(store.append_blocks(2, 40, 0)[1])  # B: 3 blocks x 2 layers fill the 6-page pool
+    pump.run()
+    freed, _ = store.purge_from_device(store.layer_block_bytes() * 6, 1_000_000, False)
+    assert freed == store.layer_block_bytes() * 6
+    node.synchronize()
+    with torch.cuda.stream(torch.cuda.ExternalStream(node.stream(K.LANE_DISK))):
+        torch.cuda._sleep(100_000_000)  # ~50 ms at B200 clocks
+    pump.add(store.append_blocks(1, 40, 2_000_000)[1])  # A reuses B's pages; HostCopy + DiskWrite posted
+    pump.run(limit=LAYERS)  # A's HOST copies land (OUT lane); the DiskWrites wait behind the spin
+    assert pump.pending, "the DiskWrites must still be pending"
+    freed, _ = store.purge_from_device(store.layer_block_bytes() * 6, 3_000_000, False)
+    assert freed == store.layer_block_bytes() * 6 and node.pages_in_use(K.POOL_DEVICE) == 0
+    before = node.stats()["cross_lane_waits"]
+    plan, sched = store.plan_layerwise_load(2, 4_000_000, 100_000, K.DEMAND)
+    assert plan.any_load
+    assert node.stats()["cross_lane_waits"] > before, "the load did not wait for the DiskWrites reading its pages"
+    pump.add(sched)
+    pump.run()
+    assert store.fully_device_resident(2)
+    verify(store, node, [1, 2])
