@@ -214,6 +214,12 @@ std::uint32_t NodePayload::alloc(Pool p) {
   return page;
 }
 
+// Re-deals a batch's freshly allocated pages (one pool) in ascending order:
+// the free list is LIFO, so pages released in ascending order come back
+// descending; ascending destinations pair with ascending sources into long
+// runs of consecutive ids, which the copy engines move as one copy each.
+void sort_pages(std::vector<std::uint32_t>& pages) { std::sort(pages.begin(), pages.end()); }
+
 // A freed page may still be read by queued work; its fence makes any later
 // writer on another lane wait for that work, so no host sync is needed.
 void NodePayload::release(const Ref& r) {
@@ -292,7 +298,7 @@ int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier
 void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push,
                          const std::vector<void*>& waits) {
   NodePayload& runner = push ? src_node : *this;
-  const int dp0 = dst.empty() ? kDevicePool : dst[0].pool;
+  const int dp0 = dst.empty() ? static_cast<int>(kDevicePool) : dst[0].pool;
   const bool from_disk = std::any_of(src.begin(), src.end(), [](const Ref& r) { return r.pool == kDiskPool; });
   const int lane = push                                           ? kLanePeer
                    : (dp0 == kDevicePool || dp0 == kLandingPool) ? kLaneIn
@@ -345,9 +351,14 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
     for (std::uint32_t b : blocks) {
       Copies& c = blocks_[key(session, layer, b)];
       release(c.tier[t]);
-      c.tier[t] = Ref{kDevicePool, alloc(kDevicePool)};
-      pages.push_back(c.tier[t].page);
-      tags.push_back(kvx_block_tag{session, layer, b});
+      c.tier[t] = Ref{};
+    }
+    for (std::size_t i = 0; i < blocks.size(); ++i) pages.push_back(alloc(kDevicePool));
+    sort_pages(pages);
+    for (std::size_t i = 0; i < blocks.size(); ++i) {
+      Copies& c = blocks_[key(session, layer, blocks[i])];
+      c.tier[t] = Ref{kDevicePool, pages[i]};
+      tags.push_back(kvx_block_tag{session, layer, blocks[i]});
       touched.emplace_back(this, c.tier[t]);
     }
     Lane& L = lanes_[kLaneIn];
@@ -425,8 +436,15 @@ void NodePayload::move_now(std::uint32_t session, std::uint16_t layer, Tier tier
                                block_event_name(why) + ")");
     Copies& c = blocks_[key(session, layer, b)];
     release(c.tier[t]);
-    c.tier[t] = Ref{static_cast<std::int8_t>(dest), alloc(dest)};
+    c.tier[t] = Ref{};
     src.push_back(from);
+  }
+  std::vector<std::uint32_t> pages;
+  for (std::size_t i = 0; i < blocks.size(); ++i) pages.push_back(alloc(dest));
+  sort_pages(pages);
+  for (std::size_t i = 0; i < blocks.size(); ++i) {
+    Copies& c = blocks_[key(session, layer, blocks[i])];
+    c.tier[t] = Ref{static_cast<std::int8_t>(dest), pages[i]};
     dst.push_back(c.tier[t]);
   }
   issue(src, dst, *src_node, push, {});
@@ -482,11 +500,16 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
       waits.push_back(ev);
     }
     src.push_back(from);
-    dst.push_back(Ref{static_cast<std::int8_t>(dest), alloc(dest)});
     f.blocks.push_back(b);
-    f.pages.push_back(dst.back());
   }
   if (f.blocks.empty()) return;
+  std::vector<std::uint32_t> pages;
+  for (std::size_t i = 0; i < f.blocks.size(); ++i) pages.push_back(alloc(dest));
+  sort_pages(pages);
+  for (std::uint32_t pg : pages) {
+    dst.push_back(Ref{static_cast<std::int8_t>(dest), pg});
+    f.pages.push_back(dst.back());
+  }
   // Sources still being written by another move are chained explicitly (and
   // by their fences); recycled destination pages wait on their fences.
   std::sort(waits.begin(), waits.end());
