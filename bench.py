@@ -15,10 +15,13 @@ attention (K4) at batch 1/8/64, the end-to-end path through the C ABI with
 pinned HOST buffers (H2D + unpack + pack + D2H, every step), and the CPU
 restatement on the host cores.
 
-N>1 (config 3, Llama-3.1-70B KV shape @ 32K, ~10.7 GB per session): every
-rank owns one session and migrates it to rank (r+1) % N over NVLink with the
-K3 kernel storing straight into the peer's page pool (CUDA IPC) — a
-point-to-point exchange, no collective; weak scaling.
+N>1 (config 3, Llama-3.1-70B KV shape @ 32K, ~10.7 GB per session):
+migration-plus-serving. Every rank decodes a batch of 70B @32K requests on
+its main stream while its own session migrates to rank (r+1) % N on a side
+stream, the K3 kernel storing straight into the peer's page pool over NVLink
+(CUDA IPC) — a point-to-point exchange, no collective; weak scaling.
+`--migrate-mode nccl` swaps in pack + ncclSend/ncclRecv + unpack for
+comparison.
 
 `--impl reference` times the reference's CPU path on the host cores: the
 reference KvStore's migration bookkeeping (oracle/_ref, 1 thread, as the
@@ -416,6 +419,14 @@ def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
                      "hidden_fraction": max(0.0, min(1.0, (t_dec + t_mig - t_both) / t_mig)),
                      "migrate_gbs_alone": n * pb / (t_mig * 1e-3) / GB}
 
+    def migrate_capped(st, mode, cap):
+        for l in range(L):
+            sl = slice(l * blocks, (l + 1) * blocks)
+            kvx.copy_pages(spool, src[sl], spool, dst[sl], blocks, mode, st.cuda_stream, max_ctas=cap)
+
+    res["background"] = background_migration(torch, kvx, decode, migrate_capped, side, dev, n * pb, t_dec,
+                                             hbm_peak, sweep=args.bg_sweep)
+
     # Physical pipeline gate: per-layer arrival events gate a batch-1 decode of
     # the migrating session; compare with the reference recurrence.
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(L)]
@@ -446,6 +457,81 @@ def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
                             "predicted_first_step_end_us": first_end / 1e3, "predicted_stall_us": stall / 1e3,
                             "unpipelined_us": ready_us[-1] + L * t_layer * 1e3}
     return res
+
+
+def background_migration(torch, kvx, decode, migrate, side, dev, session_bytes, t_step, hbm_peak, sweep=False):
+    """Serving with a session migrating underneath, on one GPU.
+
+    Decode runs `steps` back-to-back steps on a high-priority stream while one
+    session migrates on a low-priority side stream with the mover's grid
+    capped to `cap` CTAs (kvx_copy_pages_capped). In an N-GPU ring each GPU
+    reads the session it sends and writes the one it receives, so its HBM sees
+    the same read + write bytes as this local copy: this measures the HBM side
+    of "migration hidden behind decode" (NVLink itself needs two GPUs).
+    Reported per variant: migration GB/s while decode runs (vs the 770 GB/s
+    NVLink peer-copy peak), the decode time added over `steps` steps, and the
+    floor — the HBM time the migration's read + write bytes need at the
+    measured copy peak (what an ideal share of HBM would add)."""
+    steps = 4
+    floor = 2 * session_bytes / (hbm_peak * GB) * 1e3
+    out = {"decode_steps": steps, "decode_step_ms_alone": t_step, "nvlink_peak_gbs": NVLINK_PEAK_GBS,
+           "hbm_floor_extra_ms": floor, "variants": []}
+    hi = torch.cuda.Stream(dev, priority=-5)   # clamped to the device's highest priority
+    lo = torch.cuda.Stream(dev, priority=0)
+    if sweep:
+        variants = [(m, cap, geo, prio) for m in ("tma", "sm") for cap in (8, 16, 24, 32, 48, 74, 0)
+                    for geo in ((None,) if m == "sm" else (None, (8192, 3), (16384, 2)))
+                    for prio in (False, True)]
+    else:
+        # the measured-best rows of the sweep (profiles/r01_background_sweep.json)
+        variants = [("tma", 0, None, False), ("tma", 48, None, False), ("sm", 0, None, False),
+                    ("sm", 74, None, False)]
+    modes = {"tma": kvx.COPY_TMA, "sm": kvx.COPY_SM}
+    saved = {k: os.environ.get(k) for k in ("KVX_BULK_CHUNK", "KVX_BULK_STAGES")}
+
+    def run(dec_st, mig_st, mode, cap):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
+        ev[0].record(dec_st)
+        mig_st.wait_event(ev[0])
+        if mode is not None:
+            migrate(mig_st, mode, cap)
+        ev[1].record(mig_st)
+        for _ in range(steps):
+            decode(dec_st)
+        ev[2].record(dec_st)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]), ev[0].elapsed_time(ev[2])
+
+    try:
+        for prio in (False, True):  # decode alone on each stream kind (same work, reference point)
+            dec_st = hi if prio else torch.cuda.current_stream(dev)
+            out["decode_alone_ms_" + ("hi" if prio else "default")] = statistics.median(
+                run(dec_st, lo, None, 0)[1] for _ in range(3))
+        for mname, cap, geo, prio in variants:
+            for k in saved:
+                os.environ.pop(k, None)
+            if geo:
+                os.environ["KVX_BULK_CHUNK"], os.environ["KVX_BULK_STAGES"] = str(geo[0]), str(geo[1])
+            dec_st = hi if prio else torch.cuda.current_stream(dev)
+            mig_st = lo if prio else side
+            base = out["decode_alone_ms_" + ("hi" if prio else "default")]
+            rows = [run(dec_st, mig_st, modes[mname], cap) for _ in range(3)]
+            t_mig = statistics.median(r[0] for r in rows)
+            t_all = statistics.median(r[1] for r in rows)
+            extra = max(0.0, t_all - base)
+            out["variants"].append({
+                "mover": mname, "max_ctas": cap or "all", "stage": f"{geo[0] // 1024}KiBx{geo[1]}" if geo else "default",
+                "priority_streams": prio, "migrate_ms": t_mig, "migrate_gbs": session_bytes / (t_mig * 1e-3) / GB,
+                "nvlink_frac": session_bytes / (t_mig * 1e-3) / GB / NVLINK_PEAK_GBS, "decode_ms": t_all,
+                "decode_extra_ms": extra, "extra_over_floor": extra / floor})
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return out
 
 
 def bench_store_cycle(args, torch, np, kvx, dev):
@@ -612,14 +698,29 @@ def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):
 
 
 def bench_multi(args, torch, np, kvx, dev, rank, world):
-    """Ring migration of one 70B@32K session per rank to rank+1 over NVLink:
-    K3 (kvx_copy_pages) on the source GPU stores straight into the receiver's
-    page pool, opened through CUDA IPC. No collective on the data path."""
+    """Migration-plus-serving at N GPUs (config 3): every rank decodes a batch
+    of 70B @32K requests on its main stream while its own 70B @32K session
+    migrates to rank (r+1) % N on a side stream — the reference's
+    start_migration -> per-layer NetArrive (simcore.cpp:132-141,
+    kvstore.cpp:753-769) as real bytes, off the serving path.
+
+    --migrate-mode p2p (default): K3 (kvx_copy_pages) on the source GPU
+      gathers the session's pages and stores them straight into the
+      receiver's page pool over NVLink (opened through CUDA IPC): one pass,
+      no staging buffer, no receiver-side kernel, no collective.
+    --migrate-mode nccl: the comparison path — K1 pack into a per-layer buffer,
+      ncclSend/ncclRecv (batch_isend_irecv, ring), K2 unpack on the receiver.
+
+    value = N x session bytes / the max over ranks of the migration time
+    measured WHILE decode runs. Also reported: the migration alone, the decode
+    step alone and during the migration, and e2e (block tables H2D from
+    pinned host every step, a probe page of what landed D2H)."""
     import torch.distributed as dist
     from paper_2412_16434_b200 import cluster
     cfg = dict(CFG_70B)
     if args.layers:
         cfg["layers"] = args.layers
+    L = cfg["layers"]
     blocks, n = session_pages(cfg)
     layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
     pb = layout.page_bytes()
@@ -628,67 +729,203 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
     d_src = torch.from_numpy(src_ids.view(np.int32)).to(dev)
     seed = cluster.session_seed(rank)
 
-    def tags_for(seed_):
-        layer = np.repeat(np.arange(cfg["layers"], dtype=np.uint32), blocks)
-        block = np.tile(np.arange(blocks, dtype=np.uint32), cfg["layers"])
-        return torch.from_numpy(np.stack([np.full(n, seed_, np.uint32), layer, block], -1).view(np.int32)).to(dev)
+    def tags_for(seed_, count=n):
+        layer = np.repeat(np.arange(L, dtype=np.uint32), blocks)[:count]
+        block = np.tile(np.arange(blocks, dtype=np.uint32), L)[:count]
+        return torch.from_numpy(np.stack([np.full(count, seed_, np.uint32), layer, block], -1).view(np.int32)).to(dev)
 
     kvx.fill_pages(pool, d_src, tags_for(seed), n, seed, layout, kvx.FILL_VALUES)
-    torch.cuda.synchronize()
-    peers = cluster.exchange_pool_handles(dist, rank, pool.ipc_export(), 2 * n, pb)
-    nxt = cluster.ring_peer(rank, world)
-    peer = kvx.Pool.ipc_open(peers[nxt].handle, peers[nxt].num_pages, pb, dev.index)
-    _, peer_dst = cluster.session_layout(nxt, 2 * n, n)  # the receiver's landing pages
+    nxt, prv = cluster.ring_peer(rank, world), cluster.ring_source(rank, world)
+    _, my_dst = cluster.session_layout(rank, 2 * n, n)      # where my source's session lands in my pool
+    _, peer_dst = cluster.session_layout(nxt, 2 * n, n)     # where mine lands in the receiver's pool
+    d_my_dst = torch.from_numpy(my_dst.view(np.int32)).to(dev)
     d_peer_dst = torch.from_numpy(peer_dst.view(np.int32)).to(dev)
-    stream = torch.cuda.current_stream(dev)
     mode = {"auto": kvx.COPY_AUTO, "sm": kvx.COPY_SM, "tma": kvx.COPY_TMA}[args.copy_mode]
     red_dev = dev if dist.get_backend() == "nccl" else None
+    side = torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+    sl = [slice(l * blocks, (l + 1) * blocks) for l in range(L)]
 
-    def step(ev):
-        if ev:
-            ev[0].record(stream)
-        kvx.copy_pages(pool, d_src, peer, d_peer_dst, n, mode, stream)
-        if ev:
-            ev[1].record(stream)
+    peer = None
+    if args.migrate_mode == "p2p":
+        peers = cluster.exchange_pool_handles(dist, rank, pool.ipc_export(), 2 * n, pb)
+        peer = kvx.Pool.ipc_open(peers[nxt].handle, peers[nxt].num_pages, pb, dev.index)
 
-    for _ in range(args.warmup):
-        step(None)
+        def migrate(st, src=d_src, dst=d_peer_dst):
+            for l in range(L):
+                kvx.copy_pages(pool, src[sl[l]], peer, dst[sl[l]], blocks, mode, st.cuda_stream,
+                               max_ctas=args.mig_ctas)
+    else:
+        staged = dist.get_backend() != "nccl"  # gloo (CPU tests): host-staged send/recv
+        bufs = [[torch.empty(blocks * pb, dtype=torch.uint8, device=dev) for _ in range(2)] for _ in range(2)]
+        hbufs = [torch.empty(blocks * pb, dtype=torch.uint8) for _ in range(2)] if staged else None
+
+        def migrate(st, src=d_src, dst=d_my_dst):
+            with torch.cuda.stream(st):
+                for l in range(L):
+                    snd, rcv = bufs[l % 2]
+                    kvx.pack(pool, src[sl[l]], blocks, snd, kvx.COPY_AUTO, st.cuda_stream)
+                    if staged:
+                        st.synchronize()
+                        hbufs[0].copy_(snd)
+                        ops = [dist.P2POp(dist.isend, hbufs[0], nxt), dist.P2POp(dist.irecv, hbufs[1], prv)]
+                        for w in dist.batch_isend_irecv(ops):
+                            w.wait()
+                        rcv.copy_(hbufs[1])
+                    else:
+                        ops = [dist.P2POp(dist.isend, snd, nxt), dist.P2POp(dist.irecv, rcv, prv)]
+                        for w in dist.batch_isend_irecv(ops):
+                            w.wait()  # the side stream waits on the transfer, the host does not
+                    kvx.unpack(pool, dst[sl[l]], blocks, rcv, kvx.COPY_AUTO, st.cuda_stream)
+
+    # Serving: a decode batch on every rank (70B shape: 64 q heads over 8 kv heads).
+    B, hq = args.serve_batch, 64
+    ctx = cfg["ctx"]
+    dec_pages = B * L * blocks
+    dpool = kvx.Pool(max(dec_pages, 1), pb, device=dev.index)
+    if B:
+        ids = torch.arange(dec_pages, dtype=torch.int32, device=dev)
+        kvx.fill_pages(dpool, ids, torch.stack([ids * 0 + 1000 + rank, ids * 0, ids], -1).contiguous(), dec_pages,
+                       7 + rank, layout, kvx.FILL_VALUES)
+        perm = torch.randperm(dec_pages, device=dev, dtype=torch.int64).to(torch.int32)
+        tables = [perm[l * B * blocks:(l + 1) * B * blocks].view(B, blocks).contiguous() for l in range(L)]
+        ctx_t = torch.full((B,), ctx, dtype=torch.int32, device=dev)
+        q = (torch.randn(B, hq, 128, device=dev) * 0.5).to(torch.bfloat16)
+        out = torch.empty(B, hq, 128, dtype=torch.float32, device=dev)
+        att = kvx.Attention(layout, hq, blocks)
+        ws = torch.zeros(max(att.workspace_bytes(B, ctx), 1), dtype=torch.uint8, device=dev)
+
+    def decode(st):
+        for l in range(L):
+            att(dpool, tables[l], ctx_t, q, out, B, ctx, ws, st.cuda_stream)
+
+    def timed(fn, st):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e[0].record(st)
+        fn(st)
+        e[1].record(st)
+        return e
+
     torch.cuda.synchronize()
     dist.barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    with ClockSampler(dev.index) as clocks:
-        for i in range(args.steps):
-            step(evs[i])
+    # Warm-up doubles as the calibration of the serving window: migration
+    # alone and one decode step alone (every rank migrating at once).
+    for _ in range(args.warmup):
+        migrate(side)
+    torch.cuda.synchronize()
+    dist.barrier()
+    em = timed(migrate, side)
+    torch.cuda.synchronize()
+    t_mig_alone = cluster.max_over_ranks(dist, em[0].elapsed_time(em[1]), red_dev)
+    t_step = 0.0
+    if B:
+        decode(main)
+        ed = timed(decode, main)
         torch.cuda.synchronize()
-    dist.barrier()  # every sender has finished writing into its receiver
-    my_ms = evs[0][0].elapsed_time(evs[-1][-1])
-    ms = cluster.max_over_ranks(dist, my_ms, red_dev)
-    # what landed here is the ring source's session, bit for bit
-    src_rank = cluster.ring_source(rank, world)
-    _, my_dst = cluster.session_layout(rank, 2 * n, n)
+        t_step = cluster.max_over_ranks(dist, ed[0].elapsed_time(ed[1]), red_dev)
+    # decode steps per migration: enough that the migration starts and ends inside the serving window
+    K = max(1, int(np.ceil(1.25 * t_mig_alone / t_step))) if B else 0
+    dist.barrier()
+
+    rows = []
+    with ClockSampler(dev.index) as clocks:
+        for _ in range(args.steps):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            torch.cuda.synchronize()
+            dist.barrier()
+            e[0].record(main)
+            side.wait_event(e[0])
+            migrate(side)
+            e[1].record(side)
+            for _ in range(K):
+                decode(main)
+            e[2].record(main)
+            torch.cuda.synchronize()
+            rows.append((e[0].elapsed_time(e[1]), e[0].elapsed_time(e[2])))
+        dist.barrier()  # every sender has finished writing into its receiver
+    t_mig = cluster.max_over_ranks(dist, statistics.mean(r[0] for r in rows), red_dev)
+    t_win = cluster.max_over_ranks(dist, statistics.mean(r[1] for r in rows), red_dev)
+
+    # What landed here is the ring source's session, bit for bit.
     expect = kvx.Pool(n, pb, device=dev.index)
-    kvx.fill_pages(expect, torch.arange(n, dtype=torch.int32, device=dev), tags_for(cluster.session_seed(src_rank)),
-                   n, cluster.session_seed(src_rank), layout, kvx.FILL_VALUES)
+    kvx.fill_pages(expect, torch.arange(n, dtype=torch.int32, device=dev), tags_for(cluster.session_seed(prv)),
+                   n, cluster.session_seed(prv), layout, kvx.FILL_VALUES)
     torch.cuda.synchronize()
     probe = torch.randint(0, n, (min(n, 4096),), device=dev)
-    got = pool.as_tensor()[torch.from_numpy(my_dst.view(np.int32)).to(dev)[probe].long()]
+    got = pool.as_tensor()[d_my_dst[probe].long()]
     ok = bool(torch.equal(got, expect.as_tensor()[probe]))
+    expect.close()
     oks = [None] * world
     dist.all_gather_object(oks, ok)
     assert all(oks), f"migrated pages differ on ranks {[i for i, o in enumerate(oks) if not o]}"
-    ms_per_step = ms / args.steps
+
+    e2e = bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, migrate, src_ids, peer_dst,
+                          my_dst, pb, n, red_dev) if args.migrate_mode == "p2p" else None
+
     session_bytes = n * pb
-    value = world * session_bytes / (ms_per_step * 1e-3) / GB
-    kern = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-    achieved = session_bytes / (kern * 1e-3) / GB
-    peer.close()
+    value = world * session_bytes / (t_mig * 1e-3) / GB
+    achieved = session_bytes / (t_mig * 1e-3) / GB  # per GPU per direction over NVLink
+    serving = None
+    if B:
+        serving = {"decode": f"batch {B} x ctx {ctx} x {L} layers (K4, {hq} q / {cfg['kv_heads']} kv heads)",
+                   "decode_step_ms_alone": t_step, "decode_steps_per_migration": K,
+                   "window_ms": t_win, "decode_slowdown_over_window": t_win / (K * t_step) - 1.0,
+                   "migration_inside_window": bool(t_mig <= t_win),
+                   "migrate_ms_alone": t_mig_alone, "migrate_gbs_alone": session_bytes / (t_mig_alone * 1e-3) / GB}
+    if peer is not None:
+        peer.close()
     dist.barrier()
-    return dict(value=value, ms_per_step=ms_per_step, clocks=clocks.summary(), session_bytes=session_bytes,
-                cfg=cfg, verified=True,
+    launches = args.steps * (L * (1 if args.migrate_mode == "p2p" else 2) + K * L)
+    return dict(value=value, ms_per_step=t_mig, clocks=clocks.summary(), session_bytes=session_bytes,
+                cfg=cfg, verified=True, serving=serving, e2e=e2e,
                 roofline={"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
-                          "frac": achieved / NVLINK_PEAK_GBS, "traffic": None, "kernel": "kvx_copy_pages(peer)",
-                          "algorithmic_bytes_per_launch": session_bytes, "peak_kind": "measured peer copy"},
-                gpu_launches=args.steps)
+                          "frac": achieved / NVLINK_PEAK_GBS, "traffic": None,
+                          "kernel": "kvx_copy_pages(peer)" if args.migrate_mode == "p2p" else "nccl send/recv",
+                          "algorithmic_bytes_per_launch": session_bytes // L,
+                          "note": "per GPU, per direction, measured while decode runs; one launch per layer",
+                          "peak_kind": "measured peer copy (B200_PROFILING.md)"},
+                gpu_launches=launches)
+
+
+def bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, migrate, src_ids, peer_dst, my_dst, pb,
+                    n, red_dev):
+    """The ring migration through the public API as a caller drives it: every
+    step uploads the session's block tables (source and receiver page ids)
+    from pinned host memory, migrates, and reads back one landed page (the
+    last one written) from the receiver's pool."""
+    h_src = torch.from_numpy(src_ids.view(np.int32)).pin_memory()
+    h_dst = torch.from_numpy(peer_dst.view(np.int32)).pin_memory()
+    d_src = torch.empty_like(h_src, device=dev)
+    d_dst = torch.empty_like(h_dst, device=dev)
+    h_probe = torch.empty(pb, dtype=torch.uint8).pin_memory()
+    st = torch.cuda.current_stream(dev)
+    last = int(peer_dst[-1])
+
+    def step():
+        d_src.copy_(h_src, non_blocking=True)
+        d_dst.copy_(h_dst, non_blocking=True)
+        migrate(st, d_src, d_dst)
+        h_probe.copy_(peer.as_tensor()[last], non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    steps = max(1, min(args.steps, 5))
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record(st)
+    for _ in range(steps):
+        step()
+    e[1].record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = cluster.max_over_ranks(dist, e[0].elapsed_time(e[1]) / steps, red_dev)
+    assert torch.equal(h_probe, pool.as_tensor()[int(src_ids[-1])].cpu()), "e2e probe page differs"
+    world = dist.get_world_size()
+    return {"value": world * n * pb / (ms * 1e-3) / GB, "unit": UNIT, "h2d_bytes_per_step": 2 * n * 4,
+            "d2h_bytes_per_step": pb, "ms_per_step": ms, "steps": steps,
+            "path": "block tables pinned HOST -> H2D, kvx_copy_pages per layer into the peer pool (IPC), "
+                    "landed probe page D2H"}
 
 
 # ---------------------------------------------------------------------------
@@ -749,7 +986,8 @@ def arm_config(cfg, world):
                     "page into the migration buffer + unpack into a second page permutation")
     else:
         workload = (f"{cfg['model']} @{cfg['ctx']} session per rank, ring migration rank r -> r+1 "
-                    "(page-to-page into the receiver's pool)")
+                    "(page-to-page into the receiver's pool) while every rank decodes a batch of 4 "
+                    f"{cfg['model']} @{cfg['ctx']} requests")
     return {"workload": workload, "model_shape": cfg["model"], "seq_len": cfg["ctx"], "layers": cfg["layers"],
             "kv_heads": cfg["kv_heads"], "head_dim": cfg["head_dim"], "kv_dtype": "bf16", "page_bytes": pb,
             "session_bytes": n * pb, "parallelism": "single" if world == 1 else f"ring-p2p{world}",
@@ -820,9 +1058,14 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-overlap", action="store_true")
     ap.add_argument("--attn-sweep", action="store_true", help="diagnostic: time fixed split-K factors")
+    ap.add_argument("--bg-sweep", action="store_true", help="diagnostic: sweep mover CTA caps beside decode")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help="N>1 control plane")
     ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
     ap.add_argument("--layers", type=int, default=0, help="test mode: shrink the N>1 session")
+    ap.add_argument("--migrate-mode", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1: K3 stores into the peer pool (p2p) or pack + send/recv + unpack (nccl)")
+    ap.add_argument("--mig-ctas", type=int, default=0, help="N>1: cap on the migration mover's CTAs (0 = all)")
+    ap.add_argument("--serve-batch", type=int, default=4, help="N>1: decode batch run beside the migration")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -860,6 +1103,11 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": arm_config(cfg, world),
                 "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["gpu_launches"]}
+        if world > 1:
+            line["serving"] = res["serving"]
+            if res["e2e"] is not None:
+                line["e2e"] = res["e2e"]
+            line["config"]["migrate_mode"] = args.migrate_mode
         if world == 1:
             line["e2e"] = res["e2e"]
             line["decode_attention"] = res["attention"]

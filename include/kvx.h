@@ -154,6 +154,13 @@ int kvx_unpack(kvx_pool* dst, const uint32_t* d_page_ids, uint64_t n, const void
  * takes host arrays. */
 int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
                    uint64_t n, int mode, void* stream);
+/* Background migration (the reference's NetArrive moves, kvstore.cpp:753-769,
+ * run off the serving path): kvx_copy_pages with the SM movers' grid bounded
+ * to max_ctas CTAs (0 = unbounded), so a migration running beside decode
+ * occupies a fixed slice of the SMs and paces its HBM/NVLink traffic.
+ * Ignored for KVX_COPY_CE. */
+int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
+                          uint64_t n, int mode, uint32_t max_ctas, void* stream);
 
 /* ---- contents (K5) ------------------------------------------------------ */
 int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,

@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
 // AUTO picks the TMA bulk mover when both sides are in this GPU's HBM (measured
 // faster: ~95% vs ~88% of the copy roofline, profiles/), and the SM vector
 // mover for peer (NVLink) or mapped-host (PCIe) endpoints.
-int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const char* who, bool tma_ok) {
+int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const char* who, bool tma_ok,
+                uint32_t max_ctas = 0) {
   if (a.n_pages == 0) return KVX_OK;
   DeviceGuard guard(device);
   if (a.page_bytes % 16 != 0 || reinterpret_cast<uintptr_t>(a.src) % 16 || reinterpret_cast<uintptr_t>(a.dst) % 16)
@@ -167,14 +168,16 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
       configured[dev] = smem;
     }
     const uint64_t items = a.n_pages * a.chunks_per_page;
-    const unsigned grid =
+    unsigned grid =
         static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * geo.ctas_per_sm));
+    if (max_ctas && grid > max_ctas) grid = max_ctas;
     page_move_bulk<<<grid, 32, smem, stream>>>(a);
   } else if (mode == KVX_COPY_SM) {
     a.chunk_bytes = kVecChunk;
     a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + kVecChunk - 1) / kVecChunk);
     const uint64_t items = a.n_pages * a.chunks_per_page;
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * 8));
+    unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * 8));
+    if (max_ctas && grid > max_ctas) grid = max_ctas;
     page_move_vec<<<grid, kVecThreads, 0, stream>>>(a);
   } else {
     set_error(std::string(who) + ": unsupported copy mode");
@@ -262,6 +265,11 @@ int kvx_unpack(kvx_pool* dst, const uint32_t* d_page_ids, uint64_t n, const void
 
 int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
                    uint64_t n, int mode, void* stream) {
+  return kvx_copy_pages_capped(src, src_ids, dst, dst_ids, n, mode, 0, stream);
+}
+
+int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
+                          uint64_t n, int mode, uint32_t max_ctas, void* stream) {
   if (!src || !dst || (n && (!src_ids || !dst_ids))) return kvx::fail_arg("kvx_copy_pages: null argument");
   if (src->page_bytes != dst->page_bytes) return kvx::fail_arg("kvx_copy_pages: page size mismatch");
   if (n == 0) return KVX_OK;
@@ -270,7 +278,7 @@ int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, 
     MoveArgs a{src->base, src_ids, dst->base, dst_ids, n, src->page_bytes, 0, 0, 0, src->num_pages, dst->num_pages};
     const int dev = src->device >= 0 ? src->device : dst->device;
     const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
-    return kvx::launch_move(a, mode, dev, st, "kvx_copy_pages", local);
+    return kvx::launch_move(a, mode, dev, st, "kvx_copy_pages", local, max_ctas);
   }
   // Copy engines: coalesce runs of consecutive ids, one batched submission.
   std::vector<void*> dsts, srcs;

@@ -70,6 +70,7 @@ def lib() -> C.CDLL:
         "kvx_pack": ([V, V, U64, V, C.c_int, V], C.c_int),
         "kvx_unpack": ([V, V, U64, V, C.c_int, V], C.c_int),
         "kvx_copy_pages": ([V, V, V, V, U64, C.c_int, V], C.c_int),
+        "kvx_copy_pages_capped": ([V, V, V, V, U64, C.c_int, C.c_uint32, V], C.c_int),
         "kvx_fill_pages": ([V, V, V, U64, U64, P(PageLayout), C.c_int, V], C.c_int),
         "kvx_append_kv": ([V, P(PageLayout), V, V, V, V, U64, V], C.c_int),
         "kvx_decode_attention_workspace": ([P(PageLayout), P(AttnParams), C.c_int32, C.c_int32], U64),
@@ -205,7 +206,14 @@ def unpack(pool: Pool, page_ids, n: int, src, mode: int = COPY_AUTO, stream=None
     check(lib().kvx_unpack(pool.handle, _ptr(page_ids), n, _ptr(src), mode, _stream(stream)))
 
 
-def copy_pages(src: Pool, src_ids, dst: Pool, dst_ids, n: int, mode: int = COPY_AUTO, stream=None) -> None:
+def copy_pages(src: Pool, src_ids, dst: Pool, dst_ids, n: int, mode: int = COPY_AUTO, stream=None,
+               max_ctas: int = 0) -> None:
+    """K3 page -> page. max_ctas > 0 bounds the SM movers' grid (background
+    migration beside decode, kvx_copy_pages_capped)."""
+    if max_ctas and mode != COPY_CE:
+        check(lib().kvx_copy_pages_capped(src.handle, _ptr(src_ids), dst.handle, _ptr(dst_ids), n, mode, max_ctas,
+                                          _stream(stream)))
+        return
     if mode == COPY_CE:
         import numpy as np
         s = np.ascontiguousarray(src_ids, dtype=np.uint32)

@@ -122,6 +122,28 @@ def test_copy_pages_between_pools_bit_exact(dev, mode):
     assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
 
 
+@pytest.mark.parametrize("mode", [kvx.COPY_SM, kvx.COPY_TMA])
+@pytest.mark.parametrize("cap", [1, 3, 17])
+def test_capped_copy_bit_exact(dev, mode, cap):
+    """Background migration with the mover's grid capped (kvx_copy_pages_capped):
+    fewer CTAs than work items, every page still lands bit-exact."""
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(cap)
+    n, pages = 150, 400
+    src_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    dst_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    src, ref = filled_pool(layout, pages, src_ids, O.tags_array(4, 2, np.arange(n)), 13, kvx.FILL_BITS, dev)
+    dst = kvx.Pool(pages, pb, device=0)
+    dst.as_tensor().zero_()
+    kvx.copy_pages(src, to_dev(src_ids.view(np.int32), dev), dst, to_dev(dst_ids.view(np.int32), dev), n, mode,
+                   max_ctas=cap)
+    torch.cuda.synchronize()
+    ref_dst = np.zeros((pages, pb), np.uint8)
+    O.copy_pages(ref, src_ids, ref_dst, dst_ids, pb)
+    assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
+
+
 def test_host_pool_zero_copy_roundtrip(dev):
     """DEVICE -> mapped pinned HOST pool -> DEVICE with the SM mover (PCIe)."""
     layout = TINY
