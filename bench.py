@@ -651,50 +651,61 @@ def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):
     h_in = torch.empty(L * lb, dtype=torch.uint8).pin_memory()
     h_in.view(torch.int64).random_()
     h_out = torch.empty_like(h_in).pin_memory()
-    stage_in = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(2)]
-    stage_out = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    NB = 3  # staging slots per direction: H2D of layer g+2 overlaps compute of g+1 and D2H of g
+    stage_in = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(NB)]
+    stage_out = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(NB)]
     s_in, s_c, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     main = torch.cuda.current_stream(dev)
+    done_c, done_out = {}, {}  # global layer index -> event (slot reuse across step boundaries)
 
-    def step():
-        e_in = [torch.cuda.Event() for _ in range(L)]
-        e_c = [torch.cuda.Event() for _ in range(L)]
-        e_out = [torch.cuda.Event() for _ in range(L)]
-        s_in.wait_stream(main)
+    def step(k):
+        """Step k moves every layer in and out; layers of consecutive steps
+        stream back to back (a slot waits only for the layer that last used
+        it), as a serving node streams sessions through its HOST tier."""
         for l in range(L):
+            g = k * L + l
+            slot = g % NB
             with torch.cuda.stream(s_in):
-                if l >= 2:
-                    s_in.wait_event(e_c[l - 2])
-                stage_in[l % 2].copy_(h_in[l * lb:(l + 1) * lb], non_blocking=True)
-                e_in[l].record(s_in)
-            s_c.wait_event(e_in[l])
-            if l >= 2:
-                s_c.wait_event(e_out[l - 2])
+                if g - NB in done_c:
+                    s_in.wait_event(done_c.pop(g - NB))
+                stage_in[slot].copy_(h_in[l * lb:(l + 1) * lb], non_blocking=True)
+                e_in = torch.cuda.Event()
+                e_in.record(s_in)
+            s_c.wait_event(e_in)
+            if g - NB in done_out:
+                s_c.wait_event(done_out.pop(g - NB))
             ids = d_dst[l * blocks:(l + 1) * blocks]
-            kvx.unpack(pool, ids, blocks, stage_in[l % 2], kvx.COPY_AUTO, s_c)
-            kvx.pack(pool, ids, blocks, stage_out[l % 2], kvx.COPY_AUTO, s_c)
-            e_c[l].record(s_c)
+            kvx.unpack(pool, ids, blocks, stage_in[slot], kvx.COPY_AUTO, s_c)
+            kvx.pack(pool, ids, blocks, stage_out[slot], kvx.COPY_AUTO, s_c)
+            e_c = torch.cuda.Event()
+            e_c.record(s_c)
+            done_c[g] = e_c
             with torch.cuda.stream(s_out):
-                s_out.wait_event(e_c[l])
-                h_out[l * lb:(l + 1) * lb].copy_(stage_out[l % 2], non_blocking=True)
-                e_out[l].record(s_out)
-        main.wait_stream(s_out)
+                s_out.wait_event(e_c)
+                h_out[l * lb:(l + 1) * lb].copy_(stage_out[slot], non_blocking=True)
+                e_out = torch.cuda.Event()
+                e_out.record(s_out)
+                done_out[g] = e_out
 
     steps = max(3, min(args.steps, 10))
-    for _ in range(max(1, min(args.warmup, 3))):
-        step()
+    warm = max(1, min(args.warmup, 3))
+    for k in range(warm):
+        step(k)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(main)
-    for _ in range(steps):
-        step()
+    s_in.wait_stream(main)
+    for k in range(warm, warm + steps):
+        step(k)
+    main.wait_stream(s_out)
     t1.record(main)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
     assert torch.equal(h_in, h_out), "end-to-end roundtrip differs"
     return {"value": (L * lb) / (ms * 1e-3) / GB, "unit": UNIT, "h2d_bytes_per_step": L * lb,
             "d2h_bytes_per_step": L * lb, "ms_per_step": ms, "steps": steps,
-            "path": "pinned HOST -> H2D -> kvx_unpack -> kvx_pack -> D2H -> pinned HOST, per layer, 3 streams"}
+            "path": "pinned HOST -> H2D -> kvx_unpack -> kvx_pack -> D2H -> pinned HOST, per layer, 3 streams, "
+                    "3 staging slots per direction, layers of consecutive steps streamed back to back"}
 
 
 def bench_multi(args, torch, np, kvx, dev, rank, world):

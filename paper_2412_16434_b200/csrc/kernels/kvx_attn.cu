@@ -315,19 +315,26 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   l_r8 += __shfl_xor_sync(0xffffffffu, l_r8, 1);
   l_r8 += __shfl_xor_sync(0xffffffffu, l_r8, 2);
 
-  // Combine the 4 warps of the CTA through shared memory (reusing the rings).
+  // Combine the W warps of the CTA through shared memory (reusing the rings).
+  // Only the group's rows are real (the rest is mma padding); rows are padded
+  // to kOs floats so the 8-byte fragment stores of a warp hit distinct banks
+  // (a 128-float stride put all 8 row-lanes of a column on one bank).
   __syncthreads();
-  float* so = reinterpret_cast<float*>(smem);                   // [warp][16][128]
-  float* sml = so + W * 16 * kD;                                // [warp][16][2]
+  constexpr int kOs = kD + 8;
+  float* so = reinterpret_cast<float*>(smem);                   // [warp][16][kOs]
+  float* sml = so + W * 16 * kOs;                               // [warp][16][2]
   {
     const int r = lane >> 2, c = (lane & 3) * 2;
-    float* ow = so + warp * 16 * kD;
+    float* ow = so + warp * 16 * kOs;
+    if (r < a.group) {
 #pragma unroll
-    for (int n = 0; n < kD / 8; ++n) {
-      ow[r * kD + n * 8 + c] = o[n][0];
-      ow[r * kD + n * 8 + c + 1] = o[n][1];
-      ow[(r + 8) * kD + n * 8 + c] = o[n][2];
-      ow[(r + 8) * kD + n * 8 + c + 1] = o[n][3];
+      for (int n = 0; n < kD / 8; ++n)
+        *reinterpret_cast<float2*>(ow + r * kOs + n * 8 + c) = make_float2(o[n][0], o[n][1]);
+    }
+    if (r + 8 < a.group) {
+#pragma unroll
+      for (int n = 0; n < kD / 8; ++n)
+        *reinterpret_cast<float2*>(ow + (r + 8) * kOs + n * 8 + c) = make_float2(o[n][2], o[n][3]);
     }
     if ((lane & 3) == 0) {
       sml[(warp * 16 + r) * 2] = m_r;
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     for (int w = 0; w < W; ++w) {
       const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
       L += f * sml[(w * 16 + r) * 2 + 1];
-      O += f * so[(w * 16 + r) * kD + d];
+      O += f * so[(w * 16 + r) * kOs + d];
     }
     const uint64_t row = static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r;
     if (a.splits == 1) {
