@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "kvx_common.cuh"
@@ -97,19 +98,27 @@ __device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 // Address of the same shared-memory variable in CTA `rank` of the cluster.
 __device__ __forceinline__ uint32_t map_rank(uint32_t smem_addr, uint32_t rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
+__device__ __forceinline__ void st_dsmem(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+// Arrive (release, cluster scope) on an mbarrier in another CTA's shared memory.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
 }
 
 // Byte offset of 16-B chunk `col16` (0..15) of tile row `row` (0..15): rows
@@ -143,8 +152,24 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint32_t s_pages[kMaxPagesPerCta];
   __shared__ int s_last;
+  // Cluster merge (push): CTA s of a (request, kv head) cluster owns output
+  // slice s; every CTA pushes its partial of each slice into the owner's
+  // s_recv_o / s_recv_ml over DSMEM and arrives on the owner's s_merge_bar.
+  // Outside the page ring, so pushes may land while the owner still streams.
+  __shared__ float s_recv_o[16 * kD + kMaxClusterSplits];
+  __shared__ float s_recv_ml[kMaxClusterSplits * 16 * 2];
+  __shared__ __align__(8) uint64_t s_merge_bar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  if (a.cluster_merge) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s_merge_bar, static_cast<uint32_t>(a.splits));
+      fence_mbar_init();
+    }
+    // Publishes the barrier init to the cluster; the matching wait comes
+    // after the page loop, long after every CTA has arrived here.
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  }
   // Programmatic dependent launch: this CTA may be resident before the
   // previous kernel on the stream (e.g. the prior layer, or the append of
   // this step's K/V) has finished; everything we read may be its output, so
@@ -345,10 +370,8 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   }
   __syncthreads();
   const int rows = a.group;
-  // DSMEM merge: this CTA's combined partial stays in its own shared memory
-  // ([16][128] O, [16][2] (m, l)) for the cluster to read.
-  float* cta_o = sml + W * 32;
-  float* cta_ml = cta_o + 16 * kD;
+  const int chunk = (rows * kD + a.splits - 1) / a.splits;  // output slice per cluster CTA
+  if (a.cluster_merge) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // peers' barriers initialised
   for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
     const int r = e / kD, d = e - r * kD;
     float M = -INFINITY;
@@ -366,10 +389,13 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     if (a.splits == 1) {
       a.out[row * kD + d] = L > 0.f ? O / L : 0.f;
     } else if (a.cluster_merge) {
-      cta_o[r * kD + d] = O;
+      const int owner = e / chunk;
+      st_dsmem(map_rank(smem_u32(s_recv_o + split * chunk + (e - owner * chunk)), owner), O);
       if (d == 0) {
-        cta_ml[r * 2] = M;
-        cta_ml[r * 2 + 1] = L;
+        for (int s2 = 0; s2 < a.splits; ++s2) {
+          st_dsmem(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2), s2), M);
+          st_dsmem(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2 + 1), s2), L);
+        }
       }
     } else {
       a.part_o[(row * a.splits + split) * kD + d] = O;
@@ -383,41 +409,30 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   if (a.splits == 1) return;
 
   if (a.cluster_merge) {
-    // The cluster is this (request, kv head)'s `splits` CTAs (cluster rank ==
-    // split). One cluster barrier publishes every CTA's partial; each CTA then
-    // merges a 1/splits slice of the output elements, reading all partials
-    // with one round of independent DSMEM loads; a second barrier keeps every
-    // CTA's shared memory alive until all readers are done.
-    cluster_sync_all();
-    const uint32_t o_s = smem_u32(cta_o), ml_s = smem_u32(cta_ml);
+    // Our pushes are in flight to every owner: make them visible at cluster
+    // scope, then one release-arrive per owner. Each CTA then waits for all
+    // `splits` partials of its own slice and merges it from local shared
+    // memory. No CTA exits before every push into it has arrived, and none
+    // reads another CTA's memory, so no closing cluster barrier is needed.
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < a.splits) mbar_arrive_remote(map_rank(smem_u32(&s_merge_bar), threadIdx.x));
+    mbar_wait_cluster(&s_merge_bar, 0);
     const int ns = a.splits;
-    for (int e = split * blockDim.x + threadIdx.x; e < rows * kD; e += ns * blockDim.x) {
-      const int r = e / kD, d = e - r * kD;
-      float m[kMaxClusterSplits], l[kMaxClusterSplits], ov[kMaxClusterSplits];
-#pragma unroll
-      for (int s2 = 0; s2 < kMaxClusterSplits; ++s2) {
-        if (s2 < ns) {
-          m[s2] = ld_dsmem(map_rank(ml_s + r * 8, s2));
-          l[s2] = ld_dsmem(map_rank(ml_s + r * 8 + 4, s2));
-          ov[s2] = ld_dsmem(map_rank(o_s + (r * kD + d) * 4, s2));
-        }
-      }
+    const int e_end = min(rows * kD, (split + 1) * chunk);
+    for (int e = split * chunk + threadIdx.x; e < e_end; e += blockDim.x) {
+      const int r = e / kD, d = e - r * kD, off = e - split * chunk;
       float M = -INFINITY;
-#pragma unroll
-      for (int s2 = 0; s2 < kMaxClusterSplits; ++s2)
-        if (s2 < ns) M = fmaxf(M, m[s2]);
+      for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, s_recv_ml[(s2 * 16 + r) * 2]);
       const float Mb = M == -INFINITY ? 0.f : M;
       float L = 0.f, O = 0.f;
-#pragma unroll
-      for (int s2 = 0; s2 < kMaxClusterSplits; ++s2)
-        if (s2 < ns) {
-          const float f = exp2f(m[s2] - Mb);
-          L += f * l[s2];
-          O += f * ov[s2];
-        }
+      for (int s2 = 0; s2 < ns; ++s2) {
+        const float f = exp2f(s_recv_ml[(s2 * 16 + r) * 2] - Mb);
+        L += f * s_recv_ml[(s2 * 16 + r) * 2 + 1];
+        O += f * s_recv_o[s2 * chunk + off];
+      }
       a.out[(static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
     }
-    cluster_sync_all();
     KVX_TRACE(6);
     return;
   }
@@ -534,20 +549,25 @@ bool fast_path(const kvx_page_layout* l) {
   return l->dtype == KVX_DTYPE_BF16 && l->head_dim == kD && l->block_tokens == kT;
 }
 
-// Split-K factor, from the B200 split sweeps (profiles/r01_summary.md, ctx
-// 8192): the largest split count with (requests x kv heads x splits) <= half
-// the SM count, bounded by the block-table staging limit and by >= 16 pages
-// per CTA.
+// Split-K factor, from the B200 split sweeps (profiles/r01_attn_split_sweep_long.jsonl:
+// batch 1-16 x ctx 8K/32K x 32/64 q heads, every split count, both merges).
+// One-wave grids (8 warps per CTA, one CTA per SM) are best with ~2/3 of the
+// SMs streaming: splits = round(0.65 * SMs / (requests x kv heads)) (batch 2
+// -> 6, 4 -> 3, 8 -> 2, 16 -> 1; batch 1 -> 12, which plan_attention steps
+// down to the largest co-resident cluster). A sub-wave grid of 2-CTA/SM
+// blocks over a very long context (>= 1024 pages per CTA) is split 4x more
+// so the CTAs balance over the SMs (batch 16 x 32K: 2 -> 8 splits, -5%).
+// Bounded by the block-table staging limit and by >= 16 pages per CTA.
 int choose_splits(int batch, int heads, int max_ctx, int requested, int sms) {
   const int pages = std::max(1, (max_ctx + kT - 1) / kT);
   const int min_splits = (pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
   if (requested > 0) return std::max(requested, min_splits);
   const int max_splits = std::max(min_splits, pages / (kWarps * 4));
   const long base = std::max(1L, static_cast<long>(batch) * heads);
-  // One-wave grids run 8 warps per CTA; measured best there at ~half an SM
-  // count of CTAs (batch 1 -> 9 splits, batch 8 -> 1).
-  const int fill = static_cast<int>(std::max(1L, sms / (2 * base)));
-  return std::max(min_splits, std::min(max_splits, std::min(fill, 256)));
+  int s = std::max(min_splits, static_cast<int>(std::lround(0.65 * sms / static_cast<double>(base))));
+  s = std::max(1, std::min(s, 256));
+  if (s * base > sms && s * base < 2L * sms && pages / s >= 1024) s *= 4;
+  return std::max(min_splits, std::min(max_splits, s));
 }
 
 uint64_t workspace_for(uint64_t batch, uint64_t hq, uint64_t heads, int splits) {
@@ -621,10 +641,18 @@ Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge,
   const int min_splits = (pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
   Plan p{choose_splits(batch, heads, max_ctx, requested, sms), false, false};
   if (merge != KVX_MERGE_GLOBAL) {
-    const int s = p.splits;
-    const bool ok = s >= 2 && s <= kMaxClusterSplits && s >= min_splits && groups * s <= sms &&
-                    cluster_capacity(device, s) >= (requested > 0 ? 1 : groups);
-    if (ok) p = Plan{s, true, true};
+    // The largest cluster size in [~3/4 of the target, target] whose clusters
+    // are all co-resident (one wave); explicit split counts are taken as is.
+    const int target = p.splits;
+    const int lowest = requested > 0 ? target : std::max(2, (3 * target + 3) / 4);
+    for (int s = std::min(target, kMaxClusterSplits); s >= lowest; --s) {
+      const bool ok = s >= 2 && s >= min_splits && groups * s <= sms &&
+                      cluster_capacity(device, s) >= (requested > 0 ? 1 : groups);
+      if (ok) {
+        p = Plan{s, true, true};
+        break;
+      }
+    }
   }
   if (!p.cluster) p.narrow = static_cast<long>(p.splits) * groups <= sms;
   return p;
@@ -703,11 +731,14 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     attr[1].val.clusterDim.x = plan.cluster ? splits : 1;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
-    // Cluster launches go without PDL: early-resident dependent clusters cost
-    // 2-15 us per launch at >= 32K context on B200 (tools/attn_trace.cu,
-    // profiles/r01_summary.md); without PDL the cluster merge is at least as
-    // fast as the global merge at every measured shape under graph replay.
-    if (plan.cluster) attr[0].val.programmaticStreamSerializationAllowed = 0;
+    // Cluster launches go without PDL: early-resident dependent clusters
+    // cost 4-11 us per launch at batch 1 and >= 32K context and ~6% at batch
+    // 8 x 32K; the 0.3-0.5 us PDL gains at batch 2-4 x 8K do not pay for that
+    // (profiles/attn_trace/r01_cluster_pdl.log). KVX_ATTN_CLUSTER_PDL=1
+    // forces it on (measurement knob).
+    static const char* cluster_pdl_env = std::getenv("KVX_ATTN_CLUSTER_PDL");
+    const bool cluster_pdl = cluster_pdl_env && cluster_pdl_env[0] == '1';
+    if (plan.cluster && !cluster_pdl) attr[0].val.programmaticStreamSerializationAllowed = 0;
     cfg.attrs = attr;
     cfg.numAttrs = plan.cluster ? 2 : 1;
     if (narrow)

@@ -6,7 +6,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude \
 //     tools/attn_trace.cu paper_2412_16434_b200/csrc/kernels/kvx_pool.cu \
 //     paper_2412_16434_b200/csrc/kernels/kvx_copy.cu -lcuda -o build/attn_trace
-//   build/attn_trace BATCH CTX [SPLITS [MERGE]]
+//   build/attn_trace BATCH CTX [SPLITS [MERGE [Q_HEADS]]]   (Q_HEADS 32: Llama-3.1-8B, 64: 70B)
 #include <cstdint>
 __device__ unsigned long long kvx_attn_trace[8 * 65536];
 #define KVX_ATTN_TRACE 1
@@ -39,7 +39,7 @@ int main(int argc, char** argv) {
   const int ctx = argc > 2 ? atoi(argv[2]) : 8192;
   const int splits_req = argc > 3 ? atoi(argv[3]) : 0;
   const int merge = argc > 4 ? atoi(argv[4]) : KVX_MERGE_AUTO;
-  const int H = 8, Hq = 32, D = 128, T = 16;
+  const int H = 8, Hq = argc > 5 ? atoi(argv[5]) : 32, D = 128, T = 16;
   kvx_page_layout lay{H, D, T, KVX_DTYPE_BF16};
   const uint64_t pb = kvx_page_bytes(&lay);
   const int blocks = (ctx + T - 1) / T;
@@ -137,9 +137,9 @@ int main(int argc, char** argv) {
   int sms_used = 0, max_per_sm = 0;
   for (int v : sm_use) { sms_used += v > 0; max_per_sm = std::max(max_per_sm, v); }
   const double bytes = static_cast<double>(batch) * ctx * H * D * 2 * 2;
-  printf("{\"batch\": %d, \"ctx\": %d, \"splits\": %d, \"cluster\": %d, \"ctas\": %d, \"sms_used\": %d, \"max_ctas_per_sm\": %d, "
+  printf("{\"hq\": %d, \"batch\": %d, \"ctx\": %d, \"splits\": %d, \"cluster\": %d, \"ctas\": %d, \"sms_used\": %d, \"max_ctas_per_sm\": %d, "
          "\"us_per_launch\": %.2f, \"us_graph\": %.2f, \"gbs\": %.0f, \"traced_span_us\": %.2f}\n",
-         batch, ctx, splits, plan.cluster ? 1 : 0, ctas, sms_used, max_per_sm, us_launch, us_graph, bytes / us_launch * 1e-3, (tend - t0) * 1e-3);
+         Hq, batch, ctx, splits, plan.cluster ? 1 : 0, ctas, sms_used, max_per_sm, us_launch, us_graph, bytes / us_launch * 1e-3, (tend - t0) * 1e-3);
   auto row = [](const char* n, const std::vector<double>& v) {
     printf("  %-10s p0 %7.2f  p50 %7.2f  p90 %7.2f  max %7.2f us\n", n, pct(v, 0), pct(v, .5), pct(v, .9), pct(v, 1));
   };
