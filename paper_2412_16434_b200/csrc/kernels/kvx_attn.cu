@@ -55,21 +55,22 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Per-CTA timeline stamps (%globaltimer) for tools/attn_trace.cu, which
 // includes this file with KVX_ATTN_TRACE defined; compiled out otherwise.
 #ifdef KVX_ATTN_TRACE
-__device__ __forceinline__ void trace_mark(int slot) {
-  if (threadIdx.x != 0) return;
+__device__ __forceinline__ void trace_stamp(int slot) {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   const uint64_t cta = (static_cast<uint64_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  kvx_attn_trace[cta * 8 + slot] = t;
+  kvx_attn_trace[cta * 32 + slot] = t;
   if (slot == 0) {
     uint32_t sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    kvx_attn_trace[cta * 8 + 7] = sm;
+    kvx_attn_trace[cta * 32 + 31] = sm;
   }
 }
-#define KVX_TRACE(slot) trace_mark(slot)
+#define KVX_TRACE(slot) (threadIdx.x == 0 ? trace_stamp(slot) : (void)0)
+#define KVX_TRACE_IF(cond, slot) ((cond) ? trace_stamp(slot) : (void)0)
 #else
 #define KVX_TRACE(slot) ((void)0)
+#define KVX_TRACE_IF(cond, slot) ((void)0)
 #endif
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
@@ -104,12 +105,19 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t smem_addr, uint32_t rank) 
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void st_dsmem(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+// Asynchronous stores into another CTA's shared memory that count their
+// bytes on that CTA's mbarrier (complete_tx): no fence, no separate arrive.
+__device__ __forceinline__ void st_async_v4(uint32_t cluster_addr, float4 v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cluster_addr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(cluster_bar)
+               : "memory");
 }
-// Arrive (release, cluster scope) on an mbarrier in another CTA's shared memory.
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+__device__ __forceinline__ void st_async_v2(uint32_t cluster_addr, float x, float y, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+                   cluster_addr),
+               "f"(x), "f"(y), "r"(cluster_bar)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
   asm volatile(
@@ -156,19 +164,26 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   // slice s; every CTA pushes its partial of each slice into the owner's
   // s_recv_o / s_recv_ml over DSMEM and arrives on the owner's s_merge_bar.
   // Outside the page ring, so pushes may land while the owner still streams.
-  __shared__ float s_recv_o[16 * kD + kMaxClusterSplits];
-  __shared__ float s_recv_ml[kMaxClusterSplits * 16 * 2];
+  __shared__ __align__(16) float s_recv_o[16 * kD + 4 * kMaxClusterSplits];
+  __shared__ __align__(16) float s_recv_ml[kMaxClusterSplits * 16 * 2];
+  __shared__ float s_recv_w[8 * 16 + 16 * 2];
   __shared__ __align__(8) uint64_t s_merge_bar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  // Output slice per cluster CTA, in float4 units so no vector push straddles
+  // two owners.
+  const int chunk = ((a.group * kD + a.splits - 1) / a.splits + 3) & ~3;
   if (a.cluster_merge) {
     if (threadIdx.x == 0) {
-      mbar_init(&s_merge_bar, static_cast<uint32_t>(a.splits));
+      // One arrival (ours, with the byte count) + every partial's bytes.
+      const int len = max(0, min(chunk, a.group * kD - split * chunk));
+      mbar_init(&s_merge_bar, 1);
       fence_mbar_init();
+      mbar_arrive_expect_tx(&s_merge_bar, static_cast<uint32_t>(a.splits * (len * 4 + a.group * 8)));
     }
-    // Publishes the barrier init to the cluster; the matching wait comes
-    // after the page loop, long after every CTA has arrived here.
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    // Publishes the barrier (and its expected bytes) to the cluster; the
+    // matching wait comes after the page loop, long after every CTA arrived.
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   }
   // Programmatic dependent launch: this CTA may be resident before the
   // previous kernel on the stream (e.g. the prior layer, or the append of
@@ -218,7 +233,10 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
 
   uint8_t* ring = smem + warp * (kStages * kStageBytes);
   const uint32_t ring_s = smem_u32(ring);
-  // This warp's pages: p_begin + warp, + W, ...
+  // This warp's pages: p_begin + warp, + W, ... — a static deal, so every
+  // launch sums each page into the same warp's partial in the same order
+  // (bit-identical outputs run to run). A dynamic dealer (CTA-wide counter)
+  // was measured at 0-4% faster and gave up that determinism.
   const int my_first = p_begin + warp;
   const int my_count = my_first < p_end ? (p_end - my_first + W - 1) / W : 0;
 
@@ -330,6 +348,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   }
   cp_async_wait<0>();
   KVX_TRACE(4);
+  KVX_TRACE_IF(lane == 0, 16 + warp);  // per-warp loop end (slots 16..16+W-1)
   // All our global reads of the pool are done: let the next kernel's CTAs
   // start launching into SMs as ours drain.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -345,6 +364,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   // to kOs floats so the 8-byte fragment stores of a warp hit distinct banks
   // (a 128-float stride put all 8 row-lanes of a column on one bank).
   __syncthreads();
+  KVX_TRACE(8);
   constexpr int kOs = kD + 8;
   float* so = reinterpret_cast<float*>(smem);                   // [warp][16][kOs]
   float* sml = so + W * 16 * kOs;                               // [warp][16][2]
@@ -370,54 +390,59 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   }
   __syncthreads();
   const int rows = a.group;
-  const int chunk = (rows * kD + a.splits - 1) / a.splits;  // output slice per cluster CTA
-  if (a.cluster_merge) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // peers' barriers initialised
-  for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
-    const int r = e / kD, d = e - r * kD;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < W; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
-    const float Mb = M == -INFINITY ? 0.f : M;
-    float L = 0.f, O = 0.f;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
-      L += f * sml[(w * 16 + r) * 2 + 1];
-      O += f * so[(w * 16 + r) * kOs + d];
-    }
-    const uint64_t row = static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r;
-    if (a.splits == 1) {
-      a.out[row * kD + d] = L > 0.f ? O / L : 0.f;
-    } else if (a.cluster_merge) {
-      const int owner = e / chunk;
-      st_dsmem(map_rank(smem_u32(s_recv_o + split * chunk + (e - owner * chunk)), owner), O);
-      if (d == 0) {
-        for (int s2 = 0; s2 < a.splits; ++s2) {
-          st_dsmem(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2), s2), M);
-          st_dsmem(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2 + 1), s2), L);
-        }
-      }
-    } else {
-      a.part_o[(row * a.splits + split) * kD + d] = O;
-      if (d == 0) {
-        a.part_ml[(row * a.splits + split) * 2] = M;
-        a.part_ml[(row * a.splits + split) * 2 + 1] = L;
-      }
-    }
-  }
-  KVX_TRACE(5);
-  if (a.splits == 1) return;
-
   if (a.cluster_merge) {
-    // Our pushes are in flight to every owner: make them visible at cluster
-    // scope, then one release-arrive per owner. Each CTA then waits for all
-    // `splits` partials of its own slice and merges it from local shared
-    // memory. No CTA exits before every push into it has arrived, and none
-    // reads another CTA's memory, so no closing cluster barrier is needed.
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    // Per-row weights of each warp's partial, then pushes: every CTA sends
+    // its (m, l) per row to every owner (one 8-byte st.async per (row, owner))
+    // and each float4 of its partial O to the owner of that slice. The
+    // owner's mbarrier completes when all bytes have landed.
+    float* s_wf = s_recv_w;  // [W][16] warp weights
+    float* s_rml = s_wf + 8 * 16;  // [16][2] this CTA's (M, L) per row
+    if (threadIdx.x < rows) {
+      const int r = threadIdx.x;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < W; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
+      const float Mb = M == -INFINITY ? 0.f : M;
+      float L = 0.f;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
+        s_wf[w * 16 + r] = f;
+        L += f * sml[(w * 16 + r) * 2 + 1];
+      }
+      s_rml[r * 2] = M;
+      s_rml[r * 2 + 1] = L;
+    }
     __syncthreads();
-    if (threadIdx.x < a.splits) mbar_arrive_remote(map_rank(smem_u32(&s_merge_bar), threadIdx.x));
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every owner's barrier is armed
+    const uint32_t bar_local = smem_u32(&s_merge_bar);
+    if (threadIdx.x < rows * a.splits) {
+      const int r = threadIdx.x / a.splits, owner = threadIdx.x - r * a.splits;
+      st_async_v2(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2), owner), s_rml[r * 2], s_rml[r * 2 + 1],
+                  map_rank(bar_local, owner));
+    }
+    for (int q = threadIdx.x; q < rows * kD / 4; q += blockDim.x) {
+      const int e = 4 * q, r = e / kD, d = e - r * kD;
+      float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float f = s_wf[w * 16 + r];
+        const float4 v = *reinterpret_cast<const float4*>(so + (w * 16 + r) * kOs + d);
+        O.x += f * v.x;
+        O.y += f * v.y;
+        O.z += f * v.z;
+        O.w += f * v.w;
+      }
+      const int owner = e / chunk;
+      st_async_v4(map_rank(smem_u32(s_recv_o + split * chunk + (e - owner * chunk)), owner), O,
+                  map_rank(bar_local, owner));
+    }
+    KVX_TRACE(5);
+    // Our slice: wait for every split's bytes, merge from local shared memory.
+    // No CTA exits before every push into it has landed and none reads
+    // another CTA's memory, so no closing cluster barrier is needed.
     mbar_wait_cluster(&s_merge_bar, 0);
+    KVX_TRACE(10);
     const int ns = a.splits;
     const int e_end = min(rows * kD, (split + 1) * chunk);
     for (int e = split * chunk + threadIdx.x; e < e_end; e += blockDim.x) {
@@ -436,6 +461,32 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     KVX_TRACE(6);
     return;
   }
+  for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
+    const int r = e / kD, d = e - r * kD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < W; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
+    const float Mb = M == -INFINITY ? 0.f : M;
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
+      L += f * sml[(w * 16 + r) * 2 + 1];
+      O += f * so[(w * 16 + r) * kOs + d];
+    }
+    const uint64_t row = static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r;
+    if (a.splits == 1) {
+      a.out[row * kD + d] = L > 0.f ? O / L : 0.f;
+    } else {
+      a.part_o[(row * a.splits + split) * kD + d] = O;
+      if (d == 0) {
+        a.part_ml[(row * a.splits + split) * 2] = M;
+        a.part_ml[(row * a.splits + split) * 2 + 1] = L;
+      }
+    }
+  }
+  KVX_TRACE(5);
+  if (a.splits == 1) return;
 
   // Split-K merge fused in: the last CTA of this (request, kv head) to finish
   // merges every split's partial (L2-resident) — no second launch.

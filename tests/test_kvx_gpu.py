@@ -279,12 +279,15 @@ def test_full_session_migration_property(dev):
     assert torch.equal(a[idx], b[idx])
 
 
-def test_attention_split_merge_reuses_workspace(dev):
-    """The in-kernel split merge leaves its arrival counters zeroed: repeated
-    launches on one workspace give identical results, for several split counts."""
+@pytest.mark.parametrize("merge", [kvx.MERGE_GLOBAL, kvx.MERGE_CLUSTER])
+def test_attention_split_merge_reuses_workspace(dev, merge):
+    """The in-kernel split merge leaves its arrival counters zeroed (global) /
+    its cluster barriers re-armed (cluster): repeated launches give
+    bit-identical results (static page deal, fixed merge order), for several
+    split counts."""
     layout = LLAMA8B
-    for splits in (2, 5, 32):
-        got0, ref = _attention_case(dev, layout, 32, [2048, 1500, 77], splits, seed=splits, merge=kvx.MERGE_GLOBAL)
+    for splits in ((2, 5, 32) if merge == kvx.MERGE_GLOBAL else (2, 5, 6)):
+        got0, ref = _attention_case(dev, layout, 32, [2048, 1500, 77], splits, seed=splits, merge=merge)
         err = np.abs(got0 - ref)
         assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (splits, err.max())
     rng = np.random.default_rng(9)
@@ -295,7 +298,7 @@ def test_attention_split_merge_reuses_workspace(dev):
     tables = to_dev(rng.permutation(pages).astype(np.int32).reshape(3, 128), dev)
     ctx = to_dev(np.array([2048, 2000, 1], np.int32), dev)
     q = to_dev(rng.integers(0x3C00, 0x3F80, (3, 32, 128)).astype(np.uint16), dev)
-    att = kvx.Attention(layout, 32, 128, num_splits=7, split_merge=kvx.MERGE_GLOBAL)
+    att = kvx.Attention(layout, 32, 128, num_splits=7 if merge == kvx.MERGE_GLOBAL else 5, split_merge=merge)
     ws = torch.zeros(att.workspace_bytes(3, 2048), dtype=torch.uint8, device=dev)
     outs = []
     for _ in range(4):

@@ -8,7 +8,7 @@
 //     paper_2412_16434_b200/csrc/kernels/kvx_copy.cu -lcuda -o build/attn_trace
 //   build/attn_trace BATCH CTX [SPLITS [MERGE [Q_HEADS]]]   (Q_HEADS 32: Llama-3.1-8B, 64: 70B)
 #include <cstdint>
-__device__ unsigned long long kvx_attn_trace[8 * 65536];
+__device__ unsigned long long kvx_attn_trace[32 * 65536];
 #define KVX_ATTN_TRACE 1
 #include "../paper_2412_16434_b200/csrc/kernels/kvx_attn.cu"
 
@@ -113,18 +113,20 @@ int main(int argc, char** argv) {
   const kvx::Plan plan = kvx::plan_attention(batch, H, ctx, splits_req, merge, 0);
   const int splits = plan.splits;
   const int ctas = splits * H * batch;
-  std::vector<unsigned long long> tr(static_cast<size_t>(ctas) * 8);
+  std::vector<unsigned long long> tr(static_cast<size_t>(ctas) * 32);
   cudaMemcpyFromSymbol(tr.data(), kvx_attn_trace, tr.size() * 8);
   if (cudaGetLastError() != cudaSuccess) { fprintf(stderr, "cuda error\n"); return 1; }
   unsigned long long t0 = ~0ull, tend = 0;
   for (int c = 0; c < ctas; ++c) {
-    t0 = std::min(t0, tr[c * 8 + 0]);
-    tend = std::max(tend, std::max(tr[c * 8 + 5], tr[c * 8 + 6]));
+    t0 = std::min(t0, tr[c * 32 + 0]);
+    tend = std::max(tend, std::max(tr[c * 32 + 5], tr[c * 32 + 6]));
   }
   std::vector<double> start, wait, table, first, loop, combine, mergev;
+  std::vector<double> warp_skew, last_warp, push, fence, mwait, mlocal;
   std::vector<int> sm_use(256, 0);
+  const int W = plan.narrow ? kvx::kNarrowW : 4;
   for (int c = 0; c < ctas; ++c) {
-    const unsigned long long* r = &tr[c * 8];
+    const unsigned long long* r = &tr[c * 32];
     start.push_back((r[0] - t0) * 1e-3);
     wait.push_back((r[1] - r[0]) * 1e-3);
     table.push_back((r[2] - r[1]) * 1e-3);
@@ -132,7 +134,19 @@ int main(int argc, char** argv) {
     loop.push_back((r[4] - r[3]) * 1e-3);
     combine.push_back((r[5] - r[4]) * 1e-3);
     if (r[6] > r[5]) mergev.push_back((r[6] - r[5]) * 1e-3);
-    sm_use[r[7] & 255]++;
+    sm_use[r[31] & 255]++;
+    unsigned long long wmin = ~0ull, wmax = 0;
+    for (int w = 0; w < W; ++w) {
+      wmin = std::min(wmin, r[16 + w]);
+      wmax = std::max(wmax, r[16 + w]);
+    }
+    warp_skew.push_back((wmax - wmin) * 1e-3);           // first to last warp out of the page loop
+    last_warp.push_back((r[8] - wmax) * 1e-3 + 0.0);      // last warp out -> CTA barrier passed
+    push.push_back((r[5] - r[8]) * 1e-3);                 // smem combine + row weights + st.async pushes
+    if (r[10] > r[5]) {
+      mwait.push_back((r[10] - r[5]) * 1e-3);             // wait for every split's partial bytes
+      mlocal.push_back((r[6] - r[10]) * 1e-3);            // local merge + output stores
+    }
   }
   int sms_used = 0, max_per_sm = 0;
   for (int v : sm_use) { sms_used += v > 0; max_per_sm = std::max(max_per_sm, v); }
@@ -150,5 +164,10 @@ int main(int argc, char** argv) {
   row("loop", loop);
   row("combine", combine);
   row("merge", mergev);
+  row("warp_skew", warp_skew);
+  row("last->bar", last_warp);
+  row("push", push);
+  row("mbar_wait", mwait);
+  row("merge_loc", mlocal);
   return 0;
 }
