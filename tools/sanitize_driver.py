@@ -26,19 +26,22 @@ for layout in (kvx.PageLayout(8, 128, 16, kvx.BF16), kvx.PageLayout(4, 64, 16, k
         kvx.pack(pool, ids, n, buf, mode)
         kvx.unpack(pool, dst, n, buf, mode)
         kvx.copy_pages(pool, ids, pool, dst, n, mode)
+        kvx.copy_pages(pool, ids, pool, dst, n, mode, max_ctas=3)  # capped background mover
     host = kvx.Pool(n, pb, host=True)
     kvx.copy_pages(pool, ids, host, torch.arange(n, dtype=torch.int32, device=dev), n, kvx.COPY_SM)
     elt = torch.bfloat16 if layout.dtype == kvx.BF16 else torch.float32
     k = torch.randn(5, layout.num_kv_heads, layout.head_dim, device=dev).to(elt)
     kvx.append_kv(pool, layout, ids[:5], torch.arange(5, dtype=torch.int32, device=dev), k, k, 5)
-    for batch, ctx, splits in ((1, 600, 0), (3, 333, 4), (2, 1024, 1)):
+    for batch, ctx, splits, merge in ((1, 600, 0, kvx.MERGE_AUTO), (3, 333, 4, kvx.MERGE_GLOBAL),
+                                      (3, 333, 4, kvx.MERGE_CLUSTER), (1, 8192, 10, kvx.MERGE_CLUSTER),
+                                      (2, 1024, 1, kvx.MERGE_AUTO)):
         blocks = (ctx + 15) // 16
         tables = torch.from_numpy(rng.integers(0, pages, (batch, blocks)).astype(np.int32)).to(dev)
         lens = torch.full((batch,), ctx, dtype=torch.int32, device=dev)
         hq = 4 * layout.num_kv_heads
         q = torch.randn(batch, hq, layout.head_dim, device=dev).to(elt)
         out = torch.empty(batch, hq, layout.head_dim, dtype=torch.float32, device=dev)
-        att = kvx.Attention(layout, hq, blocks, num_splits=splits)
+        att = kvx.Attention(layout, hq, blocks, num_splits=splits, split_merge=merge)
         ws = torch.zeros(max(att.workspace_bytes(batch, ctx), 1), dtype=torch.uint8, device=dev)
         att(pool, tables, lens, q, out, batch, ctx, ws)
 torch.cuda.synchronize()
