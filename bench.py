@@ -237,12 +237,14 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
     e2e = None if args.skip_e2e else bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst)
     overlap = None if args.skip_overlap else bench_overlap(args, torch, np, kvx, dev, hbm_peak)
     store_cycle = None if args.skip_e2e else bench_store_cycle(args, torch, np, kvx, dev)
+    disk = None if args.skip_e2e else bench_disk(args, torch, np, kvx, cfg)
     launches = 2 * args.steps
     return dict(value=value, ms_per_step=ms_per_step, extra=extra, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": ncu_traffic(dom_name), "kernel": dom_name,
                           "algorithmic_bytes_per_launch": 2 * session_bytes, "peak_kind": peak_kind},
-                attention=attention, e2e=e2e, overlap=overlap, store_cycle=store_cycle, gpu_launches=launches,
+                attention=attention, e2e=e2e, overlap=overlap, store_cycle=store_cycle, disk_tier=disk,
+                gpu_launches=launches,
                 session_bytes=session_bytes)
 
 
@@ -273,9 +275,10 @@ def graph_time_ms(torch, launch, reps, replays, warmup=2):
 
 
 def bench_attention(args, torch, np, kvx, dev, hbm_peak):
-    """K4 over one layer of Llama-3.1-8B KV at ctx 8192 (GQA 32/8), launches
-    replayed from a CUDA graph, rotating request sets so consecutive launches
-    read >= 256 MiB (> L2)."""
+    """K4 over one layer of Llama-3.1-8B KV at ctx 8192 (GQA 32/8) at batch
+    1/8/64, and of Llama-3.1-70B KV at ctx 32768 (GQA 64/8) at batch 1/4;
+    launches replayed from a CUDA graph, rotating request sets so
+    consecutive launches read >= 256 MiB (> L2)."""
     cfg = CFG_8B
     blocks = cfg["ctx"] // cfg["block_tokens"]
     layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
@@ -316,6 +319,25 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
             res[f"batch{batch}"]["cluster_sweep_gbs"] = {
                 s: round(kv_bytes / (timed(s, kvx.MERGE_CLUSTER) * 1e-3) / GB, 1)
                 for s in (2, 3, 4, 6, 8, 9, 12, 16) if batch * cfg["kv_heads"] * s <= 148}
+    # Config 3's decode shape: Llama-3.1-70B (64 q heads over 8 kv heads, GQA 8) at ctx 32768.
+    c70 = CFG_70B
+    blocks70 = c70["ctx"] // c70["block_tokens"]
+    for batch in (1, 4):
+        sets = max(1, min(pages // (batch * blocks70), -(-256 // (batch * 128))))
+        tables = [perm[s * batch * blocks70:(s + 1) * batch * blocks70].view(batch, blocks70).contiguous()
+                  for s in range(sets)]
+        ctx = torch.full((batch,), c70["ctx"], dtype=torch.int32, device=dev)
+        q = (torch.randn(batch, 64, 128, device=dev) * 0.5).to(torch.bfloat16)
+        out = torch.empty(batch, 64, 128, dtype=torch.float32, device=dev)
+        kv_bytes = batch * c70["ctx"] * 2 * c70["kv_heads"] * c70["head_dim"] * 2
+        att = kvx.Attention(layout, 64, blocks70)
+        ws = torch.zeros(max(att.workspace_bytes(batch, c70["ctx"]), 1), dtype=torch.uint8, device=dev)
+        t = graph_time_ms(torch, lambda i: att(pool, tables[i % sets], ctx, q, out, batch, c70["ctx"], ws),
+                          max(sets, 8), max(3, min(args.steps, 20)))
+        gbs = kv_bytes / (t * 1e-3) / GB
+        res[f"llama70b_ctx32k_batch{batch}"] = {"ms_per_layer": t, "hbm_gbs": gbs, "frac": gbs / hbm_peak,
+                                                "kv_bytes": kv_bytes, "rotating_sets": sets,
+                                                "timing": "cuda-graph replay"}
     return res
 
 
@@ -532,6 +554,45 @@ def background_migration(torch, kvx, decode, migrate, side, dev, session_bytes, 
             else:
                 os.environ[k] = v
     return out
+
+
+def bench_disk(args, torch, np, kvx, cfg):
+    """DISK tier as a file (kvx_pool_create_file): one 8B@8K session (1 GiB)
+    written from a pinned HOST pool to the file at a random page placement
+    (DiskWrite, kvstore.cpp:881-900) and read back into a second HOST pool
+    (LoadDiskHost, :862-866) with kvx_copy_pages(COPY_CE): preads / pwrites
+    in stream order, O_DIRECT where the filesystem allows. Device-timed with
+    CUDA events around the host callbacks; bytes verified."""
+    import shutil
+    import tempfile
+    blocks, n = session_pages(cfg)
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    host = kvx.Pool(n, pb, host=True)
+    back = kvx.Pool(n, pb, host=True)
+    host.as_tensor().view(torch.int64).random_()
+    d = tempfile.mkdtemp(prefix="kvx_disk_", dir=os.environ.get("KVX_DISK_DIR", "/tmp"))
+    try:
+        disk = kvx.Pool.file(os.path.join(d, "disk.pages"), n, pb)
+        ids = np.arange(n, dtype=np.uint32)
+        place = np.random.default_rng(11).permutation(n).astype(np.uint32)
+        st = torch.cuda.Stream()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(st)
+        kvx.copy_pages(host, ids, disk, place, n, kvx.COPY_CE, stream=st)
+        ev[1].record(st)
+        kvx.copy_pages(disk, place, back, ids, n, kvx.COPY_CE, stream=st)
+        ev[2].record(st)
+        st.synchronize()
+        probe = np.random.default_rng(12).integers(0, n, 256)
+        assert torch.equal(back.as_tensor()[probe], host.as_tensor()[probe]), "disk round trip differs"
+        w_ms, r_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        res = {"bytes": n * pb, "write_gbs": n * pb / (w_ms * 1e-3) / GB, "read_gbs": n * pb / (r_ms * 1e-3) / GB,
+               "o_direct": disk.direct_io, "pages": n, "page_bytes": pb, "placement": "random page order",
+               "path": "pinned HOST pool <-> file pool, kvx_copy_pages(COPY_CE), 8 I/O threads"}
+        disk.close()
+        return res
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
 
 
 def bench_store_cycle(args, torch, np, kvx, dev):
@@ -1124,6 +1185,7 @@ def main():
             line["decode_attention"] = res["attention"]
             line["overlap"] = res["overlap"]
             line["store_cycle"] = res["store_cycle"]
+            line["disk_tier"] = res["disk_tier"]
             line["detail"] = res["extra"]
             if not args.skip_cpu:
                 v, cores, sample = cpu_migrate(np, cfg, 8.0, layers=8, repeat_min=3)

@@ -228,6 +228,7 @@ typedef struct {
   uint64_t seed;
   int32_t free_running; /* 0: lockstep (move at apply); 1: issue at schedule, complete at apply */
   int32_t pad_;
+  const char* disk_path; /* NULL/"": DISK tier in pinned host memory; else the file backing it */
 } kvs_payload_options;
 
 int kvs_cluster_create(kvs_cluster** out);

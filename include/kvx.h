@@ -51,6 +51,7 @@ extern "C" {
 #define KVX_ERR_CUDA 1        /* CUDA runtime/driver error or no device */
 #define KVX_ERR_ARG 2         /* invalid argument                       */
 #define KVX_ERR_UNSUPPORTED 3 /* shape/dtype/mode not implemented       */
+#define KVX_ERR_IO 5          /* file-pool read/write failed (sticky)   */
 
 #define KVX_DTYPE_F32 0
 #define KVX_DTYPE_BF16 1
@@ -105,6 +106,17 @@ uint64_t kvx_page_bytes(const kvx_page_layout* layout);
 int kvx_pool_create(int device, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
 /* HOST pool: pinned, device-mapped host memory (HOST-tier payload). */
 int kvx_pool_create_host(uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
+/* DISK tier: a pool whose pages live in a file (created / grown to
+ * num_pages * page_bytes; the file is kept on destroy). Pages move between a
+ * file pool and a HOST pool with kvx_copy_pages(KVX_COPY_CE, host id arrays):
+ * the reads/writes run in stream order (host callbacks on the stream), with
+ * O_DIRECT when the filesystem supports it. kvx_pool_base() is NULL; I/O
+ * errors are sticky and reported by every later call on the pool
+ * (KVX_ERR_IO). The reference keeps DISK as byte accounting only
+ * (kvstore.cpp:881-900 DiskWrite, :862-866 LoadDiskHost). */
+int kvx_pool_create_file(const char* path, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
+/* 1 if the pool's file was opened with O_DIRECT, 0 if buffered, -1 if not a file pool. */
+int kvx_pool_file_direct(const kvx_pool* pool);
 /* Wraps caller-owned device memory (not freed by kvx_pool_destroy). */
 int kvx_pool_wrap(int device, void* base, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
 int kvx_pool_destroy(kvx_pool* pool);

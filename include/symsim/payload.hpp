@@ -15,8 +15,11 @@
 //                   by migration — a page of this GPU's LANDING pool
 //                   (NetArrive: K3 kernel on the source GPU storing straight
 //                   into it over NVLink / peer memory)
-//   DISK copy    -> a page of the disk pool (pinned host memory standing in
-//                   for the SSD tier; copy engines)
+//   DISK copy    -> a page of the disk pool: a file when disk_path is set
+//                   (preads / pwrites in stream order, O_DIRECT where the
+//                   filesystem allows; HBM <-> file through a pinned bounce
+//                   ring per lane), else pinned host memory standing in for
+//                   the SSD (copy engines)
 //
 // Two modes (SURVEY.md §7 hard part 1):
 //   lockstep      every move happens inside apply_transfer, synchronously:
@@ -44,6 +47,7 @@
 
 #include <cstdint>
 #include <map>
+#include <string>
 #include <unordered_map>
 #include <vector>
 
@@ -58,7 +62,8 @@ struct PayloadOptions {
   std::uint64_t device_pages = 0;   // HBM pool
   std::uint64_t host_pages = 0;     // pinned host pool (HOST tier)
   std::uint64_t landing_pages = 0;  // HBM pool for migrated HOST-tier copies
-  std::uint64_t disk_pages = 0;     // DISK tier stand-in (pinned host)
+  std::uint64_t disk_pages = 0;     // DISK tier: pages in disk_path, or pinned host if empty
+  std::string disk_path;            // file backing the DISK tier (created / grown; kept)
   std::uint64_t seed = 0;           // content of Created blocks
   int fill_mode = KVX_FILL_VALUES;
   bool free_running = false;
@@ -147,10 +152,12 @@ class NodePayload final : public TierBackend {
     std::vector<std::pair<std::uint64_t, void*>> pending;  // (ticket, event), ascending
     std::uint32_t* d_ids[2] = {nullptr, nullptr};           // page-id scratch for this lane's kernels
     std::size_t d_ids_cap[2] = {0, 0};
+    kvx_pool* bounce = nullptr;  // pinned staging between HBM and a file-backed DISK pool
     void retire();
     void* event_for(std::uint64_t ticket);  // nullptr once complete
     void drain();                           // after a stream sync: everything complete
   };
+  static constexpr std::size_t kBouncePages = 256;  // per-lane HBM <-> disk-file staging
   struct Fence {  // the last batch that read or wrote a page
     std::int32_t node = -1;
     std::int32_t lane = 0;

@@ -423,6 +423,7 @@ symsim::PayloadOptions to_payload_opts(const kvs_payload_options* o) {
   p.disk_pages = o->disk_pages;
   p.seed = o->seed;
   p.free_running = o->free_running != 0;
+  if (o->disk_path) p.disk_path = o->disk_path;
   return p;
 }
 }  // namespace
@@ -525,6 +526,7 @@ int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int
       if (!slot) {
         symsim::PayloadOptions o = base;
         o.device = node_id % devices;
+        if (!o.disk_path.empty()) o.disk_path += ".node" + std::to_string(node_id);  // one DISK file per node
         slot = std::make_unique<symsim::NodePayload>(&c->cluster, node_id, o);
       }
       return slot.get();

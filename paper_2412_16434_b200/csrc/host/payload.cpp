@@ -155,6 +155,8 @@ NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOpti
     if (counts[p] == 0) continue;
     if (p == kDevicePool || p == kLandingPool)
       kvx_check(kvx_pool_create(opts_.device, counts[p], page_bytes_, &pools_[p]), "device pool");
+    else if (p == kDiskPool && !opts_.disk_path.empty())
+      kvx_check(kvx_pool_create_file(opts_.disk_path.c_str(), counts[p], page_bytes_, &pools_[p]), "disk file");
     else
       kvx_check(kvx_pool_create_host(counts[p], page_bytes_, &pools_[p]), "host pool");
     free_[p].resize(counts[p]);
@@ -179,6 +181,7 @@ NodePayload::~NodePayload() {
   for (Lane& L : lanes_) {
     L.drain();
     for (auto* d : L.d_ids) kvx_free(d);
+    if (L.bounce) kvx_pool_destroy(L.bounce);
     kvx_stream_destroy(L.stream);
   }
   kvx_free(d_tags_);
@@ -323,10 +326,26 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
       kvx_pool* from = src_node.pools_[sp];
       kvx_pool* to = pools_[dp];
       const bool on_device = (sp == kDevicePool || sp == kLandingPool) && (dp == kDevicePool || dp == kLandingPool);
+      const bool file_hop = !opts_.disk_path.empty() && (sp == kDiskPool || dp == kDiskPool) &&
+                            (sp == kDevicePool || sp == kLandingPool || dp == kDevicePool || dp == kLandingPool);
       if (on_device) {
         const std::uint32_t* ds = runner.device_ids(L, s_ids, 0);
         const std::uint32_t* dd = runner.device_ids(L, d_ids, 1);
         kvx_check(kvx_copy_pages(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO, L.stream), "page copy");
+      } else if (file_hop) {
+        // HBM <-> file: through this lane's pinned bounce pages, a chunk at a
+        // time; stream order keeps each chunk's file I/O ahead of the copy
+        // that refills the bounce pages.
+        if (!L.bounce) kvx_check(kvx_pool_create_host(kBouncePages, page_bytes_, &L.bounce), "bounce pool");
+        for (std::size_t at = 0; at < s_ids.size(); at += kBouncePages) {
+          const std::size_t k = std::min<std::size_t>(kBouncePages, s_ids.size() - at);
+          std::vector<std::uint32_t> b_ids(k);
+          for (std::size_t i = 0; i < k; ++i) b_ids[i] = static_cast<std::uint32_t>(i);
+          kvx_check(kvx_copy_pages(from, s_ids.data() + at, L.bounce, b_ids.data(), k, KVX_COPY_CE, L.stream),
+                    "disk hop (in)");
+          kvx_check(kvx_copy_pages(L.bounce, b_ids.data(), to, d_ids.data() + at, k, KVX_COPY_CE, L.stream),
+                    "disk hop (out)");
+        }
       } else {
         kvx_check(kvx_copy_pages(from, s_ids.data(), to, d_ids.data(), s_ids.size(), KVX_COPY_CE, L.stream),
                   "copy-engine copy");

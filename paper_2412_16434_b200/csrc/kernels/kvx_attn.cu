@@ -726,6 +726,7 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
                          int32_t batch, int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream) {
   if (!pool || !layout || !params || !d_block_tables || !d_ctx_lens || !d_q || !d_out)
     return kvx::fail_arg("kvx_decode_attention: null argument");
+  if (pool->fd >= 0) return kvx::fail_arg("kvx_decode_attention: not on a file pool");
   if (batch <= 0) return KVX_OK;
   const int H = layout->num_kv_heads, Hq = params->num_q_heads;
   if (H <= 0 || Hq <= 0 || Hq % H != 0) return kvx::fail_arg("kvx_decode_attention: num_q_heads must be a multiple of num_kv_heads");

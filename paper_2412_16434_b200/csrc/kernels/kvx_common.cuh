@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include <string>
+#include <vector>
 
 #include "kvx.h"
 
@@ -17,6 +20,9 @@ struct kvx_pool {
   bool owned = false;    // cudaFree / cudaFreeHost on destroy
   bool ipc = false;      // opened from a peer's IPC handle
   bool host = false;
+  int fd = -1;           // file pool (DISK tier): pages at offset page * page_bytes
+  bool direct = false;   // fd opened with O_DIRECT
+  std::atomic<int> io_errno{0};  // first failed read/write (sticky)
 };
 
 namespace kvx {
@@ -25,6 +31,15 @@ void set_error(const std::string& msg);
 int fail_cuda(cudaError_t e, const char* what);
 int fail_arg(const char* what);
 int sm_count(int device);
+// File pools (DISK tier): sticky I/O error check, and stream-ordered page I/O
+// between a file pool and host memory (kvx_pool.cu).
+int check_io(const kvx_pool* pool, const char* who);
+struct FileRun {
+  uint8_t* host;     // host bytes (pinned pool page run)
+  uint64_t offset;   // byte offset in the file
+  uint64_t bytes;
+};
+int enqueue_file_io(kvx_pool* file, std::vector<FileRun> runs, bool write, cudaStream_t stream, const char* who);
 
 // Makes `device` current for the scope (kernels must launch on the device
 // that owns the stream and the pool); no-op for host pools (device < 0).

@@ -251,6 +251,7 @@ extern "C" {
 
 int kvx_pack(const kvx_pool* src, const uint32_t* d_page_ids, uint64_t n, void* d_dst, int mode, void* stream) {
   if (!src || (n && (!d_page_ids || !d_dst))) return kvx::fail_arg("kvx_pack: null argument");
+  if (src->fd >= 0) return kvx::fail_arg("kvx_pack: file pools move through kvx_copy_pages(KVX_COPY_CE)");
   MoveArgs a{src->base, d_page_ids, static_cast<uint8_t*>(d_dst), nullptr, n, src->page_bytes, 0, 0, 0,
              src->num_pages, 0};
   return kvx::launch_move(a, mode, src->device, kvx::as_stream(stream), "kvx_pack", !src->host && !src->ipc);
@@ -258,6 +259,7 @@ int kvx_pack(const kvx_pool* src, const uint32_t* d_page_ids, uint64_t n, void* 
 
 int kvx_unpack(kvx_pool* dst, const uint32_t* d_page_ids, uint64_t n, const void* d_src, int mode, void* stream) {
   if (!dst || (n && (!d_page_ids || !d_src))) return kvx::fail_arg("kvx_unpack: null argument");
+  if (dst->fd >= 0) return kvx::fail_arg("kvx_unpack: file pools move through kvx_copy_pages(KVX_COPY_CE)");
   MoveArgs a{static_cast<const uint8_t*>(d_src), nullptr, dst->base, d_page_ids, n, dst->page_bytes, 0, 0, 0,
              0, dst->num_pages};
   return kvx::launch_move(a, mode, dst->device, kvx::as_stream(stream), "kvx_unpack", !dst->host && !dst->ipc);
@@ -274,6 +276,30 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
   if (src->page_bytes != dst->page_bytes) return kvx::fail_arg("kvx_copy_pages: page size mismatch");
   if (n == 0) return KVX_OK;
   const cudaStream_t st = kvx::as_stream(stream);
+  if (src->fd >= 0 || dst->fd >= 0) {
+    // DISK tier: file pool <-> pinned HOST pool, runs of consecutive ids as
+    // single preads / pwrites, executed in stream order.
+    const kvx_pool* file = src->fd >= 0 ? src : dst;
+    const kvx_pool* mem = src->fd >= 0 ? dst : src;
+    if (mode != KVX_COPY_CE || mem->fd >= 0 || !mem->host || !mem->base) {
+      kvx::set_error("kvx_copy_pages: a file pool exchanges pages only with a HOST pool (KVX_COPY_CE, host ids)");
+      return KVX_ERR_UNSUPPORTED;
+    }
+    const bool write = dst->fd >= 0;
+    std::vector<kvx::FileRun> runs;
+    for (uint64_t i = 0; i < n;) {
+      if (src_ids[i] >= src->num_pages || dst_ids[i] >= dst->num_pages)
+        return kvx::fail_arg("kvx_copy_pages: page id out of range");
+      uint64_t j = i + 1;
+      while (j < n && src_ids[j] == src_ids[j - 1] + 1 && dst_ids[j] == dst_ids[j - 1] + 1) ++j;
+      const uint32_t mem_id = write ? src_ids[i] : dst_ids[i];
+      const uint32_t file_id = write ? dst_ids[i] : src_ids[i];
+      runs.push_back(kvx::FileRun{mem->base + static_cast<uint64_t>(mem_id) * mem->page_bytes,
+                                  static_cast<uint64_t>(file_id) * file->page_bytes, (j - i) * file->page_bytes});
+      i = j;
+    }
+    return kvx::enqueue_file_io(const_cast<kvx_pool*>(file), std::move(runs), write, st, "kvx_copy_pages(file)");
+  }
   if (mode != KVX_COPY_CE) {
     MoveArgs a{src->base, src_ids, dst->base, dst_ids, n, src->page_bytes, 0, 0, 0, src->num_pages, dst->num_pages};
     const int dev = src->device >= 0 ? src->device : dst->device;
@@ -314,6 +340,7 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
 int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n, uint64_t seed,
                    const kvx_page_layout* layout, int fill_mode, void* stream) {
   if (!pool || (n && (!d_page_ids || !d_tags))) return kvx::fail_arg("kvx_fill_pages: null argument");
+  if (pool->fd >= 0) return kvx::fail_arg("kvx_fill_pages: not on a file pool");
   if (fill_mode != KVX_FILL_BITS && fill_mode != KVX_FILL_VALUES) return kvx::fail_arg("kvx_fill_pages: bad mode");
   const int dtype = layout ? layout->dtype : KVX_DTYPE_BF16;
   if (fill_mode == KVX_FILL_VALUES && (!layout || kvx_page_bytes(layout) != pool->page_bytes))
@@ -331,6 +358,7 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
                   const void* d_k, const void* d_v, uint64_t n, void* stream) {
   if (!pool || !layout || (n && (!d_page_ids || !d_slots || !d_k || !d_v)))
     return kvx::fail_arg("kvx_append_kv: null argument");
+  if (pool->fd >= 0) return kvx::fail_arg("kvx_append_kv: not on a file pool");
   if (kvx_page_bytes(layout) != pool->page_bytes) return kvx::fail_arg("kvx_append_kv: layout/page size mismatch");
   const int elt = layout->dtype == KVX_DTYPE_BF16 ? 2 : 4;
   const int row_bytes = layout->head_dim * elt;

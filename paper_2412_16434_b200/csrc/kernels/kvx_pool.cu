@@ -7,10 +7,17 @@
 // migration kernel on the source GPU stores straight into the receiver's
 // pages over NVLink (SURVEY.md §5 "Distributed communication backend").
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cerrno>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kvx_common.cuh"
@@ -45,6 +52,81 @@ int sm_count(int device) {
     cache[device] = n;
   }
   return cache[device];
+}
+
+int check_io(const kvx_pool* pool, const char* who) {
+  if (!pool || pool->fd < 0) return KVX_OK;
+  const int e = pool->io_errno.load();
+  if (e == 0) return KVX_OK;
+  g_error = std::string(who) + ": disk-tier file I/O failed earlier: " + std::strerror(e);
+  return KVX_ERR_IO;
+}
+
+namespace {
+
+constexpr uint64_t kIoThreads = 8;  // concurrent preads / pwrites per large job
+
+struct FileJob {
+  kvx_pool* pool;
+  std::vector<FileRun> runs;
+  bool write;
+};
+
+// Whole-run pread/pwrite with retry on short transfers; the first failure is
+// recorded on the pool (sticky) and later runs are skipped.
+void do_run(kvx_pool* p, const FileRun& r, bool write) {
+  uint64_t done = 0;
+  while (done < r.bytes && p->io_errno.load() == 0) {
+    const ssize_t n = write ? ::pwrite(p->fd, r.host + done, r.bytes - done, static_cast<off_t>(r.offset + done))
+                            : ::pread(p->fd, r.host + done, r.bytes - done, static_cast<off_t>(r.offset + done));
+    if (n < 0 && errno == EINTR) continue;
+    if (n <= 0) {
+      int expected = 0;
+      p->io_errno.compare_exchange_strong(expected, n < 0 ? errno : EIO);
+      return;
+    }
+    done += static_cast<uint64_t>(n);
+  }
+}
+
+// Big jobs fan out over a few threads (queue depth for the SSD); the
+// callback returns — and the stream proceeds — only when all runs are done.
+void run_file_job(void* arg) {
+  FileJob* job = static_cast<FileJob*>(arg);
+  kvx_pool* p = job->pool;
+  uint64_t total = 0;
+  for (const FileRun& r : job->runs) total += r.bytes;
+  const int threads = static_cast<int>(std::min<uint64_t>(kIoThreads, std::max<uint64_t>(1, total >> 22)));
+  if (threads <= 1 || job->runs.size() < 2) {
+    for (const FileRun& r : job->runs) do_run(p, r, job->write);
+  } else {
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+      for (size_t i = next++; i < job->runs.size(); i = next++) do_run(p, job->runs[i], job->write);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+  }
+  delete job;
+}
+
+}  // namespace
+
+// The I/O runs as a host callback in stream order: after everything queued
+// before it on `stream` (e.g. the copy that filled the host pages it writes),
+// before everything queued after it (e.g. the copy that reads what it loaded).
+int enqueue_file_io(kvx_pool* file, std::vector<FileRun> runs, bool write, cudaStream_t stream, const char* who) {
+  if (int rc = check_io(file, who)) return rc;
+  if (runs.empty()) return KVX_OK;
+  auto* job = new FileJob{file, std::move(runs), write};
+  const cudaError_t e = cudaLaunchHostFunc(stream, run_file_job, job);
+  if (e != cudaSuccess) {
+    delete job;
+    return fail_cuda(e, who);
+  }
+  return KVX_OK;
 }
 
 }  // namespace kvx
@@ -98,6 +180,39 @@ int kvx_pool_create_host(uint64_t num_pages, uint64_t page_bytes, kvx_pool** out
   return KVX_OK;
 }
 
+int kvx_pool_create_file(const char* path, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out) {
+  if (!out || !path || num_pages == 0 || page_bytes == 0 || page_bytes % 4096 != 0)
+    return kvx::fail_arg("kvx_pool_create_file: need a path, num_pages > 0 and page_bytes a multiple of 4096");
+  bool direct = true;
+  int fd = ::open(path, O_RDWR | O_CREAT | O_DIRECT, 0600);
+  if (fd < 0 && errno == EINVAL) {  // filesystem without O_DIRECT (e.g. tmpfs): buffered I/O
+    direct = false;
+    fd = ::open(path, O_RDWR | O_CREAT, 0600);
+  }
+  if (fd < 0) {
+    kvx::set_error(std::string("kvx_pool_create_file: open ") + path + ": " + std::strerror(errno));
+    return KVX_ERR_IO;
+  }
+  const uint64_t bytes = num_pages * page_bytes;
+  struct stat st {};
+  if (::fstat(fd, &st) != 0 || (static_cast<uint64_t>(st.st_size) < bytes && ::ftruncate(fd, static_cast<off_t>(bytes)) != 0)) {
+    kvx::set_error(std::string("kvx_pool_create_file: size ") + path + ": " + std::strerror(errno));
+    ::close(fd);
+    return KVX_ERR_IO;
+  }
+  auto* pool = new kvx_pool;
+  pool->num_pages = num_pages;
+  pool->page_bytes = page_bytes;
+  pool->device = -1;
+  pool->host = true;
+  pool->fd = fd;
+  pool->direct = direct;
+  *out = pool;
+  return KVX_OK;
+}
+
+int kvx_pool_file_direct(const kvx_pool* pool) { return pool && pool->fd >= 0 ? (pool->direct ? 1 : 0) : -1; }
+
 int kvx_pool_wrap(int device, void* base, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out) {
   if (!out || !base || num_pages == 0 || page_bytes == 0 || page_bytes % 16 != 0 ||
       reinterpret_cast<uintptr_t>(base) % 16 != 0)
@@ -115,6 +230,7 @@ int kvx_pool_wrap(int device, void* base, uint64_t num_pages, uint64_t page_byte
 int kvx_pool_destroy(kvx_pool* pool) {
   if (!pool) return KVX_OK;
   cudaError_t e = cudaSuccess;
+  if (pool->fd >= 0) ::close(pool->fd);
   if (pool->ipc) e = cudaIpcCloseMemHandle(pool->base);
   else if (pool->owned && pool->host) e = cudaFreeHost(pool->base);
   else if (pool->owned) e = cudaFree(pool->base);
@@ -228,6 +344,26 @@ int kvx_memcpy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
 
 int kvx_read_page(const kvx_pool* pool, uint64_t page, void* host_out) {
   if (!pool || !host_out || page >= pool->num_pages) return kvx::fail_arg("kvx_read_page: bad page");
+  if (pool->fd >= 0) {  // file pool: aligned bounce for O_DIRECT, then copy out
+    if (int rc = kvx::check_io(pool, "kvx_read_page")) return rc;
+    void* bounce = nullptr;
+    if (posix_memalign(&bounce, 4096, pool->page_bytes) != 0) return kvx::fail_arg("kvx_read_page: out of memory");
+    uint64_t done = 0;
+    while (done < pool->page_bytes) {
+      const ssize_t n = ::pread(pool->fd, static_cast<uint8_t*>(bounce) + done, pool->page_bytes - done,
+                                static_cast<off_t>(page * pool->page_bytes + done));
+      if (n < 0 && errno == EINTR) continue;
+      if (n <= 0) {
+        free(bounce);
+        kvx::set_error(std::string("kvx_read_page: pread: ") + std::strerror(n < 0 ? errno : EIO));
+        return KVX_ERR_IO;
+      }
+      done += static_cast<uint64_t>(n);
+    }
+    std::memcpy(host_out, bounce, pool->page_bytes);
+    free(bounce);
+    return KVX_OK;
+  }
   KVX_CUDA_TRY(cudaMemcpy(host_out, pool->base + page * pool->page_bytes, pool->page_bytes, cudaMemcpyDefault),
                "kvx_read_page");
   return KVX_OK;

@@ -113,7 +113,7 @@ class _PayloadOpts(C.Structure):
                 ("block_tokens", C.c_int32), ("dtype", C.c_int32), ("fill_mode", C.c_int32),
                 ("device_pages", C.c_uint64), ("host_pages", C.c_uint64), ("landing_pages", C.c_uint64),
                 ("disk_pages", C.c_uint64), ("seed", C.c_uint64), ("free_running", C.c_int32),
-                ("pad_", C.c_int32)]
+                ("pad_", C.c_int32), ("disk_path", C.c_char_p)]
 
 
 @dataclass
@@ -570,11 +570,13 @@ class PayloadOptions:
     disk_pages: int = 0
     seed: int = 0
     free_running: bool = False
+    disk_path: str = ""  # file backing the DISK tier ("" = pinned host stand-in)
 
     def _c(self) -> "_PayloadOpts":
         return _PayloadOpts(self.device, self.num_kv_heads, self.head_dim, self.block_tokens, self.dtype,
                             self.fill_mode, self.device_pages, self.host_pages, self.landing_pages,
-                            self.disk_pages, self.seed, int(self.free_running), 0)
+                            self.disk_pages, self.seed, int(self.free_running), 0,
+                            self.disk_path.encode() if self.disk_path else None)
 
     def page_bytes(self) -> int:
         return 2 * self.num_kv_heads * self.block_tokens * self.head_dim * (2 if self.dtype == 1 else 4)

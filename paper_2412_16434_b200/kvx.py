@@ -59,6 +59,9 @@ def lib() -> C.CDLL:
         "kvx_pool_create": ([C.c_int, U64, U64, P(V)], C.c_int),
         "kvx_pool_create_host": ([U64, U64, P(V)], C.c_int),
         "kvx_pool_wrap": ([C.c_int, V, U64, U64, P(V)], C.c_int),
+        "kvx_pool_create_file": ([C.c_char_p, U64, U64, P(V)], C.c_int),
+        "kvx_pool_file_direct": ([V], C.c_int),
+        "kvx_read_page": ([V, U64, V], C.c_int),
         "kvx_pool_destroy": ([V], C.c_int),
         "kvx_pool_base": ([V], V),
         "kvx_pool_num_pages": ([V], U64),
@@ -140,6 +143,27 @@ class Pool:
         p = cls(num_pages, page_bytes, device, _handle=h.value)
         p._keep = tensor
         return p
+
+    @classmethod
+    def file(cls, path: str, num_pages: int, page_bytes: int) -> "Pool":
+        """DISK-tier pool backed by a file (kvx_pool_create_file); pages move to
+        and from HOST pools with copy_pages(..., COPY_CE) on host id arrays."""
+        h = C.c_void_p()
+        check(lib().kvx_pool_create_file(str(path).encode(), num_pages, page_bytes, C.byref(h)))
+        p = cls(num_pages, page_bytes, -1, _handle=h.value)
+        p.path = str(path)
+        return p
+
+    @property
+    def direct_io(self) -> bool:
+        return lib().kvx_pool_file_direct(self.handle) == 1
+
+    def read_page(self, page: int):
+        """Synchronous copy of one page to a new numpy array (any pool kind)."""
+        import numpy as np
+        out = np.empty(self.page_bytes, np.uint8)
+        check(lib().kvx_read_page(self.handle, page, out.ctypes.data))
+        return out
 
     @classmethod
     def ipc_open(cls, handle64: bytes, num_pages: int, page_bytes: int, device: int) -> "Pool":

@@ -92,12 +92,15 @@ int main(int argc, char** argv) {
   std::int64_t device_pages = 0;
   std::string policy = "symphony";
   bool free_running = false;
+  std::string disk_dir;  // --disk-dir: DISK tier in files (one per node) instead of pinned host memory
   for (int i = 1; i < argc; ++i) {
+    if (!std::strcmp(argv[i], "--disk-dir") && i + 1 < argc) disk_dir = argv[++i];
     if (!std::strcmp(argv[i], "--device-pages") && i + 1 < argc) device_pages = std::atoll(argv[++i]);
     if (!std::strcmp(argv[i], "--policy") && i + 1 < argc) policy = argv[++i];
     if (!std::strcmp(argv[i], "--free-running")) free_running = true;
   }
   (void)free_running;
+  (void)disk_dir;
   RunConfig cfg;
   cfg.policy = policy_from(policy);
   cfg.num_nodes = 2;
@@ -123,7 +126,9 @@ int main(int argc, char** argv) {
   po.seed = kSeed;
   po.free_running = free_running;
   set_default_tier_backend_factory([&](int node_id) -> TierBackend* {
-    nodes.push_back(std::make_unique<NodePayload>(&cluster, node_id, po));
+    PayloadOptions o = po;
+    if (!disk_dir.empty()) o.disk_path = disk_dir + "/node" + std::to_string(node_id) + ".pages";
+    nodes.push_back(std::make_unique<NodePayload>(&cluster, node_id, o));
     return nodes.back().get();
   });
 #endif

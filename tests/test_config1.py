@@ -66,3 +66,24 @@ def test_config1_trace_with_real_pages(variant, mode):
     summary = [ln for ln in proc.stdout.splitlines() if ln.startswith("payload verified_copies")][0]
     copies, bad = int(summary.split()[2]), int(summary.split()[4])
     assert copies > 0 and bad == 0, summary
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", list(MODES))
+def test_config1_with_disk_tier_in_files(mode, tmp_path):
+    """Same gates with the DISK tier backed by one file per node: every
+    write-behind DiskWrite of the purge-heavy variant lands in the node's file
+    (read back with pread for the bit-exact check)."""
+    if not PROD_BIN.exists():
+        pytest.skip("oracle/_ref/payload_sim not built (needs the reference sources; build here and ship)")
+    proc = subprocess.run([str(PROD_BIN), *VARIANTS["dev30"], *MODES[mode], "--disk-dir", str(tmp_path)],
+                          capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
+    assert _state_lines(proc.stdout) == _state_lines((GOLDEN / "config1_dev30.txt").read_text())
+    summary = [ln for ln in proc.stdout.splitlines() if ln.startswith("payload verified_copies")][0]
+    copies, bad = int(summary.split()[2]), int(summary.split()[4])
+    assert copies > 0 and bad == 0, summary
+    assert sorted(p.name for p in tmp_path.iterdir()) == ["node0.pages", "node1.pages"]
+    disk_pages = [int(ln.split(" disk ")[1].split()[0]) for ln in proc.stdout.splitlines()
+                  if ln.startswith("payload node") and " disk " in ln]
+    assert sum(disk_pages) > 0, "the trace must leave DISK copies in the files"

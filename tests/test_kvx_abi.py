@@ -37,3 +37,18 @@ def test_page_bytes_match_the_store_accounting(product_libs):
         per_token = layers * 2 * heads * dim * elt
         gpu = K.GpuProfile(kv_bytes_per_token=per_token, num_layers=layers)
         assert K.kv_bytes_per_layer(16, gpu) == kvx.page_bytes(kvx.PageLayout(heads, dim, 16, dtype))
+
+
+def test_file_pool_without_a_device(product_libs, tmp_path):
+    """The DISK-tier file pool is host-only: creating it and reading a page
+    needs no GPU (a fresh file reads as zeros); it refuses kernels."""
+    from paper_2412_16434_b200 import kvx
+    pb = 32768
+    pool = kvx.Pool.file(tmp_path / "disk.pages", 8, pb)
+    assert (tmp_path / "disk.pages").stat().st_size == 8 * pb
+    assert not pool.read_page(7).any()
+    with pytest.raises(kvx.KvxError):
+        pool.read_page(8)
+    with pytest.raises(kvx.KvxError):
+        kvx.Pool.file(tmp_path / "bad.pages", 8, 1000)  # pages must be 4 KiB multiples (O_DIRECT)
+    pool.close()

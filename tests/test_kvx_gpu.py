@@ -144,6 +144,38 @@ def test_capped_copy_bit_exact(dev, mode, cap):
     assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
 
 
+@pytest.mark.parametrize("layout", [TINY, LLAMA8B], ids=["tiny-f32", "8b-bf16"])
+def test_file_pool_roundtrip_bit_exact(dev, layout, tmp_path):
+    """DISK tier as a file: HOST pool -> file -> second HOST pool, in stream
+    order on one stream (pwrite then pread as host callbacks), runs of
+    consecutive ids coalesced; every page bit-exact, and the file holds the
+    pages at page_id * page_bytes. Device pools cannot exchange with a file."""
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(21)
+    n, pages = 50, 64
+    host = kvx.Pool(pages, pb, host=True)
+    host_np = host.as_tensor().numpy()
+    host_np[:] = rng.integers(0, 256, host_np.shape, dtype=np.uint8)
+    disk = kvx.Pool.file(tmp_path / "disk.pages", pages, pb)
+    src_ids = np.concatenate([np.arange(10, 20), rng.permutation(np.arange(20, pages))[:n - 10]]).astype(np.uint32)
+    dst_ids = np.concatenate([np.arange(30, 40), rng.permutation(np.setdiff1d(np.arange(pages), np.arange(30, 40)))[:n - 10]]).astype(np.uint32)
+    back = kvx.Pool(pages, pb, host=True)
+    back.as_tensor().zero_()
+    s = torch.cuda.Stream()
+    kvx.copy_pages(host, src_ids, disk, dst_ids, n, kvx.COPY_CE, stream=s)
+    kvx.copy_pages(disk, dst_ids, back, src_ids, n, kvx.COPY_CE, stream=s)
+    s.synchronize()
+    got = back.as_tensor().numpy()
+    assert np.array_equal(got[src_ids], host_np[src_ids])
+    for i in (0, 17, n - 1):
+        assert np.array_equal(disk.read_page(int(dst_ids[i])), host_np[src_ids[i]])
+    raw = np.fromfile(tmp_path / "disk.pages", np.uint8).reshape(pages, pb)
+    assert np.array_equal(raw[dst_ids], host_np[src_ids])
+    dev_pool = kvx.Pool(pages, pb, device=0)
+    with pytest.raises(kvx.KvxError):
+        kvx.copy_pages(dev_pool, src_ids, disk, dst_ids, n, kvx.COPY_CE)
+
+
 def test_host_pool_zero_copy_roundtrip(dev):
     """DEVICE -> mapped pinned HOST pool -> DEVICE with the SM mover (PCIe)."""
     layout = TINY

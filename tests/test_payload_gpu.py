@@ -33,10 +33,27 @@ def tiny_profile():
     return K.GpuProfile(kv_bytes_per_token=LAYERS * 2 * 4 * 64 * 4, num_layers=LAYERS, hbm_capacity=10**12)
 
 
+_DISK = {"dir": None, "n": 0}
+
+
+@pytest.fixture(params=["disk-pinned", "disk-file"], autouse=True)
+def disk_backing(request, tmp_path):
+    """Every test runs twice: DISK tier in pinned host memory, and DISK tier
+    in files (kvx_pool_create_file: preads / pwrites in stream order, HBM
+    <-> file through the per-lane bounce pages)."""
+    _DISK["dir"] = tmp_path if request.param == "disk-file" else None
+    yield
+    _DISK["dir"] = None
+
+
 def payload_opts(device_pages=64, host_pages=64, landing_pages=64, disk_pages=128, free_running=False):
+    path = ""
+    if _DISK["dir"] is not None:
+        _DISK["n"] += 1
+        path = str(_DISK["dir"] / f"disk{_DISK['n']}.pages")
     return K.PayloadOptions(device=0, num_kv_heads=4, head_dim=64, block_tokens=16, dtype=0, fill_mode=1,
                             device_pages=device_pages, host_pages=host_pages, landing_pages=landing_pages,
-                            disk_pages=disk_pages, seed=SEED, free_running=free_running)
+                            disk_pages=disk_pages, seed=SEED, free_running=free_running, disk_path=path)
 
 
 MODES = pytest.mark.parametrize("free_running", [False, True], ids=["lockstep", "free-running"])
