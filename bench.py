@@ -319,6 +319,33 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
             res[f"batch{batch}"]["cluster_sweep_gbs"] = {
                 s: round(kv_bytes / (timed(s, kvx.MERGE_CLUSTER) * 1e-3) / GB, 1)
                 for s in (2, 3, 4, 6, 8, 9, 12, 16) if batch * cfg["kv_heads"] * s <= 148}
+    # One decode step of one layer as the engine runs it (append this token's
+    # K/V, then attend): kvx_append_kv + kvx_decode_attention (two launches)
+    # vs kvx_decode_attention_append (append fused into the attention launch).
+    for batch in (1, 8):
+        sets = max(1, min(pages // (batch * blocks), -(-256 // (batch * 32))))
+        tables = [perm[s * batch * blocks:(s + 1) * batch * blocks].view(batch, blocks).contiguous()
+                  for s in range(sets)]
+        ctx = torch.full((batch,), cfg["ctx"], dtype=torch.int32, device=dev)
+        q = (torch.randn(batch, 32, 128, device=dev) * 0.5).to(torch.bfloat16)
+        nk = (torch.randn(batch, cfg["kv_heads"], 128, device=dev) * 0.5).to(torch.bfloat16)
+        nv = (torch.randn(batch, cfg["kv_heads"], 128, device=dev) * 0.5).to(torch.bfloat16)
+        out = torch.empty(batch, 32, 128, dtype=torch.float32, device=dev)
+        slots = torch.full((batch,), (cfg["ctx"] - 1) % cfg["block_tokens"], dtype=torch.int32, device=dev)
+        last = [t[:, (cfg["ctx"] - 1) // cfg["block_tokens"]].contiguous() for t in tables]
+        att = kvx.Attention(layout, 32, blocks)
+        ws = torch.zeros(max(att.workspace_bytes(batch, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
+        reps, replays = max(sets, 16), max(3, min(args.steps, 20))
+
+        def two(i):
+            kvx.append_kv(pool, layout, last[i % sets], slots, nk, nv, batch)
+            att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws)
+
+        t_two = graph_time_ms(torch, two, reps, replays)
+        t_fused = graph_time_ms(torch, lambda i: att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws,
+                                                     new_k=nk, new_v=nv), reps, replays)
+        res[f"decode_step_batch{batch}"] = {"append_then_attend_ms": t_two, "fused_ms": t_fused,
+                                            "speedup": t_two / t_fused, "timing": "cuda-graph replay, per layer"}
     # Config 3's decode shape: Llama-3.1-70B (64 q heads over 8 kv heads, GQA 8) at ctx 32768.
     c70 = CFG_70B
     blocks70 = c70["ctx"] // c70["block_tokens"]

@@ -197,6 +197,18 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
                          const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q,
                          float* d_out, int32_t batch, int32_t max_ctx, void* d_workspace,
                          uint64_t workspace_bytes, void* stream);
+/* One decode step of one layer, fused: first writes this step's token —
+ * d_new_k[b][H][D] / d_new_v[b][H][D] (layout dtype), position
+ * ctx_lens[b] - 1, into its slot of the page its block table names (the
+ * bytes behind Engine::apply_step's append_blocks(1), engine.cpp:132-166,
+ * kvstore.cpp:202-271) — then attends over ctx_lens[b] tokens as
+ * kvx_decode_attention. On the bf16 / d128 / 16-token fast path the append
+ * is done inside the attention launch by the CTA that streams the last page
+ * (one launch per layer instead of two). */
+int kvx_decode_attention_append(kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
+                                const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q,
+                                const void* d_new_k, const void* d_new_v, float* d_out, int32_t batch,
+                                int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -142,6 +142,8 @@ struct AttnArgs {
   const uint32_t* tables;
   const int32_t* ctx_lens;
   const uint16_t* q;  // [B][Hq][128] bf16
+  const uint16_t* new_k;  // [B][H][128] bf16: this step's token (position ctx-1), or null
+  const uint16_t* new_v;
   float* out;         // [B][Hq][128]
   float* part_o;      // [B][Hq][S][128]
   float* part_ml;     // [B][Hq][S][2]
@@ -224,6 +226,22 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     s_pages[i] = page;
   }
   __syncthreads();
+  if (a.new_k != nullptr && p_begin < p_end && p_end == n_pages) {
+    // Fused append (the decode step's append_blocks(1), kvstore.cpp:202-271 /
+    // engine.cpp:132-166): this CTA streams the request's last page, so it
+    // writes this step's K and V row of kv head h into their slot first;
+    // no other CTA reads that page, and the barrier below makes the rows
+    // visible to this CTA's page loads.
+    if (threadIdx.x < 32) {
+      const int t = ctx - 1, slot = t - (n_pages - 1) * kT;
+      uint8_t* page = const_cast<uint8_t*>(a.pool) + static_cast<uint64_t>(s_pages[n_pages - 1 - p_begin]) * a.page_bytes;
+      const int kv = threadIdx.x >> 4, c = threadIdx.x & 15;  // lanes 0-15: K row, 16-31: V row (16 x 16 B)
+      const uint16_t* src = (kv ? a.new_v : a.new_k) + (static_cast<uint64_t>(b) * a.heads + h) * kD;
+      uint8_t* dst = page + static_cast<uint64_t>((kv * a.heads + h) * kT + slot) * (kD * 2);
+      reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
+    }
+    __syncthreads();
+  }
   KVX_TRACE(2);
 
   float o[kD / 8][4];
@@ -596,6 +614,29 @@ __global__ void attn_generic(const uint8_t* pool, uint64_t page_bytes, const uin
   for (int i = 0; i < per_lane; ++i) orow[lane + 32 * i] = l > 0.f ? acc[i] / l : 0.f;
 }
 
+// The decode step's append for the generic path: request b's token at
+// position ctx_lens[b] - 1 goes to its slot in the page its block table
+// names (one CTA per request, every kv head's K and V row).
+__global__ void __launch_bounds__(128) append_from_table(uint8_t* pool, uint64_t page_bytes, uint64_t pool_pages,
+                                                         const uint32_t* tables, const int32_t* ctx_lens,
+                                                         const uint8_t* new_k, const uint8_t* new_v, int heads,
+                                                         int block_tokens, int row_bytes, int max_blocks) {
+  const int b = blockIdx.x;
+  const int t = ctx_lens[b] - 1;
+  if (t < 0) return;
+  const uint32_t page = tables[static_cast<uint64_t>(b) * max_blocks + t / block_tokens];
+  if (page >= pool_pages) __trap();
+  const int slot = t % block_tokens;
+  uint8_t* base = pool + static_cast<uint64_t>(page) * page_bytes;
+  const int vecs = row_bytes / 16;
+  for (int e = threadIdx.x; e < 2 * heads * vecs; e += blockDim.x) {
+    const int kv = e / (heads * vecs), rem = e - kv * heads * vecs, h = rem / vecs, c = rem - h * vecs;
+    const uint8_t* src = (kv ? new_v : new_k) + (static_cast<uint64_t>(b) * heads + h) * row_bytes;
+    uint8_t* dst = base + (static_cast<uint64_t>(kv * heads + h) * block_tokens + slot) * row_bytes;
+    reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
+  }
+}
+
 bool fast_path(const kvx_page_layout* l) {
   return l->dtype == KVX_DTYPE_BF16 && l->head_dim == kD && l->block_tokens == kT;
 }
@@ -721,9 +762,15 @@ uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx
   return kvx::workspace_for(batch, params->num_q_heads, layout->num_kv_heads, splits);
 }
 
-int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
-                         const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q, float* d_out,
-                         int32_t batch, int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace kvx {
+namespace {
+
+int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
+                     const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q, const void* d_new_k,
+                     const void* d_new_v, float* d_out, int32_t batch, int32_t max_ctx, void* d_workspace,
+                     uint64_t workspace_bytes, void* stream) {
   if (!pool || !layout || !params || !d_block_tables || !d_ctx_lens || !d_q || !d_out)
     return kvx::fail_arg("kvx_decode_attention: null argument");
   if (pool->fd >= 0) return kvx::fail_arg("kvx_decode_attention: not on a file pool");
@@ -752,6 +799,8 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     a.tables = d_block_tables;
     a.ctx_lens = d_ctx_lens;
     a.q = static_cast<const uint16_t*>(d_q);
+    a.new_k = static_cast<const uint16_t*>(d_new_k);
+    a.new_v = static_cast<const uint16_t*>(d_new_v);
     a.out = d_out;
     a.heads = H;
     a.group = group;
@@ -805,6 +854,14 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
     kvx::set_error("kvx_decode_attention: head_dim must be a multiple of 32 and <= 256");
     return KVX_ERR_UNSUPPORTED;
   }
+  if (d_new_k) {
+    const int row_bytes = layout->head_dim * (layout->dtype == KVX_DTYPE_BF16 ? 2 : 4);
+    kvx::append_from_table<<<batch, 128, 0, st>>>(pool->base, pool->page_bytes, pool->num_pages, d_block_tables,
+                                                  d_ctx_lens, static_cast<const uint8_t*>(d_new_k),
+                                                  static_cast<const uint8_t*>(d_new_v), H, layout->block_tokens,
+                                                  row_bytes, params->max_blocks);
+    KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention_append(append)");
+  }
   dim3 grid(Hq, batch);
   if (layout->dtype == KVX_DTYPE_F32)
     kvx::attn_generic<float><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, d_block_tables, d_ctx_lens,
@@ -817,6 +874,31 @@ int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, co
                                                      scale);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention(generic)");
   return KVX_OK;
+}
+
+}  // namespace
+}  // namespace kvx
+
+extern "C" {
+
+int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
+                         const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q, float* d_out,
+                         int32_t batch, int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  return kvx::decode_attention(pool, layout, params, d_block_tables, d_ctx_lens, d_q, nullptr, nullptr, d_out, batch,
+                               max_ctx, d_workspace, workspace_bytes, stream);
+}
+
+int kvx_decode_attention_append(kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,
+                                const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q,
+                                const void* d_new_k, const void* d_new_v, float* d_out, int32_t batch,
+                                int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream) {
+  if (!d_new_k || !d_new_v) return kvx::fail_arg("kvx_decode_attention_append: null new K/V");
+  if (pool && layout) {
+    const int row_bytes = layout->head_dim * (layout->dtype == KVX_DTYPE_BF16 ? 2 : 4);
+    if (row_bytes % 16) return kvx::fail_arg("kvx_decode_attention_append: head_dim * sizeof(dtype) must be a multiple of 16");
+  }
+  return kvx::decode_attention(pool, layout, params, d_block_tables, d_ctx_lens, d_q, d_new_k, d_new_v, d_out, batch,
+                               max_ctx, d_workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -79,6 +79,8 @@ def lib() -> C.CDLL:
         "kvx_decode_attention_workspace": ([P(PageLayout), P(AttnParams), C.c_int32, C.c_int32], U64),
         "kvx_decode_attention": ([V, P(PageLayout), P(AttnParams), V, V, V, V, C.c_int32, C.c_int32, V, U64, V],
                                  C.c_int),
+        "kvx_decode_attention_append": ([V, P(PageLayout), P(AttnParams), V, V, V, V, V, V, C.c_int32, C.c_int32, V,
+                                         U64, V], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(h, name)
@@ -276,10 +278,18 @@ class Attention:
         return lib().kvx_decode_attention_workspace(C.byref(self.layout), C.byref(p), batch, max_ctx)
 
     def __call__(self, pool: Pool, block_tables, ctx_lens, q, out, batch: int, max_ctx: int, workspace=None,
-                 stream=None) -> None:
+                 stream=None, new_k=None, new_v=None) -> None:
+        """new_k / new_v ([batch][kv heads][head_dim]): fused decode step —
+        append this token at position ctx_lens[b] - 1, then attend
+        (kvx_decode_attention_append)."""
         p = self.params()
         ws = _ptr(workspace)
         ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        if new_k is not None or new_v is not None:
+            check(lib().kvx_decode_attention_append(pool.handle, C.byref(self.layout), C.byref(p), _ptr(block_tables),
+                                                    _ptr(ctx_lens), _ptr(q), _ptr(new_k), _ptr(new_v), _ptr(out),
+                                                    batch, max_ctx, ws, ws_bytes, _stream(stream)))
+            return
         check(lib().kvx_decode_attention(pool.handle, C.byref(self.layout), C.byref(p), _ptr(block_tables),
                                          _ptr(ctx_lens), _ptr(q), _ptr(out), batch, max_ctx, ws, ws_bytes,
                                          _stream(stream)))

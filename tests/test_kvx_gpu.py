@@ -342,6 +342,43 @@ def test_attention_split_merge_reuses_workspace(dev, merge):
         assert torch.equal(o, outs[0])
 
 
+@pytest.mark.parametrize("layout,hq,splits", [(LLAMA8B, 32, 0), (LLAMA8B, 32, 5), (LLAMA8B, 64, 3), (TINY, 8, 0)],
+                         ids=["8b-auto", "8b-5splits", "70b-3splits", "tiny-f32"])
+def test_fused_append_decode_step(dev, layout, hq, splits):
+    """kvx_decode_attention_append (append this step's K/V at ctx-1, then
+    attend) == kvx_append_kv + kvx_decode_attention: identical pool bytes
+    and bit-identical outputs; lengths at page boundaries (ctx % 16 in
+    {1, 0, 15}) and a one-token request."""
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(hq + splits)
+    ctx_lens = np.array([1, 16, 17, 31, 500, 1024], np.int32)
+    B = len(ctx_lens)
+    mb = 64
+    pages = B * mb + 3
+    all_ids = np.arange(pages, dtype=np.uint32)
+    tables = rng.permutation(pages)[:B * mb].astype(np.uint32).reshape(B, mb)
+    pool_a, _ = filled_pool(layout, pages, all_ids, O.tags_array(6, 1, all_ids), 31, kvx.FILL_VALUES, dev)
+    pool_b, _ = filled_pool(layout, pages, all_ids, O.tags_array(6, 1, all_ids), 31, kvx.FILL_VALUES, dev)
+    elt = torch.bfloat16 if layout.dtype == kvx.BF16 else torch.float32
+    H, D = layout.num_kv_heads, layout.head_dim
+    nk = torch.randn(B, H, D, device=dev).to(elt)
+    nv = torch.randn(B, H, D, device=dev).to(elt)
+    q = torch.randn(B, hq, D, device=dev).to(elt)
+    d_tables, d_ctx = to_dev(tables.view(np.int32), dev), to_dev(ctx_lens, dev)
+    att = kvx.Attention(layout, hq, mb, num_splits=splits)
+    ws = torch.zeros(max(att.workspace_bytes(B, mb * 16), 1), dtype=torch.uint8, device=dev)
+    out_a = torch.empty(B, hq, D, dtype=torch.float32, device=dev)
+    out_b = torch.empty_like(out_a)
+    att(pool_a, d_tables, d_ctx, q, out_a, B, mb * 16, ws, new_k=nk, new_v=nv)
+    t = ctx_lens - 1
+    ids = to_dev(tables[np.arange(B), t // 16].astype(np.int32), dev)
+    kvx.append_kv(pool_b, layout, ids, to_dev((t % 16).astype(np.int32), dev), nk, nv, B)
+    att(pool_b, d_tables, d_ctx, q, out_b, B, mb * 16, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(pool_a.as_tensor(), pool_b.as_tensor())
+    assert torch.equal(out_a, out_b)
+
+
 def test_full_70b_session_migration_property(dev):
     """Config 3 at full size on one GPU (10.7 GB, Llama-3.1-70B KV @ 32K):
     every layer's 2,048 pages move page->page (K3, the migration kernel) into

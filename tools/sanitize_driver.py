@@ -44,5 +44,7 @@ for layout in (kvx.PageLayout(8, 128, 16, kvx.BF16), kvx.PageLayout(4, 64, 16, k
         att = kvx.Attention(layout, hq, blocks, num_splits=splits, split_merge=merge)
         ws = torch.zeros(max(att.workspace_bytes(batch, ctx), 1), dtype=torch.uint8, device=dev)
         att(pool, tables, lens, q, out, batch, ctx, ws)
+        nk = torch.randn(batch, layout.num_kv_heads, layout.head_dim, device=dev).to(elt)
+        att(pool, tables, lens, q, out, batch, ctx, ws, new_k=nk, new_v=nk)  # fused append + attend
 torch.cuda.synchronize()
 print("sanitize driver done")
