@@ -958,8 +958,8 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
     dist.all_gather_object(oks, ok)
     assert all(oks), f"migrated pages differ on ranks {[i for i, o in enumerate(oks) if not o]}"
 
-    e2e = bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, migrate, src_ids, peer_dst,
-                          my_dst, pb, n, red_dev) if args.migrate_mode == "p2p" else None
+    e2e = bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, src_ids, peer_dst, my_dst, pb, n,
+                          blocks, red_dev) if args.migrate_mode == "p2p" else None
 
     session_bytes = n * pb
     value = world * session_bytes / (t_mig * 1e-3) / GB
@@ -986,45 +986,97 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
                 gpu_launches=launches)
 
 
-def bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, migrate, src_ids, peer_dst, my_dst, pb,
-                    n, red_dev):
-    """The ring migration through the public API as a caller drives it: every
-    step uploads the session's block tables (source and receiver page ids)
-    from pinned host memory, migrates, and reads back one landed page (the
-    last one written) from the receiver's pool."""
-    h_src = torch.from_numpy(src_ids.view(np.int32)).pin_memory()
-    h_dst = torch.from_numpy(peer_dst.view(np.int32)).pin_memory()
-    d_src = torch.empty_like(h_src, device=dev)
-    d_dst = torch.empty_like(h_dst, device=dev)
-    h_probe = torch.empty(pb, dtype=torch.uint8).pin_memory()
-    st = torch.cuda.current_stream(dev)
-    last = int(peer_dst[-1])
+def bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, src_ids, peer_dst, my_dst, pb, n,
+                    blocks, red_dev):
+    """Migration end to end between HOST tiers, as the reference models it
+    (the source's copy moves to the receiver, which lands it in its HOST tier:
+    NetArrive sets kHost, kvstore.cpp:914-923). Per step and per layer, with
+    the session's first `layers` layers (a bounded sample: pinned host buffers
+    for a whole 70B session on every rank would not fit the host):
+      source: pinned HOST -> H2D staging -> K2 unpack into its DEVICE pages ->
+              K3 into the receiver's pool over NVLink (CUDA IPC);
+      (every rank's sends landed: barrier)
+      receiver: K1 pack of what landed -> D2H -> pinned HOST.
+    Streams per direction overlap layers; max over ranks; bytes verified."""
+    L = min(8, n // blocks)
+    lb = blocks * pb
+    rank, world = dist.get_rank(), dist.get_world_size()
+    prv = cluster.ring_source(rank, world)
+    g = torch.Generator().manual_seed(1000 + rank)
+    h_src = torch.randint(0, 256, (L * lb,), dtype=torch.uint8, generator=g).pin_memory()
+    h_dst = torch.empty(L * lb, dtype=torch.uint8).pin_memory()
+    NB = 3
+    stage = [torch.empty(lb, dtype=torch.uint8, device=dev) for _ in range(NB)]
+    s_in, s_c, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+    main = torch.cuda.current_stream(dev)
+    d_src = torch.from_numpy(src_ids.view(np.int32)).to(dev)
+    d_peer = torch.from_numpy(peer_dst.view(np.int32)).to(dev)
+    d_mine = torch.from_numpy(my_dst.view(np.int32)).to(dev)
+
+    def send_phase():
+        s_in.wait_stream(main)
+        done = {}
+        for l in range(L):
+            sl = slice(l * blocks, (l + 1) * blocks)
+            with torch.cuda.stream(s_in):
+                if l - NB in done:
+                    s_in.wait_event(done.pop(l - NB))
+                stage[l % NB].copy_(h_src[l * lb:(l + 1) * lb], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(s_in)
+            s_c.wait_event(e)
+            kvx.unpack(pool, d_src[sl], blocks, stage[l % NB], kvx.COPY_AUTO, s_c.cuda_stream)
+            kvx.copy_pages(pool, d_src[sl], peer, d_peer[sl], blocks, kvx.COPY_AUTO, s_c.cuda_stream)
+            e2 = torch.cuda.Event()
+            e2.record(s_c)
+            done[l] = e2
+        main.wait_stream(s_c)
+
+    def receive_phase():
+        s_c.wait_stream(main)
+        done = {}
+        for l in range(L):
+            sl = slice(l * blocks, (l + 1) * blocks)
+            if l - NB in done:
+                s_c.wait_event(done.pop(l - NB))
+            kvx.pack(pool, d_mine[sl], blocks, stage[l % NB], kvx.COPY_AUTO, s_c.cuda_stream)
+            e = torch.cuda.Event()
+            e.record(s_c)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(e)
+                h_dst[l * lb:(l + 1) * lb].copy_(stage[l % NB], non_blocking=True)
+                e2 = torch.cuda.Event()
+                e2.record(s_out)
+                done[l] = e2
+        main.wait_stream(s_out)
 
     def step():
-        d_src.copy_(h_src, non_blocking=True)
-        d_dst.copy_(h_dst, non_blocking=True)
-        migrate(st, d_src, d_dst)
-        h_probe.copy_(peer.as_tensor()[last], non_blocking=True)
+        send_phase()
+        torch.cuda.synchronize()
+        dist.barrier()  # every sender's pages have landed in its receiver
+        receive_phase()
 
-    for _ in range(2):
-        step()
+    step()
     torch.cuda.synchronize()
     dist.barrier()
-    steps = max(1, min(args.steps, 5))
+    steps = max(1, min(args.steps, 3))
     e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    e[0].record(st)
+    e[0].record(main)
     for _ in range(steps):
         step()
-    e[1].record(st)
+    e[1].record(main)
     torch.cuda.synchronize()
-    dist.barrier()
     ms = cluster.max_over_ranks(dist, e[0].elapsed_time(e[1]) / steps, red_dev)
-    assert torch.equal(h_probe, pool.as_tensor()[int(src_ids[-1])].cpu()), "e2e probe page differs"
-    world = dist.get_world_size()
-    return {"value": world * n * pb / (ms * 1e-3) / GB, "unit": UNIT, "h2d_bytes_per_step": 2 * n * 4,
-            "d2h_bytes_per_step": pb, "ms_per_step": ms, "steps": steps,
-            "path": "block tables pinned HOST -> H2D, kvx_copy_pages per layer into the peer pool (IPC), "
-                    "landed probe page D2H"}
+    dist.barrier()
+    expect = torch.randint(0, 256, (L * lb,), dtype=torch.uint8, generator=torch.Generator().manual_seed(1000 + prv))
+    ok = bool(torch.equal(h_dst, expect))
+    oks = [None] * world
+    dist.all_gather_object(oks, ok)
+    assert all(oks), f"e2e HOST-to-HOST bytes differ on ranks {[i for i, o in enumerate(oks) if not o]}"
+    return {"value": world * L * lb / (ms * 1e-3) / GB, "unit": UNIT, "h2d_bytes_per_step": L * lb,
+            "d2h_bytes_per_step": L * lb, "ms_per_step": ms, "steps": steps, "layers_sampled": L,
+            "path": "source pinned HOST -> H2D -> kvx_unpack -> kvx_copy_pages into the peer pool (IPC/NVLink) | "
+                    "barrier | receiver kvx_pack -> D2H -> pinned HOST (per layer, streams overlap layers)"}
 
 
 # ---------------------------------------------------------------------------
