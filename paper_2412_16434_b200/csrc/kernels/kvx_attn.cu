@@ -19,6 +19,7 @@
 // the tensor pipe is idle >95% of the time even with mma.sync.
 
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <cstdlib>
 #include <cmath>
@@ -668,10 +669,12 @@ uint64_t workspace_for(uint64_t batch, uint64_t hq, uint64_t heads, int splits) 
 }
 
 // One-time per-device kernel attributes (dynamic smem, cluster sizes > 8).
+// Idempotent, so concurrent first calls from several host threads are fine;
+// the flags are atomics so the check itself is race-free.
 int configure(int device) {
-  static bool configured[64] = {};
+  static std::atomic<bool> configured[64] = {};
   const int slot = device < 0 ? 0 : device % 64;
-  if (configured[slot]) return KVX_OK;
+  if (configured[slot].load(std::memory_order_acquire)) return KVX_OK;
   KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kStagesWide, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes(kStagesWide, 4)),
                "kvx_decode_attention: smem attribute");
@@ -680,16 +683,17 @@ int configure(int device) {
                "kvx_decode_attention: smem attribute");
   KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                "kvx_decode_attention: cluster attribute");
-  configured[slot] = true;
+  configured[slot].store(true, std::memory_order_release);
   return KVX_OK;
 }
 
 // How many clusters of `splits` one-SM CTAs (8 warps, 192 KiB smem) the
 // device runs at once (cudaOccupancyMaxActiveClusters; GPC-shape dependent).
 int cluster_capacity(int device, int splits) {
-  static int cache[64][kMaxClusterSplits + 1] = {};
+  static std::atomic<int> cache[64][kMaxClusterSplits + 1] = {};
   const int slot = device < 0 ? 0 : device % 64;
-  int& c = cache[slot][splits];
+  std::atomic<int>& cached = cache[slot][splits];
+  int c = cached.load(std::memory_order_relaxed);
   if (c == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(splits, 1, 1);
@@ -708,6 +712,7 @@ int cluster_capacity(int device, int splits) {
       cudaGetLastError();
       c = -1;  // cached "does not fit"
     }
+    cached.store(c, std::memory_order_relaxed);
   }
   return c;
 }

@@ -15,6 +15,8 @@
 // shared-memory stages (no register staging at all).
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdlib>
 #include <vector>
 
@@ -161,11 +163,18 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
     a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + a.chunk_bytes - 1) / a.chunk_bytes);
     a.stages = geo.stages;
     const uint32_t smem = static_cast<uint32_t>(geo.stages) * a.chunk_bytes;
-    static uint32_t configured[64] = {};
-    const int dev = device < 0 ? 0 : device;
-    if (configured[dev] < smem) {
-      KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), who);
-      configured[dev] = smem;
+    // Largest dynamic smem configured so far per device; raised under a
+    // mutex so a smaller request can never lower the attribute after a
+    // larger one was recorded.
+    static std::atomic<uint32_t> configured[64] = {};
+    static std::mutex mu;
+    std::atomic<uint32_t>& have = configured[(device < 0 ? 0 : device) % 64];
+    if (have.load(std::memory_order_acquire) < smem) {
+      std::lock_guard<std::mutex> lock(mu);
+      if (have.load(std::memory_order_relaxed) < smem) {
+        KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), who);
+        have.store(smem, std::memory_order_release);
+      }
     }
     const uint64_t items = a.n_pages * a.chunks_per_page;
     unsigned grid =
