@@ -958,6 +958,8 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
     dist.all_gather_object(oks, ok)
     assert all(oks), f"migrated pages differ on ranks {[i for i, o in enumerate(oks) if not o]}"
 
+    gate = bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_src, d_peer_dst, d_my_dst,
+                                     blocks, L, layout, red_dev, args.mig_ctas) if args.migrate_mode == "p2p" else None
     e2e = bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, src_ids, peer_dst, my_dst, pb, n,
                           blocks, red_dev) if args.migrate_mode == "p2p" else None
 
@@ -975,6 +977,8 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
         peer.close()
     dist.barrier()
     launches = args.steps * (L * (1 if args.migrate_mode == "p2p" else 2) + K * L)
+    if serving is not None and gate is not None:
+        serving["pipeline_gate"] = gate
     return dict(value=value, ms_per_step=t_mig, clocks=clocks.summary(), session_bytes=session_bytes,
                 cfg=cfg, verified=True, serving=serving, e2e=e2e,
                 roofline={"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
@@ -984,6 +988,94 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
                           "note": "per GPU, per direction, measured while decode runs; one launch per layer",
                           "peak_kind": "measured peer copy (B200_PROFILING.md)"},
                 gpu_launches=launches)
+
+
+def bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_src, d_peer_dst, d_my_dst, blocks,
+                              L, layout, red_dev, mig_ctas=0):
+    """The reference's layer-wise pipeline gate (pipeline_gate, kvstore.cpp:
+    46-59; a request may decode layer l as soon as layer l has arrived)
+    realised across GPUs with device-side signals, no host in the loop: after
+    each layer's K3 launch the sender's stream writes the step number into
+    the receiver's per-layer flag (kvx_signal_write into the receiver's flag
+    page, opened through CUDA IPC); the receiver's decode of the migrating
+    session (batch 1, 64 q heads, full context) waits on flag l
+    (kvx_signal_wait) before attending over layer l. Compared with the
+    recurrence's prediction from the measured per-layer arrivals and decode
+    time, and with waiting for the whole session first."""
+    from paper_2412_16434_b200 import kvstore as K
+    rank, world = dist.get_rank(), dist.get_world_size()
+    prv, nxt = cluster.ring_source(rank, world), cluster.ring_peer(rank, world)
+    main, side = torch.cuda.current_stream(dev), torch.cuda.Stream(dev)
+    fpb = (4 * L + 15) // 16 * 16
+    flags = kvx.Pool(1, fpb, device=dev.index)
+    flags.as_tensor().zero_()
+    torch.cuda.synchronize()
+    peers = cluster.exchange_pool_handles(dist, rank, flags.ipc_export(), 1, fpb)
+    peer_flags = kvx.Pool.ipc_open(peers[nxt].handle, 1, fpb, dev.index)
+    sl = [slice(l * blocks, (l + 1) * blocks) for l in range(L)]
+    tables = [d_my_dst[sl[l]].view(1, blocks) for l in range(L)]
+    ctx = blocks * layout.block_tokens
+    ctx_t = torch.full((1,), ctx, dtype=torch.int32, device=dev)
+    q = (torch.randn(1, 64, 128, device=dev) * 0.5).to(torch.bfloat16)
+    out = torch.empty(1, 64, 128, dtype=torch.float32, device=dev)
+    att = kvx.Attention(layout, 64, blocks)
+    ws = torch.zeros(max(att.workspace_bytes(1, ctx), 1), dtype=torch.uint8, device=dev)
+
+    def send(step=None, timing=None):
+        for l in range(L):
+            kvx.copy_pages(pool, d_src[sl[l]], peer, d_peer_dst[sl[l]], blocks, kvx.COPY_AUTO, side.cuda_stream,
+                           max_ctas=mig_ctas)
+            if step is not None:
+                kvx.signal_write(peer_flags.base + 4 * l, step, side.cuda_stream)
+            if timing is not None:
+                timing[l + 1].record(side)
+
+    # measured alone: per-layer decode time, and the arrivals (sender clock)
+    for l in range(L):
+        att(pool, tables[l], ctx_t, q, out, 1, ctx, ws, main.cuda_stream)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record(main)
+    for l in range(L):
+        att(pool, tables[l], ctx_t, q, out, 1, ctx, ws, main.cuda_stream)
+    e[1].record(main)
+    torch.cuda.synchronize()
+    t_layer_us = e[0].elapsed_time(e[1]) * 1e3 / L
+    dist.barrier()
+    tev = [torch.cuda.Event(enable_timing=True) for _ in range(L + 1)]
+    tev[0].record(side)
+    send(timing=tev)
+    torch.cuda.synchronize()
+    ready_us = [tev[0].elapsed_time(tev[l + 1]) * 1e3 for l in range(L)]
+    all_ready = [None] * world
+    dist.all_gather_object(all_ready, ready_us)
+    src_ready = all_ready[prv]
+
+    gated = []
+    for step in range(1, 4):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        t[0].record(main)
+        side.wait_event(t[0])
+        send(step=step)
+        for l in range(L):
+            kvx.signal_wait(flags.base + 4 * l, step, main.cuda_stream)
+            att(pool, tables[l], ctx_t, q, out, 1, ctx, ws, main.cuda_stream)
+        t[1].record(main)
+        torch.cuda.synchronize()
+        gated.append(t[0].elapsed_time(t[1]) * 1e3)
+    dist.barrier()
+    peer_flags.close()
+    measured = statistics.median(gated)
+    first_end, _, stall = K.pipeline_gate([int(r * 1e3) for r in src_ready], 0, int(L * t_layer_us * 1e3))
+    worst = cluster.max_over_ranks(dist, measured, red_dev)
+    return {"decode": f"batch 1 over the migrating session ({L} layers, ctx {ctx}, 64 q heads)",
+            "layer_arrival_us_first_last": [src_ready[0], src_ready[-1]], "layer_decode_us": t_layer_us,
+            "measured_first_step_end_us": measured, "max_over_ranks_us": worst,
+            "predicted_first_step_end_us": first_end / 1e3, "predicted_stall_us": stall / 1e3,
+            "unpipelined_us": src_ready[-1] + L * t_layer_us, "mover_max_ctas": mig_ctas or "all",
+            "how": "per-layer device flags: sender stream writes into the receiver's flag page over IPC after "
+                   "each K3 launch (kvx_signal_write), receiver stream waits on it before each K4 (kvx_signal_wait)"}
 
 
 def bench_multi_e2e(args, torch, np, kvx, dev, dist, cluster, pool, peer, src_ids, peer_dst, my_dst, pb, n,

@@ -152,6 +152,15 @@ int kvx_event_record(void* event, void* stream);
 int kvx_event_synchronize(void* event);
 int kvx_event_query(void* event);
 int kvx_stream_wait_event(void* stream, void* event);
+/* Device-side signals between GPUs (no host in the loop): `stream` writes
+ * `value` to a 32-bit flag once all its prior work is complete and visible
+ * (the flag may live in a peer GPU's memory opened through CUDA IPC), and a
+ * stream waits until a flag is >= `value` before running its later work.
+ * This is how a migration's per-layer arrival (the reference's NetArrive,
+ * kvstore.cpp:914-923) gates the receiver's decode of that layer
+ * (pipeline_gate, kvstore.cpp:46-59) across GPUs. */
+int kvx_signal_write(void* d_flag, uint32_t value, void* stream);
+int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream);
 
 /* ---- page movement (K1-K3) ---------------------------------------------- */
 /* dst[i * page_bytes ...] = page(ids[i]) for i < n. ids in device memory. */

@@ -409,4 +409,33 @@ int kvx_stream_wait_event(void* stream, void* event) {
   return KVX_OK;
 }
 
+namespace {
+int fail_cu(CUresult r, const char* what) {
+  const char* name = nullptr;
+  cuGetErrorName(r, &name);
+  kvx::set_error(std::string(what) + ": " + (name ? name : "CUDA driver error"));
+  return KVX_ERR_CUDA;
+}
+}  // namespace
+
+int kvx_signal_write(void* d_flag, uint32_t value, void* stream) {
+  if (!d_flag || reinterpret_cast<uintptr_t>(d_flag) % 4) return kvx::fail_arg("kvx_signal_write: need a 4-B aligned flag");
+  // Default flags: a memory barrier orders every prior write of the stream
+  // (e.g. the K3 stores into a peer's pages) before the flag becomes visible.
+  const CUresult r = cuStreamWriteValue32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value,
+                                          CU_STREAM_WRITE_VALUE_DEFAULT);
+  return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_write");
+}
+
+int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream) {
+  if (!d_flag || reinterpret_cast<uintptr_t>(d_flag) % 4) return kvx::fail_arg("kvx_signal_wait: need a 4-B aligned flag");
+  int dev = 0, can_flush = 0;
+  cudaGetDevice(&dev);
+  cuDeviceGetAttribute(&can_flush, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, dev);
+  const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+  const CUresult r = cuStreamWaitValue32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value,
+                                         flags);
+  return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_wait");
+}
+
 }  // extern "C"

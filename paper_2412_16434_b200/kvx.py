@@ -70,6 +70,8 @@ def lib() -> C.CDLL:
         "kvx_pool_ipc_export": ([V, V], C.c_int),
         "kvx_pool_ipc_open": ([C.c_int, V, U64, U64, P(V)], C.c_int),
         "kvx_enable_peer_access": ([C.c_int, C.c_int], C.c_int),
+        "kvx_signal_write": ([V, C.c_uint32, V], C.c_int),
+        "kvx_signal_wait": ([V, C.c_uint32, V], C.c_int),
         "kvx_pack": ([V, V, U64, V, C.c_int, V], C.c_int),
         "kvx_unpack": ([V, V, U64, V, C.c_int, V], C.c_int),
         "kvx_copy_pages": ([V, V, V, V, U64, C.c_int, V], C.c_int),
@@ -222,6 +224,16 @@ def _device_view(ptr: int, nbytes: int, device: int):
 
 def page_bytes(layout: PageLayout) -> int:
     return lib().kvx_page_bytes(C.byref(layout))
+
+
+def signal_write(flag_addr: int, value: int, stream=None) -> None:
+    """Stream-ordered write of a 32-bit flag (peer memory allowed) after all prior work."""
+    check(lib().kvx_signal_write(flag_addr, value, _stream(stream)))
+
+
+def signal_wait(flag_addr: int, value: int, stream=None) -> None:
+    """The stream waits until the 32-bit flag is >= value."""
+    check(lib().kvx_signal_wait(flag_addr, value, _stream(stream)))
 
 
 def pack(pool: Pool, page_ids, n: int, dst, mode: int = COPY_AUTO, stream=None) -> None:

@@ -176,6 +176,28 @@ def test_file_pool_roundtrip_bit_exact(dev, layout, tmp_path):
         kvx.copy_pages(dev_pool, src_ids, disk, dst_ids, n, kvx.COPY_CE)
 
 
+def test_device_signal_orders_streams(dev):
+    """kvx_signal_write / kvx_signal_wait: a consumer stream that waits on a
+    flag sees everything the producer stream wrote before setting it (here a
+    50 ms spin delays the producer, so without the wait the copy would read
+    the old bytes)."""
+    flag = torch.zeros(4, dtype=torch.int32, device=dev)
+    src = torch.zeros(1 << 20, dtype=torch.uint8, device=dev)
+    dst = torch.empty_like(src)
+    prod, cons = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(prod):
+        torch.cuda._sleep(100_000_000)
+        src.fill_(7)
+    kvx.signal_write(flag.data_ptr() + 4, 3, prod)
+    kvx.signal_wait(flag.data_ptr() + 4, 3, cons)
+    with torch.cuda.stream(cons):
+        dst.copy_(src)
+    torch.cuda.synchronize()
+    assert int(flag[1]) == 3 and bool((dst == 7).all())
+    with pytest.raises(kvx.KvxError):
+        kvx.signal_write(flag.data_ptr() + 2, 1, prod)  # misaligned flag
+
+
 def test_host_pool_zero_copy_roundtrip(dev):
     """DEVICE -> mapped pinned HOST pool -> DEVICE with the SM mover (PCIe)."""
     layout = TINY
