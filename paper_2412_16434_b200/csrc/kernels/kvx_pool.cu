@@ -409,32 +409,62 @@ int kvx_stream_wait_event(void* stream, void* event) {
   return KVX_OK;
 }
 
+}  // extern "C"
+
 namespace {
+// Stream memory operations are driver-API entry points; they are resolved
+// through the runtime (cudaGetDriverEntryPoint) so libkvx.so does not link
+// libcuda directly and still loads on a machine without a GPU driver (the
+// CPU test suite checks its exports there).
+using WriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <typename Fn>
+int driver_fn(const char* name, Fn* out) {
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  const cudaError_t e = cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess) return kvx::fail_cuda(e, name);
+  if (q != cudaDriverEntryPointSuccess || !fn) {
+    kvx::set_error(std::string(name) + ": driver entry point unavailable");
+    return KVX_ERR_CUDA;
+  }
+  *out = reinterpret_cast<Fn>(fn);
+  return KVX_OK;
+}
+
 int fail_cu(CUresult r, const char* what) {
-  const char* name = nullptr;
-  cuGetErrorName(r, &name);
-  kvx::set_error(std::string(what) + ": " + (name ? name : "CUDA driver error"));
+  kvx::set_error(std::string(what) + ": CUDA driver error " + std::to_string(static_cast<int>(r)));
   return KVX_ERR_CUDA;
 }
 }  // namespace
 
+extern "C" {
+
 int kvx_signal_write(void* d_flag, uint32_t value, void* stream) {
   if (!d_flag || reinterpret_cast<uintptr_t>(d_flag) % 4) return kvx::fail_arg("kvx_signal_write: need a 4-B aligned flag");
+  static WriteValue32 write_value = nullptr;
+  if (!write_value)
+    if (int rc = driver_fn("cuStreamWriteValue32", &write_value)) return rc;
   // Default flags: a memory barrier orders every prior write of the stream
   // (e.g. the K3 stores into a peer's pages) before the flag becomes visible.
-  const CUresult r = cuStreamWriteValue32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value,
-                                          CU_STREAM_WRITE_VALUE_DEFAULT);
+  const CUresult r = write_value(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value,
+                                 CU_STREAM_WRITE_VALUE_DEFAULT);
   return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_write");
 }
 
 int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream) {
   if (!d_flag || reinterpret_cast<uintptr_t>(d_flag) % 4) return kvx::fail_arg("kvx_signal_wait: need a 4-B aligned flag");
+  static WaitValue32 wait_value = nullptr;
+  if (!wait_value)
+    if (int rc = driver_fn("cuStreamWaitValue32", &wait_value)) return rc;
   int dev = 0, can_flush = 0;
   cudaGetDevice(&dev);
-  cuDeviceGetAttribute(&can_flush, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, dev);
+  cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, dev);
   const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
-  const CUresult r = cuStreamWaitValue32(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value,
-                                         flags);
+  const CUresult r = wait_value(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value, flags);
   return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_wait");
 }
 

@@ -52,3 +52,15 @@ def test_file_pool_without_a_device(product_libs, tmp_path):
     with pytest.raises(kvx.KvxError):
         kvx.Pool.file(tmp_path / "bad.pages", 8, 1000)  # pages must be 4 KiB multiples (O_DIRECT)
     pool.close()
+
+
+def test_kvx_library_loads_without_a_driver(product_libs):
+    """libkvx.so resolves driver-API entry points through the runtime, so it
+    has no hard dependency on libcuda.so (the build check and the CPU suite
+    load it on machines without a GPU driver)."""
+    import shutil
+    import subprocess
+    if shutil.which("readelf") is None:
+        pytest.skip("readelf not available")
+    out = subprocess.run(["readelf", "-d", str(product_libs.KVX_LIB)], capture_output=True, text=True).stdout
+    assert "libcuda.so" not in out
