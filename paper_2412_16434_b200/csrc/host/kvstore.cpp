@@ -257,10 +257,13 @@ bool KvStore::evict_host_lru(std::int64_t bytes_needed, Ns now) {
     for (std::size_t l = 0; l < s.layers.size(); ++l) {
       std::vector<std::uint32_t> dropped;
       Layer& lay = s.layers[l];
-      for (std::size_t b = 0; b < lay.size(); ++b)
-        if ((lay[b] & kBacked) == kBacked) {
-          lay[b] = static_cast<std::uint8_t>(lay[b] & ~kOnHost);
-          got += page_bytes_;
+      std::uint8_t* const f = lay.data();  // locals: byte stores would force reloads through `lay`
+      const std::size_t nb = lay.size();
+      const std::int64_t pb = page_bytes_;
+      for (std::size_t b = 0; b < nb; ++b)
+        if ((f[b] & kBacked) == kBacked) {
+          f[b] = static_cast<std::uint8_t>(f[b] & ~kOnHost);
+          got += pb;
           if (backend_) dropped.push_back(static_cast<std::uint32_t>(b));
         }
       report_loss(idx, static_cast<std::uint16_t>(l), Tier::Host, dropped);
@@ -369,11 +372,13 @@ std::vector<BlockKey> KvStore::append_blocks(std::uint32_t session, std::int64_t
     Layer& lay = s.layers[static_cast<std::size_t>(l)];
     lay.resize(last);
     std::vector<std::uint32_t> lost[3];
+    std::uint8_t* const f = lay.data();
+    const bool track = backend_ != nullptr;
     for (std::uint32_t b = first; b < last; ++b) {
-      if (backend_)
+      if (track)
         for (unsigned t = 1; t < 3; ++t)
-          if (lay[b] & (1u << t)) lost[t].push_back(b);
-      lay[b] = static_cast<std::uint8_t>((lay[b] & ~kResidency) | kOnDev);
+          if (f[b] & (1u << t)) lost[t].push_back(b);
+      f[b] = static_cast<std::uint8_t>((f[b] & ~kResidency) | kOnDev);
       created.push_back(BlockKey{session, static_cast<std::uint16_t>(l), b});
     }
     if (!backend_) continue;
@@ -400,13 +405,15 @@ std::vector<BlockKey> KvStore::append_blocks(std::uint32_t session, std::int64_t
       m.kind = Kind::HostCopy;
       m.complete_at = link_done(pcie_down_, now, bytes, Link::PcieD2H);
       used_[1] += bytes;
-      for (std::uint32_t b = first; b < last; ++b) lay[b] |= kHostPending;
+      std::uint8_t* const f = lay.data();
+      for (std::uint32_t b = first; b < last; ++b) f[b] |= kHostPending;
       disk_ready = m.complete_at;
       post(m, scheduled);
     }
     m.kind = Kind::DiskWrite;
     m.complete_at = link_done(disk_out_, disk_ready, bytes, Link::DiskWrite);
-    for (std::uint32_t b = first; b < last; ++b) lay[b] |= kDiskPending;
+    std::uint8_t* const fd = lay.data();
+    for (std::uint32_t b = first; b < last; ++b) fd[b] |= kDiskPending;
     s.persists_in_flight += 1;
     post(m, scheduled);
   }
@@ -570,14 +577,24 @@ std::optional<LoadPlan> KvStore::plan_layerwise_load(std::uint32_t session, Ns n
     std::int64_t src_blocks[3] = {0, 0, 0};  // [host, disk, inbound]
     std::uint32_t lo = 0, hi = 0;
     bool any = false;
-    for (std::size_t b = 0; b < lay.size(); ++b) {
-      std::uint8_t& f = lay[b];
-      if (f & (kOnDev | kLoadPending)) continue;
-      if (!any) lo = static_cast<std::uint32_t>(b);
-      hi = static_cast<std::uint32_t>(b);
-      any = true;
-      f |= kLoadPending;
-      ++src_blocks[(f & kOnHost) ? 0 : (f & kOnDisk) ? 1 : 2];
+    {
+      std::uint8_t* const p = lay.data();
+      const std::size_t nb = lay.size();
+      std::int64_t host = 0, disk = 0, inbound = 0;
+      for (std::size_t b = 0; b < nb; ++b) {
+        const std::uint8_t f = p[b];
+        if (f & (kOnDev | kLoadPending)) continue;
+        if (!any) lo = static_cast<std::uint32_t>(b);
+        hi = static_cast<std::uint32_t>(b);
+        any = true;
+        p[b] = static_cast<std::uint8_t>(f | kLoadPending);
+        host += (f & kOnHost) != 0;
+        disk += !(f & kOnHost) && (f & kOnDisk);
+        inbound += !(f & (kOnHost | kOnDisk));
+      }
+      src_blocks[0] = host;
+      src_blocks[1] = disk;
+      src_blocks[2] = inbound;
     }
     const std::int64_t src_bytes[3] = {src_blocks[0] * page_bytes_, src_blocks[1] * page_bytes_,
                                        src_blocks[2] * page_bytes_};
@@ -684,8 +701,11 @@ PromoteResult KvStore::promote(std::uint32_t session, Ns now, std::vector<Schedu
     m.kind = Kind::LoadH2D;
     m.bytes = bytes;
     m.complete_at = link_done(pcie_up_, up_ready, bytes, Link::PcieH2D);
-    for (std::uint32_t b = lo; b <= hi; ++b)
-      if (!(lay[b] & kOnDev)) lay[b] |= kLoadPending;
+    {
+      std::uint8_t* const p = lay.data();
+      for (std::uint32_t b = lo; b <= hi; ++b)
+        if (!(p[b] & kOnDev)) p[b] |= kLoadPending;
+    }
     post(m, scheduled);
     s.load_eta[li] = m.complete_at;
     ++res.device_layers;
@@ -717,20 +737,26 @@ void KvStore::offload_session(std::uint32_t session, Ns now, std::vector<Schedul
     std::uint32_t lo = 0, hi = 0;
     bool any = false;
     std::vector<std::uint32_t> gone;
-    for (std::size_t b = 0; b < lay.size(); ++b) {
-      std::uint8_t& f = lay[b];
-      if (!(f & kOnDev)) continue;
-      if (f & kBacked) {
-        f = static_cast<std::uint8_t>(f & ~kOnDev);
-        used_[0] -= page_bytes_;
-        demoted += page_bytes_;
-        if (backend_) gone.push_back(static_cast<std::uint32_t>(b));
-      } else {
-        if (!any) lo = static_cast<std::uint32_t>(b);
-        hi = static_cast<std::uint32_t>(b);
-        any = true;
-        copy += page_bytes_;
+    {
+      std::uint8_t* const p = lay.data();
+      const std::size_t nb = lay.size();
+      const std::int64_t pb = page_bytes_;
+      const bool track = backend_ != nullptr;
+      for (std::size_t b = 0; b < nb; ++b) {
+        const std::uint8_t f = p[b];
+        if (!(f & kOnDev)) continue;
+        if (f & kBacked) {
+          p[b] = static_cast<std::uint8_t>(f & ~kOnDev);
+          demoted += pb;
+          if (track) gone.push_back(static_cast<std::uint32_t>(b));
+        } else {
+          if (!any) lo = static_cast<std::uint32_t>(b);
+          hi = static_cast<std::uint32_t>(b);
+          any = true;
+          copy += pb;
+        }
       }
+      used_[0] -= demoted;
     }
     report_loss(session, static_cast<std::uint16_t>(l), Tier::Device, gone);
     if (demoted > 0)
@@ -747,8 +773,9 @@ void KvStore::offload_session(std::uint32_t session, Ns now, std::vector<Schedul
     m.reason = TransferReason::Persist;
     m.complete_at = link_done(pcie_down_, now, copy, Link::PcieD2H);
     used_[1] += copy;
+    std::uint8_t* const p = lay.data();
     for (std::uint32_t b = lo; b <= hi; ++b)
-      if ((lay[b] & kOnDev) && !(lay[b] & kBacked)) lay[b] |= kHostPending | kDropOnPersist;
+      if ((p[b] & kOnDev) && !(p[b] & kBacked)) p[b] |= kHostPending | kDropOnPersist;
     post(m, scheduled);
   }
 }
@@ -855,8 +882,9 @@ void KvStore::void_session_offload(std::uint32_t session) {
     m.voided = true;
     if (m.layer >= s.layers.size()) continue;
     Layer& lay = s.layers[m.layer];
-    for (std::uint64_t b = m.lo; b <= m.hi && b < lay.size(); ++b)
-      lay[b] = static_cast<std::uint8_t>(lay[b] & ~(kHostPending | kDropOnPersist));
+    std::uint8_t* const p = lay.data();
+    const std::uint64_t z = std::min<std::uint64_t>(static_cast<std::uint64_t>(m.hi) + 1, lay.size());
+    for (std::uint64_t b = m.lo; b < z; ++b) p[b] = static_cast<std::uint8_t>(p[b] & ~(kHostPending | kDropOnPersist));
   }
 }
 
@@ -889,23 +917,40 @@ KvStore::ApplyResult KvStore::apply_transfer(std::uint64_t id, Ns now) {
   std::vector<std::uint32_t> gained, dev_dropped;
   const bool track = backend_ != nullptr;  // hoisted: flag stores alias members
   std::uint8_t* const flags = lay.data();
+  // Byte-flag loops below work on local copies of the bounds and the base
+  // pointer: a uint8_t store may alias anything reached through a reference,
+  // which would force a reload per element and block vectorisation.
+  const std::uint64_t lo = m.lo;
   // Sets `bit` on every block of the range, remembering which ones are new.
   auto gain_bit = [&](std::uint8_t bit, std::uint8_t clear) {
+    std::uint8_t* const f = flags;
+    const std::uint64_t a = lo, z = stop;
     if (track)
-      for (std::uint64_t b = m.lo; b < stop; ++b)
-        if (!(flags[b] & bit)) gained.push_back(static_cast<std::uint32_t>(b));
+      for (std::uint64_t b = a; b < z; ++b)
+        if (!(f[b] & bit)) gained.push_back(static_cast<std::uint32_t>(b));
     const std::uint8_t keep = static_cast<std::uint8_t>(~clear);
-    for (std::uint64_t b = m.lo; b < stop; ++b) flags[b] = static_cast<std::uint8_t>((flags[b] | bit) & keep);
+    for (std::uint64_t b = a; b < z; ++b) f[b] = static_cast<std::uint8_t>((f[b] | bit) & keep);
   };
   // Completes a deferred drop: DEVICE residency leaves once a persist lands.
   auto settle_drop = [&]() {
+    std::uint8_t* const f = flags;
+    const std::uint64_t a = lo, z = stop;
     std::int64_t n = 0;
-    for (std::uint64_t b = m.lo; b < stop; ++b)
-      if ((flags[b] & kDropOnPersist) && (flags[b] & kOnDev)) {
-        flags[b] = static_cast<std::uint8_t>(flags[b] & ~(kOnDev | kDropOnPersist));
-        ++n;
-        if (track) dev_dropped.push_back(static_cast<std::uint32_t>(b));
+    constexpr std::uint8_t both = kDropOnPersist | kOnDev;
+    if (track) {
+      for (std::uint64_t b = a; b < z; ++b)
+        if ((f[b] & both) == both) {
+          f[b] = static_cast<std::uint8_t>(f[b] & ~both);
+          ++n;
+          dev_dropped.push_back(static_cast<std::uint32_t>(b));
+        }
+    } else {
+      for (std::uint64_t b = a; b < z; ++b) {
+        const bool hit = (f[b] & both) == both;
+        n += hit;
+        f[b] = static_cast<std::uint8_t>(hit ? f[b] & ~both : f[b]);
       }
+    }
     used_[0] -= n * page_bytes_;
   };
 
@@ -945,13 +990,15 @@ KvStore::ApplyResult KvStore::apply_transfer(std::uint64_t id, Ns now) {
       gain_bit(kOnHost, kHostPending);
       report_gain(m.session, m.layer, Tier::Host, BlockEvent::SwapOut, gained);
       {
+        std::uint8_t* const f = flags;
+        const std::uint64_t a = lo, z = stop;
         std::int64_t n = 0;
-        for (std::uint64_t b = m.lo; b < stop; ++b) {
-          if (flags[b] & kOnDev) {
+        for (std::uint64_t b = a; b < z; ++b) {
+          if (f[b] & kOnDev) {
             ++n;
             if (track) dev_dropped.push_back(static_cast<std::uint32_t>(b));
           }
-          flags[b] = static_cast<std::uint8_t>(flags[b] & ~(kOnDev | kDropOnPersist));
+          f[b] = static_cast<std::uint8_t>(f[b] & ~(kOnDev | kDropOnPersist));
         }
         used_[0] -= n * page_bytes_;
       }
