@@ -401,6 +401,43 @@ def test_fused_append_decode_step(dev, layout, hq, splits):
     assert torch.equal(out_a, out_b)
 
 
+def test_fused_decode_step_full_size(dev):
+    """Config 2's decode shape at full context (8B KV, ctx 8192, batch 4,
+    auto plan = clustered split-K): the fused step equals append + attention
+    bit for bit, and the appended rows are where the block table says."""
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    B, ctx, mb = 4, 8192, 512
+    pages = B * mb
+    rng = np.random.default_rng(77)
+    tables = rng.permutation(pages).astype(np.uint32).reshape(B, mb)
+    ids = torch.arange(pages, dtype=torch.int32, device=dev)
+    tags = torch.stack([ids * 0 + 9, ids * 0, ids], -1).contiguous()
+    pool_a = kvx.Pool(pages, pb, device=0)
+    pool_b = kvx.Pool(pages, pb, device=0)
+    for p_ in (pool_a, pool_b):
+        kvx.fill_pages(p_, ids, tags, pages, 5, layout, kvx.FILL_VALUES)
+    nk = torch.randn(B, 8, 128, device=dev).to(torch.bfloat16)
+    nv = torch.randn(B, 8, 128, device=dev).to(torch.bfloat16)
+    q = torch.randn(B, 32, 128, device=dev).to(torch.bfloat16)
+    lens = np.array([ctx, ctx - 15, ctx - 16, 4097], np.int32)
+    d_tables, d_ctx = to_dev(tables.view(np.int32), dev), to_dev(lens, dev)
+    att = kvx.Attention(layout, 32, mb)
+    ws = torch.zeros(max(att.workspace_bytes(B, ctx), 1), dtype=torch.uint8, device=dev)
+    out_a = torch.empty(B, 32, 128, dtype=torch.float32, device=dev)
+    out_b = torch.empty_like(out_a)
+    att(pool_a, d_tables, d_ctx, q, out_a, B, ctx, ws, new_k=nk, new_v=nv)
+    t = lens - 1
+    kvx.append_kv(pool_b, layout, to_dev(tables[np.arange(B), t // 16].astype(np.int32), dev),
+                  to_dev((t % 16).astype(np.int32), dev), nk, nv, B)
+    att(pool_b, d_tables, d_ctx, q, out_b, B, ctx, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(pool_a.as_tensor(), pool_b.as_tensor())
+    assert torch.equal(out_a, out_b)
+    page = pool_a.as_tensor()[int(tables[1, t[1] // 16])].view(torch.bfloat16).view(2, 8, 16, 128)
+    assert torch.equal(page[0, :, t[1] % 16], nk[1]) and torch.equal(page[1, :, t[1] % 16], nv[1])
+
+
 def test_full_70b_session_migration_property(dev):
     """Config 3 at full size on one GPU (10.7 GB, Llama-3.1-70B KV @ 32K):
     every layer's 2,048 pages move page->page (K3, the migration kernel) into
