@@ -1243,6 +1243,9 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
+    # torchrun sets OMP_NUM_THREADS=1 per rank; the reference arm runs on rank
+    # 0 alone and may use every host core (set before OpenMP initialises).
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     cfg = CFG_8B if world == 1 else CFG_70B
     import oracle.oracle as O
     O.build_payload()
