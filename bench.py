@@ -1012,6 +1012,20 @@ def bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_
     torch.cuda.synchronize()
     peers = cluster.exchange_pool_handles(dist, rank, flags.ipc_export(), 1, fpb)
     peer_flags = kvx.Pool.ipc_open(peers[nxt].handle, 1, fpb, dev.index)
+    # Capability probe (every rank, then agree): stream memory ops on a
+    # peer's IPC-mapped page. If any rank cannot, all skip the gate together.
+    err = None
+    try:
+        kvx.signal_write(peer_flags.base, 0, side.cuda_stream)
+        kvx.signal_wait(flags.base, 0, side.cuda_stream)
+        side.synchronize()
+    except Exception as e:  # noqa: BLE001 — reported in the JSON, not fatal to the bench
+        err = str(e)
+    errs = [None] * world
+    dist.all_gather_object(errs, err)
+    if any(errs):
+        peer_flags.close()
+        return {"skipped": f"device signals unavailable: {[e for e in errs if e][0]}"}
     sl = [slice(l * blocks, (l + 1) * blocks) for l in range(L)]
     tables = [d_my_dst[sl[l]].view(1, blocks) for l in range(L)]
     ctx = blocks * layout.block_tokens
