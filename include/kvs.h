@@ -229,6 +229,8 @@ typedef struct {
   int32_t free_running; /* 0: lockstep (move at apply); 1: issue at schedule, complete at apply */
   int32_t pad_;
   const char* disk_path; /* NULL/"": DISK tier in pinned host memory; else the file backing it */
+  uint32_t migrate_max_ctas; /* cap on the K3 grid of migration pushes (0 = all SMs) */
+  uint32_t pad2_;
 } kvs_payload_options;
 
 int kvs_cluster_create(kvs_cluster** out);

@@ -64,6 +64,7 @@ struct PayloadOptions {
   std::uint64_t landing_pages = 0;  // HBM pool for migrated HOST-tier copies
   std::uint64_t disk_pages = 0;     // DISK tier: pages in disk_path, or pinned host if empty
   std::string disk_path;            // file backing the DISK tier (created / grown; kept)
+  std::uint32_t migrate_max_ctas = 0;  // cap on the K3 grid of migration pushes (0 = all SMs)
   std::uint64_t seed = 0;           // content of Created blocks
   int fill_mode = KVX_FILL_VALUES;
   bool free_running = false;

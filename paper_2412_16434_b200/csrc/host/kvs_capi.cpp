@@ -424,6 +424,7 @@ symsim::PayloadOptions to_payload_opts(const kvs_payload_options* o) {
   p.seed = o->seed;
   p.free_running = o->free_running != 0;
   if (o->disk_path) p.disk_path = o->disk_path;
+  p.migrate_max_ctas = o->migrate_max_ctas;
   return p;
 }
 }  // namespace

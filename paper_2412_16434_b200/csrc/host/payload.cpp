@@ -331,7 +331,9 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
       if (on_device) {
         const std::uint32_t* ds = runner.device_ids(L, s_ids, 0);
         const std::uint32_t* dd = runner.device_ids(L, d_ids, 1);
-        kvx_check(kvx_copy_pages(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO, L.stream), "page copy");
+        kvx_check(kvx_copy_pages_capped(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO,
+                                        push ? src_node.opts_.migrate_max_ctas : 0u, L.stream),
+                  "page copy");
       } else if (file_hop) {
         // HBM <-> file: through this lane's pinned bounce pages, a chunk at a
         // time; stream order keeps each chunk's file I/O ahead of the copy

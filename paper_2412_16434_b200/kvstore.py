@@ -113,7 +113,8 @@ class _PayloadOpts(C.Structure):
                 ("block_tokens", C.c_int32), ("dtype", C.c_int32), ("fill_mode", C.c_int32),
                 ("device_pages", C.c_uint64), ("host_pages", C.c_uint64), ("landing_pages", C.c_uint64),
                 ("disk_pages", C.c_uint64), ("seed", C.c_uint64), ("free_running", C.c_int32),
-                ("pad_", C.c_int32), ("disk_path", C.c_char_p)]
+                ("pad_", C.c_int32), ("disk_path", C.c_char_p), ("migrate_max_ctas", C.c_uint32),
+                ("pad2_", C.c_uint32)]
 
 
 @dataclass
@@ -571,12 +572,13 @@ class PayloadOptions:
     seed: int = 0
     free_running: bool = False
     disk_path: str = ""  # file backing the DISK tier ("" = pinned host stand-in)
+    migrate_max_ctas: int = 0  # cap on the K3 grid of migration pushes (0 = all SMs)
 
     def _c(self) -> "_PayloadOpts":
         return _PayloadOpts(self.device, self.num_kv_heads, self.head_dim, self.block_tokens, self.dtype,
                             self.fill_mode, self.device_pages, self.host_pages, self.landing_pages,
                             self.disk_pages, self.seed, int(self.free_running), 0,
-                            self.disk_path.encode() if self.disk_path else None)
+                            self.disk_path.encode() if self.disk_path else None, self.migrate_max_ctas, 0)
 
     def page_bytes(self) -> int:
         return 2 * self.num_kv_heads * self.block_tokens * self.head_dim * (2 if self.dtype == 1 else 4)

@@ -184,16 +184,20 @@ def test_swap_offload_and_reactivation(dev, free_running):
 
 
 @MODES
-def test_migration_lands_in_receiver_hbm(dev, free_running):
+@pytest.mark.parametrize("cap", [0, 2], ids=["uncapped", "capped-2-ctas"])
+def test_migration_lands_in_receiver_hbm(dev, free_running, cap):
     """import_migration on node 1 pulls the frozen session from node 0: each
     layer's NetArrive lands in node 1's HBM landing pool (HOST tier in the
     ledger, reference kvstore.cpp:914-923); the follow-up demand load is an
-    HBM->HBM page copy."""
+    HBM->HBM page copy. Also with the migration pushes' grid capped
+    (PayloadOptions.migrate_max_ctas)."""
     cluster = K.PayloadCluster()
     stores, nodes, pumps = [], [], []
     for n in range(2):
         st = K.KvStore(gpu=tiny_profile(), opts=K.Options(node_id=n))
-        nd = K.NodePayload(cluster, n, payload_opts(free_running=free_running))
+        opts = payload_opts(free_running=free_running)
+        opts.migrate_max_ctas = cap
+        nd = K.NodePayload(cluster, n, opts)
         nd.attach(st)
         st.register_session(5, "mig")
         st.finalize_sessions()
