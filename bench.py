@@ -401,7 +401,7 @@ def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
     L, blocks = cfg["layers"], cfg["ctx"] // cfg["block_tokens"]
     layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
     pb = layout.page_bytes()
-    B = 16
+    B = args.bg_batch  # decode batch (16 default; 64 = config 5's decode batches)
     dec_pages = B * L * blocks
     dpool = kvx.Pool(dec_pages, pb, device=dev.index)
     ids = torch.arange(dec_pages, dtype=torch.int32, device=dev)
@@ -1363,6 +1363,7 @@ def main():
     ap.add_argument("--skip-overlap", action="store_true")
     ap.add_argument("--attn-sweep", action="store_true", help="diagnostic: time fixed split-K factors")
     ap.add_argument("--bg-sweep", action="store_true", help="diagnostic: sweep mover CTA caps beside decode")
+    ap.add_argument("--bg-batch", type=int, default=16, help="decode batch of the overlap / background section")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"], help="N>1 control plane")
     ap.add_argument("--same-device", action="store_true", help="test mode: all ranks on cuda:0")
     ap.add_argument("--layers", type=int, default=0, help="test mode: shrink the N>1 session")
