@@ -29,11 +29,17 @@ constexpr int kVecThreads = 256;
 constexpr int kVecUnroll = 4;
 constexpr uint32_t kVecChunk = kVecThreads * kVecUnroll * 16;  // 16 KiB per work item
 
-// TMA mover geometry, measured on B200 (profiles/r01_summary.md sweep):
-//   gather OR scatter (pack/unpack; one side contiguous): 32 KiB x 4 stages,
-//     one CTA per SM -> 6.40 / 6.47 TB/s (98-99% of the measured copy peak)
-//   gather AND scatter (page -> page copy): 64 KiB x 3 stages -> 6.25 TB/s
-// KVX_BULK_CHUNK / KVX_BULK_STAGES / KVX_BULK_CTAS_PER_SM override both (sweeps).
+// TMA mover geometry per access pattern, measured on B200 (1 GiB session of
+// 16,384 scattered 64 KiB pages, profiles/r01_mover_geometry_sweep.txt):
+//   gather, contiguous destination (pack):      32 KiB x 4 stages, 1 CTA/SM
+//     -> 6.60 TB/s (16 KiB x 6 x 2: 6.57)
+//   contiguous source, scatter (unpack):        16 KiB x 6 stages, 2 CTAs/SM
+//     -> 6.60 TB/s (32 KiB x 4 x 1: 6.49)
+//   gather AND scatter (page -> page copy):     16 KiB x 6 stages, 2 CTAs/SM
+//     -> 6.41-6.42 TB/s (64 KiB x 3 x 1: 6.09-6.25; 32 KiB x 4 x 1: 6.27)
+// Two CTAs per SM give each SM two independent issue loops (more chunks in
+// flight) where a scattered destination makes each store's completion slower.
+// KVX_BULK_CHUNK / KVX_BULK_STAGES / KVX_BULK_CTAS_PER_SM override all (sweeps).
 constexpr int kBulkMaxStages = 16;
 struct BulkGeometry {
   uint32_t chunk;
@@ -41,8 +47,8 @@ struct BulkGeometry {
   int ctas_per_sm;
 };
 
-BulkGeometry bulk_geometry(bool both_scattered) {
-  BulkGeometry b = both_scattered ? BulkGeometry{65536, 3, 1} : BulkGeometry{32768, 4, 1};
+BulkGeometry bulk_geometry(bool src_scattered, bool dst_scattered) {
+  BulkGeometry b = (src_scattered && !dst_scattered) ? BulkGeometry{32768, 4, 1} : BulkGeometry{16384, 6, 2};
   if (const char* e = std::getenv("KVX_BULK_CHUNK")) b.chunk = static_cast<uint32_t>(std::atoi(e));
   if (const char* e = std::getenv("KVX_BULK_STAGES")) b.stages = std::atoi(e);
   if (const char* e = std::getenv("KVX_BULK_CTAS_PER_SM")) b.ctas_per_sm = std::atoi(e);
@@ -158,7 +164,7 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
   const int sms = sm_count(device);
   if (mode == KVX_COPY_AUTO) mode = tma_ok ? KVX_COPY_TMA : KVX_COPY_SM;
   if (mode == KVX_COPY_TMA) {
-    const BulkGeometry geo = bulk_geometry(a.src_ids != nullptr && a.dst_ids != nullptr);
+    const BulkGeometry geo = bulk_geometry(a.src_ids != nullptr, a.dst_ids != nullptr);
     a.chunk_bytes = static_cast<uint32_t>(std::min<uint64_t>(a.page_bytes, geo.chunk));
     a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + a.chunk_bytes - 1) / a.chunk_bytes);
     a.stages = geo.stages;
