@@ -214,7 +214,7 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
     }
 
     # Variants (not the headline): other copy mode, fused page->page K3.
-    other = kvx.COPY_TMA if mode != kvx.COPY_TMA else kvx.COPY_SM
+    other = kvx.COPY_SM if mode in (kvx.COPY_AUTO, kvx.COPY_TMA) else kvx.COPY_TMA  # AUTO = TMA for HBM<->HBM
     _, (p2, u2) = time_events(torch, lambda i, ev: step(i, ev, other), max(5, args.steps // 2), 2, marks=2)
     extra["alt_mode"] = "tma" if other == kvx.COPY_TMA else "sm"
     extra["alt_pack_hbm_gbs"] = 2 * session_bytes / (statistics.mean(p2) * 1e-3) / GB
