@@ -169,7 +169,6 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   // Outside the page ring, so pushes may land while the owner still streams.
   __shared__ __align__(16) float s_recv_o[16 * kD + 4 * kMaxClusterSplits];
   __shared__ __align__(16) float s_recv_ml[kMaxClusterSplits * 16 * 2];
-  __shared__ float s_recv_w[8 * 16 + 16 * 2];
   __shared__ __align__(8) uint64_t s_merge_bar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -414,43 +413,40 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     // its (m, l) per row to every owner (one 8-byte st.async per (row, owner))
     // and each float4 of its partial O to the owner of that slice. The
     // owner's mbarrier completes when all bytes have landed.
-    float* s_wf = s_recv_w;  // [W][16] warp weights
-    float* s_rml = s_wf + 8 * 16;  // [16][2] this CTA's (M, L) per row
-    if (threadIdx.x < rows) {
-      const int r = threadIdx.x;
-      float M = -INFINITY;
+    // Every thread derives the weights of the row it pushes itself (redundant
+    // but parallel: measured faster than a few threads + a barrier here).
+    auto row_weights = [&](int r, float (&f)[W], float& M, float& L) {
+      M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < W; ++w) M = fmaxf(M, sml[(w * 16 + r) * 2]);
       const float Mb = M == -INFINITY ? 0.f : M;
-      float L = 0.f;
+      L = 0.f;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const float f = exp2f(sml[(w * 16 + r) * 2] - Mb);
-        s_wf[w * 16 + r] = f;
-        L += f * sml[(w * 16 + r) * 2 + 1];
+        f[w] = exp2f(sml[(w * 16 + r) * 2] - Mb);
+        L += f[w] * sml[(w * 16 + r) * 2 + 1];
       }
-      s_rml[r * 2] = M;
-      s_rml[r * 2 + 1] = L;
-    }
-    __syncthreads();
+    };
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every owner's barrier is armed
     const uint32_t bar_local = smem_u32(&s_merge_bar);
     if (threadIdx.x < rows * a.splits) {
       const int r = threadIdx.x / a.splits, owner = threadIdx.x - r * a.splits;
-      st_async_v2(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2), owner), s_rml[r * 2], s_rml[r * 2 + 1],
-                  map_rank(bar_local, owner));
+      float f[W], M, L;
+      row_weights(r, f, M, L);
+      st_async_v2(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2), owner), M, L, map_rank(bar_local, owner));
     }
     for (int q = threadIdx.x; q < rows * kD / 4; q += blockDim.x) {
       const int e = 4 * q, r = e / kD, d = e - r * kD;
+      float f[W], M, L;
+      row_weights(r, f, M, L);
       float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const float f = s_wf[w * 16 + r];
         const float4 v = *reinterpret_cast<const float4*>(so + (w * 16 + r) * kOs + d);
-        O.x += f * v.x;
-        O.y += f * v.y;
-        O.z += f * v.z;
-        O.w += f * v.w;
+        O.x += f[w] * v.x;
+        O.y += f[w] * v.y;
+        O.z += f[w] * v.z;
+        O.w += f[w] * v.w;
       }
       const int owner = e / chunk;
       st_async_v4(map_rank(smem_u32(s_recv_o + split * chunk + (e - owner * chunk)), owner), O,
