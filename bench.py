@@ -257,7 +257,8 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
     return dict(value=value, ms_per_step=ms_per_step, extra=extra, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": ncu_traffic(dom_name), "kernel": dom_name,
-                          "algorithmic_bytes_per_launch": 2 * session_bytes, "peak_kind": peak_kind},
+                          "algorithmic_bytes_per_launch": 2 * session_bytes, "peak_kind": peak_kind,
+                          "frac_of_nominal_8tbs": achieved / 8000.0},
                 attention=attention, e2e=e2e, overlap=overlap, store_cycle=store_cycle, disk_tier=disk,
                 gpu_launches=launches,
                 session_bytes=session_bytes)
