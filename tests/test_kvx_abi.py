@@ -64,3 +64,27 @@ def test_kvx_library_loads_without_a_driver(product_libs):
         pytest.skip("readelf not available")
     out = subprocess.run(["readelf", "-d", str(product_libs.KVX_LIB)], capture_output=True, text=True).stdout
     assert "libcuda.so" not in out
+
+
+def test_product_path_does_not_route_through_the_oracle(product_libs):
+    """The oracle is test infrastructure: no product module imports it, no
+    product library links it, and the store mirror loads the product library
+    unless a test passes the oracle's path explicitly."""
+    import ast
+    import shutil
+    import subprocess
+    pkg = ROOT / "paper_2412_16434_b200"
+    for py in pkg.glob("*.py"):
+        tree = ast.parse(py.read_text())
+        for node in ast.walk(tree):
+            if isinstance(node, ast.Import):
+                assert not any(a.name.split(".")[0] == "oracle" for a in node.names), py
+            if isinstance(node, ast.ImportFrom):
+                assert (node.module or "").split(".")[0] != "oracle", py
+    if shutil.which("readelf"):
+        for lib in (product_libs.KVX_LIB, product_libs.HOST_LIB):
+            out = subprocess.run(["readelf", "-d", str(lib)], capture_output=True, text=True).stdout
+            assert "oracle" not in out and "symsim_oracle" not in out, lib
+    from paper_2412_16434_b200 import _build, kvstore as K
+    lib = K.load_kvs_library()
+    assert lib._name == str(_build.HOST_LIB) and "oracle" not in lib._name
