@@ -25,7 +25,9 @@
 //
 // usage: payload_sim [--device-pages N] [--policy symphony|swap|retain|recompute]
 
+#include <algorithm>
 #include <cinttypes>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -84,6 +86,50 @@ Trace chat_trace(std::uint64_t seed) {
   return t;
 }
 
+// Config 5's traffic at test scale (--zipf S): S multi-turn sessions from the
+// reference corpus generator, session popularity Zipf(1.2) mapped to turns
+// per session (rank r gets max(2, 64 / r^1.2) turns, cycling its own turn
+// list), fast closed-loop users (4,000 wpm, Exp(0.5 s) think), advisories
+// injected by the reference generator. Same construction as
+// tests/cpp/serve_sim.cpp config5(); here on the tiny KV shape so every page
+// of every node fits one GPU.
+Trace zipf_trace(int sessions, int users, std::uint64_t seed) {
+  SyntheticSpec spec;
+  spec.sessions = sessions;
+  spec.multi_turn_fraction = 1.0;
+  auto scripts = synthesize_corpus(spec, seed);
+  std::mt19937_64 rng(seed + 7);
+  std::vector<std::size_t> order(scripts.size());
+  for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::shuffle(order.begin(), order.end(), rng);
+  for (std::size_t r = 0; r < order.size(); ++r) {
+    auto& sc = scripts[order[r]];
+    const int want = std::max(2, static_cast<int>(std::lround(64.0 / std::pow(static_cast<double>(r + 1), 1.2))));
+    std::vector<Turn> turns;
+    for (int k = 0; k < want; ++k) turns.push_back(sc.turns[static_cast<std::size_t>(k) % sc.turns.size()]);
+    sc.turns = std::move(turns);
+  }
+  SpeedModel speeds;
+  speeds.typing_wpm_mean = 4000.0;
+  Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1, speeds);
+  std::exponential_distribution<double> think(2.0);
+  for (auto& e : t.events) {
+    if (e.kind != EventKind::Inference || e.turn_index == 0) continue;
+    const auto& sc = t.sessions[e.session_index];
+    e.delta = ns_from_sec(think(rng)) +
+              ns_from_sec(static_cast<double>(sc.turns[e.turn_index].prompt_words) * 60.0 / sc.user.typing_wpm);
+  }
+  return inject_advisories(std::move(t), 0.0, seed + 3);
+}
+
+std::uint64_t fnv(std::uint64_t h, std::uint64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xFF;
+    h *= 1099511628211ULL;
+  }
+  return h;
+}
+
 const char* tier_s(Tier t) { return tier_name(t); }
 
 }  // namespace
@@ -93,7 +139,15 @@ int main(int argc, char** argv) {
   std::string policy = "symphony";
   bool free_running = false;
   std::string disk_dir;  // --disk-dir: DISK tier in files (one per node) instead of pinned host memory
+  int zipf_sessions = 0, users = 64, num_nodes = 2;
+  std::int64_t pool_pages = 0;  // --pages: per-node DEVICE / HOST / landing pages (and the store's capacities)
+  bool digest = false;          // --digest: hashes of the ledger and records instead of every row
   for (int i = 1; i < argc; ++i) {
+    if (!std::strcmp(argv[i], "--zipf") && i + 1 < argc) zipf_sessions = std::atoi(argv[++i]);
+    if (!std::strcmp(argv[i], "--users") && i + 1 < argc) users = std::atoi(argv[++i]);
+    if (!std::strcmp(argv[i], "--nodes") && i + 1 < argc) num_nodes = std::atoi(argv[++i]);
+    if (!std::strcmp(argv[i], "--pages") && i + 1 < argc) pool_pages = std::atoll(argv[++i]);
+    if (!std::strcmp(argv[i], "--digest")) digest = true;
     if (!std::strcmp(argv[i], "--disk-dir") && i + 1 < argc) disk_dir = argv[++i];
     if (!std::strcmp(argv[i], "--device-pages") && i + 1 < argc) device_pages = std::atoll(argv[++i]);
     if (!std::strcmp(argv[i], "--policy") && i + 1 < argc) policy = argv[++i];
@@ -103,15 +157,19 @@ int main(int argc, char** argv) {
   (void)disk_dir;
   RunConfig cfg;
   cfg.policy = policy_from(policy);
-  cfg.num_nodes = 2;
+  cfg.num_nodes = num_nodes;
   cfg.gpu.num_layers = kLayers;
   cfg.gpu.kv_bytes_per_token = static_cast<std::int64_t>(kLayers) * 2 * kHeads * kDim * 4;
   cfg.gpu.hbm_capacity = 80'000'000'000;
   const std::int64_t page = cfg.gpu.kv_bytes_per_token / kLayers * kBlockTokens;
   if (device_pages > 0) cfg.device_capacity = device_pages * page;  // force cooperative purges
   cfg.host_capacity = 4096 * page;
+  if (pool_pages > 0) {  // the store's tiers are exactly the pools behind them
+    cfg.device_capacity = pool_pages * page;
+    cfg.host_capacity = pool_pages * page;
+  }
   cfg.sample_period = ns_from_sec(5);
-  const Trace trace = chat_trace(20260417);
+  const Trace trace = zipf_sessions > 0 ? zipf_trace(zipf_sessions, users, 505) : chat_trace(20260417);
 
 #ifdef WITH_PAYLOAD
   PayloadCluster cluster;
@@ -123,6 +181,12 @@ int main(int argc, char** argv) {
   po.host_pages = 4096;
   po.landing_pages = 4096;
   po.disk_pages = 8192;
+  if (pool_pages > 0) {
+    po.device_pages = static_cast<std::uint64_t>(pool_pages) + 64;
+    po.host_pages = static_cast<std::uint64_t>(pool_pages);
+    po.landing_pages = static_cast<std::uint64_t>(pool_pages);
+    po.disk_pages = 4 * static_cast<std::uint64_t>(pool_pages);
+  }
   po.seed = kSeed;
   po.free_running = free_running;
   set_default_tier_backend_factory([&](int node_id) -> TierBackend* {
@@ -139,14 +203,37 @@ int main(int argc, char** argv) {
   std::printf("policy %s nodes %d transfers %zu records %zu\n", rep.policy.c_str(), rep.num_nodes,
               rep.transfers.size(), rep.records.size());
   std::size_t migrate_rows = 0;
+  std::uint64_t hl = 1469598103934665603ULL, hr = 1469598103934665603ULL;
   for (const auto& r : rep.transfers) {
     if (r.reason == TransferReason::Migrate) ++migrate_rows;
+    if (digest) {
+      hl = fnv(hl, static_cast<std::uint64_t>(r.time));
+      hl = fnv(hl, (static_cast<std::uint64_t>(r.node) << 40) ^ (static_cast<std::uint64_t>(r.session) << 8) ^
+                       static_cast<std::uint64_t>(r.reason));
+      hl = fnv(hl, (static_cast<std::uint64_t>(r.layer_lo) << 32) | (static_cast<std::uint64_t>(r.layer_hi) << 16) |
+                       (static_cast<std::uint64_t>(r.from) << 4) | static_cast<std::uint64_t>(r.to));
+      hl = fnv(hl, static_cast<std::uint64_t>(r.bytes));
+      continue;
+    }
     std::printf("T %" PRId64 " n%d s%u l%u-%u %s>%s %" PRId64 " %s\n", r.time, r.node, r.session, r.layer_lo,
                 r.layer_hi, tier_s(r.from), tier_s(r.to), r.bytes, reason_name(r.reason));
   }
-  for (const auto& r : rep.records)
+  for (const auto& r : rep.records) {
+    if (digest) {
+      hr = fnv(hr, (static_cast<std::uint64_t>(r.session) << 32) | r.turn);
+      hr = fnv(hr, static_cast<std::uint64_t>(r.node));
+      hr = fnv(hr, static_cast<std::uint64_t>(r.arrival));
+      hr = fnv(hr, static_cast<std::uint64_t>(r.first_token));
+      hr = fnv(hr, static_cast<std::uint64_t>(r.finish));
+      hr = fnv(hr, static_cast<std::uint64_t>(r.load_stall));
+      continue;
+    }
     std::printf("R s%u t%u n%d arr %" PRId64 " adm %" PRId64 " ft %" PRId64 " fin %" PRId64 " stall %" PRId64 "\n",
                 r.session, r.turn, r.node, r.arrival, r.admit, r.first_token, r.finish, r.load_stall);
+  }
+  if (digest)
+    std::printf("digest ledger %016" PRIx64 " records %016" PRIx64 " rows %zu records %zu\n", hl, hr,
+                rep.transfers.size(), rep.records.size());
   std::printf("migrate_rows %zu\n", migrate_rows);
 
 #ifdef WITH_PAYLOAD
