@@ -23,7 +23,8 @@
 // then migrates sessions to node 1 (the trick of
 // /root/reference/proj/tests/acceptance.cpp:172-188).
 //
-// usage: payload_sim [--device-pages N] [--policy symphony|swap|retain|recompute]
+// usage: payload_sim [--device-pages N] [--policy symphony|swap|retain|recompute] [--free-running]
+//                    [--disk-dir DIR] [--zipf S | --sharegpt S] [--users U] [--nodes N] [--pages P] [--digest]
 
 #include <algorithm>
 #include <cinttypes>
@@ -122,6 +123,28 @@ Trace zipf_trace(int sessions, int users, std::uint64_t seed) {
   return inject_advisories(std::move(t), 0.0, seed + 3);
 }
 
+// Config 4's traffic at test scale (--sharegpt S): the reference corpus
+// generator's ShareGPT-like defaults (73.4% multi-turn, lognormal lengths)
+// for S sessions, fast closed-loop users, Poisson think times (Exp, mean
+// 0.5 s), advisories from the reference generator (serve_sim.cpp config4()).
+Trace sharegpt_trace(int sessions, int users, std::uint64_t seed) {
+  SyntheticSpec spec;
+  spec.sessions = sessions;
+  auto scripts = synthesize_corpus(spec, seed);
+  SpeedModel speeds;
+  speeds.typing_wpm_mean = 4000.0;
+  Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1, speeds);
+  std::mt19937_64 rng(seed + 2);
+  std::exponential_distribution<double> think(2.0);
+  for (auto& e : t.events) {
+    if (e.kind != EventKind::Inference || e.turn_index == 0) continue;
+    const auto& sc = t.sessions[e.session_index];
+    e.delta = ns_from_sec(think(rng)) +
+              ns_from_sec(static_cast<double>(sc.turns[e.turn_index].prompt_words) * 60.0 / sc.user.typing_wpm);
+  }
+  return inject_advisories(std::move(t), 0.0, seed + 3);
+}
+
 std::uint64_t fnv(std::uint64_t h, std::uint64_t v) {
   for (int i = 0; i < 8; ++i) {
     h ^= (v >> (8 * i)) & 0xFF;
@@ -139,11 +162,12 @@ int main(int argc, char** argv) {
   std::string policy = "symphony";
   bool free_running = false;
   std::string disk_dir;  // --disk-dir: DISK tier in files (one per node) instead of pinned host memory
-  int zipf_sessions = 0, users = 64, num_nodes = 2;
+  int zipf_sessions = 0, sharegpt_sessions = 0, users = 64, num_nodes = 2;
   std::int64_t pool_pages = 0;  // --pages: per-node DEVICE / HOST / landing pages (and the store's capacities)
   bool digest = false;          // --digest: hashes of the ledger and records instead of every row
   for (int i = 1; i < argc; ++i) {
     if (!std::strcmp(argv[i], "--zipf") && i + 1 < argc) zipf_sessions = std::atoi(argv[++i]);
+    if (!std::strcmp(argv[i], "--sharegpt") && i + 1 < argc) sharegpt_sessions = std::atoi(argv[++i]);
     if (!std::strcmp(argv[i], "--users") && i + 1 < argc) users = std::atoi(argv[++i]);
     if (!std::strcmp(argv[i], "--nodes") && i + 1 < argc) num_nodes = std::atoi(argv[++i]);
     if (!std::strcmp(argv[i], "--pages") && i + 1 < argc) pool_pages = std::atoll(argv[++i]);
@@ -169,7 +193,9 @@ int main(int argc, char** argv) {
     cfg.host_capacity = pool_pages * page;
   }
   cfg.sample_period = ns_from_sec(5);
-  const Trace trace = zipf_sessions > 0 ? zipf_trace(zipf_sessions, users, 505) : chat_trace(20260417);
+  const Trace trace = zipf_sessions > 0      ? zipf_trace(zipf_sessions, users, 505)
+                      : sharegpt_sessions > 0 ? sharegpt_trace(sharegpt_sessions, users, 404)
+                                              : chat_trace(20260417);
 
 #ifdef WITH_PAYLOAD
   PayloadCluster cluster;
