@@ -906,20 +906,32 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
 
         def migrate(st, src=d_src, dst=d_my_dst):
             with torch.cuda.stream(st):
-                for l in range(L):
-                    snd, rcv = bufs[l % 2]
-                    kvx.pack(pool, src[sl[l]], blocks, snd, kvx.COPY_AUTO, st.cuda_stream)
-                    if staged:
+                if staged:  # gloo (tests): host-staged, one layer at a time
+                    for l in range(L):
+                        snd, rcv = bufs[l % 2]
+                        kvx.pack(pool, src[sl[l]], blocks, snd, kvx.COPY_AUTO, st.cuda_stream)
                         st.synchronize()
                         hbufs[0].copy_(snd)
                         ops = [dist.P2POp(dist.isend, hbufs[0], nxt), dist.P2POp(dist.irecv, hbufs[1], prv)]
                         for w in dist.batch_isend_irecv(ops):
                             w.wait()
                         rcv.copy_(hbufs[1])
-                    else:
-                        ops = [dist.P2POp(dist.isend, snd, nxt), dist.P2POp(dist.irecv, rcv, prv)]
-                        for w in dist.batch_isend_irecv(ops):
-                            w.wait()  # the side stream waits on the transfer, the host does not
+                        kvx.unpack(pool, dst[sl[l]], blocks, rcv, kvx.COPY_AUTO, st.cuda_stream)
+                    return
+                # NCCL: software-pipelined over two buffer pairs — layer l+1 is
+                # packed on the side stream while layer l's send/recv runs on
+                # NCCL's stream; the side stream waits for l's transfer only
+                # before unpacking it. A buffer pair is reused two layers later,
+                # after its unpack (recv) and the wait on its send were queued.
+                kvx.pack(pool, src[sl[0]], blocks, bufs[0][0], kvx.COPY_AUTO, st.cuda_stream)
+                for l in range(L):
+                    snd, rcv = bufs[l % 2]
+                    works = dist.batch_isend_irecv([dist.P2POp(dist.isend, snd, nxt),
+                                                    dist.P2POp(dist.irecv, rcv, prv)])
+                    if l + 1 < L:
+                        kvx.pack(pool, src[sl[l + 1]], blocks, bufs[(l + 1) % 2][0], kvx.COPY_AUTO, st.cuda_stream)
+                    for w in works:
+                        w.wait()  # the side stream waits on the transfer, the host does not
                     kvx.unpack(pool, dst[sl[l]], blocks, rcv, kvx.COPY_AUTO, st.cuda_stream)
 
     # Serving: a decode batch on every rank (70B shape: 64 q heads over 8 kv heads).
