@@ -149,42 +149,66 @@ const char* kvs_last_error(void);
 /* 1 for the product build, 0 for the oracle build of the same source. */
 int kvs_is_product(void);
 
+/* replaces symsim::KvStore::KvStore, kvstore.hpp:118 */
 int kvs_create(const kvs_gpu_profile* gpu, const kvs_link_profile* links, const kvs_options* opts,
                kvs_store** out);
 void kvs_destroy(kvs_store* s);
 
+/* replaces symsim::register_session, kvstore.hpp:120 */
 int kvs_register_session(kvs_store* s, uint32_t session, const char* id, int32_t priority);
+/* replaces symsim::finalize_sessions, kvstore.hpp:121 */
 int kvs_finalize_sessions(kvs_store* s);
 
 int kvs_get_counters(kvs_store* s, kvs_counters* out);
 int kvs_get_session(kvs_store* s, uint32_t session, kvs_session_info* out);
+/* replaces symsim::bytes_for_new_blocks, kvstore.hpp:133 */
 int kvs_bytes_for_new_blocks(kvs_store* s, uint32_t session, int64_t new_tokens, int64_t* out);
+/* replaces symsim::bytes_for_load, kvstore.hpp:135 */
 int kvs_bytes_for_load(kvs_store* s, uint32_t session, int64_t* out);
+/* replaces symsim::bytes_for_promote, kvstore.hpp:137 */
 int kvs_bytes_for_promote(kvs_store* s, uint32_t session, int64_t* out);
+/* replaces symsim::reserve_device, kvstore.hpp:139 */
 int kvs_reserve_device(kvs_store* s, int64_t bytes);
+/* replaces symsim::unreserve_device, kvstore.hpp:140 */
 int kvs_unreserve_device(kvs_store* s, int64_t bytes);
+/* replaces symsim::set_active, kvstore.hpp:149 */
 int kvs_set_active(kvs_store* s, uint32_t session, int32_t active, int64_t now);
 
 /* Scheduled transfers -> kvs_out_scheduled; created keys -> kvs_out_keys. */
+/* replaces symsim::append_blocks, kvstore.hpp:157 (kvstore.cpp:202-271) */
 int kvs_append_blocks(kvs_store* s, uint32_t session, int64_t new_tokens, int64_t now);
+/* replaces symsim::purge_from_device, kvstore.hpp:166 (kvstore.cpp:332-431) */
 int kvs_purge_from_device(kvs_store* s, int64_t bytes_needed, int64_t now, int32_t spare_high_priority,
                           int64_t* freed);
 /* layer_ready -> kvs_out_times. */
+/* replaces symsim::plan_layerwise_load, kvstore.hpp:177 (kvstore.cpp:433-543) */
 int kvs_plan_layerwise_load(kvs_store* s, uint32_t session, int64_t now, int64_t compute_per_layer,
                             int32_t reason, kvs_load_plan* out);
+/* replaces symsim::promote, kvstore.hpp:183 (kvstore.cpp:545-640) */
 int kvs_promote(kvs_store* s, uint32_t session, int64_t now, kvs_promote_result* out);
+/* replaces symsim::offload_session, kvstore.hpp:188 (kvstore.cpp:642-708) */
 int kvs_offload_session(kvs_store* s, uint32_t session, int64_t now);
+/* replaces symsim::release_session, kvstore.hpp:191 (kvstore.cpp:710-736) */
 int kvs_release_session(kvs_store* s, uint32_t session, int64_t now);
+/* replaces symsim::mark_migrating_out, kvstore.hpp:196 (kvstore.cpp:738-742) */
 int kvs_mark_migrating_out(kvs_store* s, uint32_t session);
+/* replaces symsim::import_migration, kvstore.hpp:200 (kvstore.cpp:744-789) */
 int kvs_import_migration(kvs_store* s, uint32_t session, int64_t tokens, int64_t now);
+/* replaces symsim::apply_transfer, kvstore.hpp:213 (kvstore.cpp:816-926) */
 int kvs_apply_transfer(kvs_store* s, uint64_t id, int64_t now, kvs_apply_result* out);
+/* replaces symsim::void_session_loads, kvstore.hpp:218 */
 int kvs_void_session_loads(kvs_store* s, uint32_t session);
+/* replaces symsim::void_session_offload, kvstore.hpp:219 */
 int kvs_void_session_offload(kvs_store* s, uint32_t session);
 /* Candidates in eviction order -> kvs_out_metas. */
+/* replaces symsim::evictable_blocks, kvstore.hpp:226 (kvstore.cpp:310-330) */
 int kvs_evictable_blocks(kvs_store* s, int32_t spare_high_priority);
+/* replaces symsim::check_budgets, kvstore.hpp:228 */
 int kvs_check_budgets(kvs_store* s);
+/* replaces symsim::device_usage_debug, kvstore.hpp:130 */
 int kvs_device_usage_debug(kvs_store* s, char* buf, size_t cap);
 
+/* replaces symsim::ledger, kvstore.hpp:221 */
 size_t kvs_ledger_size(kvs_store* s);
 int kvs_ledger_copy(kvs_store* s, size_t start, size_t count, kvs_record* out);
 
@@ -195,7 +219,9 @@ size_t kvs_out_metas(kvs_store* s, const kvs_block_meta** out);
 
 /* Free functions of the reference API. evict_order writes the permutation of
  * the input indices into `order` (n entries). */
+/* replaces symsim::evict_order, kvstore.hpp:43 (kvstore.cpp:34-44) */
 int kvs_evict_order(const kvs_block_meta* candidates, size_t n, uint32_t* order);
+/* replaces symsim::pipeline_gate, kvstore.hpp:96 (kvstore.cpp:46-59) */
 int kvs_pipeline_gate(const int64_t* layer_ready, size_t n, int64_t compute_ready, int64_t step_ns,
                       kvs_gate_result* out);
 int kvs_transfer_time(int64_t bytes, int32_t link, const kvs_link_profile* links, int64_t* out);
