@@ -368,8 +368,10 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   KVX_TRACE(4);
   KVX_TRACE_IF(lane == 0, 16 + warp);  // per-warp loop end (slots 16..16+W-1)
   // All our global reads of the pool are done: let the next kernel's CTAs
-  // start launching into SMs as ours drain.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // start launching into SMs as ours drain. Cluster launches signal only at
+  // the very end (below): dependents placed while these clusters still hold
+  // their SMs fragment the GPCs and the next launch loses co-residence.
+  if (!a.cluster_merge) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Full row sums across the 4 lanes sharing a row.
   l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
       a.out[(static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
     }
     KVX_TRACE(6);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
   for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
@@ -833,13 +836,15 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     attr[1].val.clusterDim.x = plan.cluster ? splits : 1;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
-    // Cluster launches go without PDL: early-resident dependent clusters
-    // cost 4-11 us per launch at batch 1 and >= 32K context and ~6% at batch
-    // 8 x 32K; the 0.3-0.5 us PDL gains at batch 2-4 x 8K do not pay for that
-    // (profiles/attn_trace/r01_cluster_pdl.log). KVX_ATTN_CLUSTER_PDL=1
-    // forces it on (measurement knob).
+    // Cluster launches use PDL too, with launch_dependents at the very end of
+    // the kernel (after the split merge): signalled after the page loop, the
+    // early-resident dependent clusters fragmented the GPCs and cost 4-11 us
+    // per launch at batch 1 >= 32K; signalled at the end they save 0.3-0.6 us
+    // per launch at every clustered shape (profiles/attn_trace/
+    // r01_cluster_pdl_late.log). KVX_ATTN_CLUSTER_PDL=0 turns it off
+    // (measurement knob).
     static const char* cluster_pdl_env = std::getenv("KVX_ATTN_CLUSTER_PDL");
-    const bool cluster_pdl = cluster_pdl_env && cluster_pdl_env[0] == '1';
+    const bool cluster_pdl = !(cluster_pdl_env && cluster_pdl_env[0] == '0');
     if (plan.cluster && !cluster_pdl) attr[0].val.programmaticStreamSerializationAllowed = 0;
     cfg.attrs = attr;
     cfg.numAttrs = plan.cluster ? 2 : 1;
