@@ -1302,7 +1302,7 @@ def arm_config(cfg, world):
         workload = (f"{cfg['model']} @{cfg['ctx']} session per rank, ring migration rank r -> r+1 "
                     "(page-to-page into the receiver's pool) while every rank decodes a batch of 4 "
                     f"{cfg['model']} @{cfg['ctx']} requests")
-    return {"workload": workload, "model_shape": cfg["model"], "seq_len": cfg["ctx"], "layers": cfg["layers"],
+    return {"workload": workload, "kv_shape": cfg["model"], "seq_len": cfg["ctx"], "layers": cfg["layers"],
             "kv_heads": cfg["kv_heads"], "head_dim": cfg["head_dim"], "kv_dtype": "bf16", "page_bytes": pb,
             "session_bytes": n * pb, "parallelism": "single" if world == 1 else f"ring-p2p{world}",
             "l2": "inputs larger than the 126 MB L2 (1 GiB / 10.7 GB per step); no flush"}
