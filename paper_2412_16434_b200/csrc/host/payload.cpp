@@ -18,6 +18,8 @@
 
 #include "symsim/payload.hpp"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges show per lane in nsys / ncu
+
 #include <algorithm>
 #include <chrono>
 #include <stdexcept>
@@ -308,6 +310,11 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
                    : (dp0 == kDiskPool || from_disk)             ? kLaneDisk
                                                                  : kLaneOut;
   Lane& L = runner.lanes_[lane];
+  static const char* const kLaneNames[] = {"kvs:IN", "kvs:OUT", "kvs:DISK", "kvs:PEER"};
+  nvtxRangePushA(kLaneNames[lane]);  // host-side enqueue of this batch (NVTX, SURVEY.md §5 tracing)
+  struct PopRange {
+    ~PopRange() { nvtxRangePop(); }
+  } pop_range;
   std::vector<Touch> touched;
   touched.reserve(src.size() + dst.size());
   for (const Ref& r : src) touched.emplace_back(&src_node, r);
@@ -552,7 +559,9 @@ void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
   InFlight& f = it->second;
   if (kvx_event_query(f.event) == KVX_NOT_READY) {  // the GPU is behind the model clock
     const std::uint64_t t0 = now_ns();
+    nvtxRangePushA("kvs:apply_wait");
     kvx_check(kvx_event_synchronize(f.event), "event sync");
+    nvtxRangePop();
     apply_wait_ns_ += now_ns() - t0;
   }
   // Later moves touching these pages are ordered by the pages' fences.

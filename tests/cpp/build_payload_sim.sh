@@ -19,7 +19,8 @@ mkdir -p "$OUT" "$OBJ/overlay/symsim"
 for h in kvstore costmodel time; do cp "$ROOT/include/symsim/$h.hpp" "$OBJ/overlay/symsim/$h.hpp"; done
 make -s -C "$ROOT/paper_2412_16434_b200/csrc" all
 
-PROD_FLAGS=(-std=c++20 -O2 -DWITH_PAYLOAD -I"$OBJ/overlay" -I"$REF/include" -I"$ROOT/include" -I"$JSON_DIR")
+CUDA_INC="${CUDA_HOME:-/usr/local/cuda}/include"
+PROD_FLAGS=(-std=c++20 -O2 -DWITH_PAYLOAD -I"$OBJ/overlay" -I"$REF/include" -I"$ROOT/include" -I"$CUDA_INC" -I"$JSON_DIR")
 REF_FLAGS=(-std=c++20 -O2 -I"$REF/include" -I"$JSON_DIR")
 
 pids=()
