@@ -782,6 +782,8 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
   const int H = layout->num_kv_heads, Hq = params->num_q_heads;
   if (H <= 0 || Hq <= 0 || Hq % H != 0) return kvx::fail_arg("kvx_decode_attention: num_q_heads must be a multiple of num_kv_heads");
   if (kvx_page_bytes(layout) != pool->page_bytes) return kvx::fail_arg("kvx_decode_attention: layout/page size mismatch");
+  if (max_ctx < 0 || static_cast<int64_t>(max_ctx) > static_cast<int64_t>(params->max_blocks) * layout->block_tokens)
+    return kvx::fail_arg("kvx_decode_attention: max_ctx exceeds the block-table row (max_blocks * block_tokens)");
   const int group = Hq / H;
   const float scale = params->scale > 0.f ? params->scale : 1.0f / std::sqrt(static_cast<float>(layout->head_dim));
   const cudaStream_t st = kvx::as_stream(stream);

@@ -198,6 +198,19 @@ def test_device_signal_orders_streams(dev):
         kvx.signal_write(flag.data_ptr() + 2, 1, prod)  # misaligned flag
 
 
+def test_attention_rejects_context_beyond_the_table(dev):
+    """max_ctx larger than a block-table row could read past it: refused."""
+    layout = LLAMA8B
+    pool = kvx.Pool(8, layout.page_bytes(), device=0)
+    att = kvx.Attention(layout, 32, 4)  # rows of 4 pages = 64 tokens
+    tables = torch.zeros(1, 4, dtype=torch.int32, device=dev)
+    q = torch.zeros(1, 32, 128, dtype=torch.bfloat16, device=dev)
+    out = torch.empty(1, 32, 128, dtype=torch.float32, device=dev)
+    ctx = torch.tensor([65], dtype=torch.int32, device=dev)
+    with pytest.raises(kvx.KvxError):
+        att(pool, tables, ctx, q, out, 1, 65)
+
+
 def test_host_pool_zero_copy_roundtrip(dev):
     """DEVICE -> mapped pinned HOST pool -> DEVICE with the SM mover (PCIe)."""
     layout = TINY
