@@ -41,7 +41,11 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "KV migrate GB/s (% HBM/NVLink roofline)"
+# BASELINE.json's metric, verbatim. `value` is its first half (KV migrate
+# GB/s; the roofline fraction is the `roofline` object); the second half
+# (requests/s at equal p50 latency) comes from the calibrated serving sweeps
+# in profiles/ (tools/serving_equal_p50.py), not from a per-run measurement.
+METRIC = "KV migrate GB/s (% HBM/NVLink roofline); requests/s at equal p50 latency"
 UNIT = "GB/s"
 GB = 1e9
 
