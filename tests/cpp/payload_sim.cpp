@@ -47,7 +47,10 @@ using namespace symsim;
 
 namespace {
 
-constexpr int kLayers = 2, kHeads = 4, kDim = 64, kBlockTokens = 16;
+// KV shape: config 1's tiny fp32 shape by default; --shape 8b switches to
+// Llama-3.1-8B's (32 layers, 8 kv heads, head_dim 128, bf16: 64 KiB pages).
+int kLayers = 2, kHeads = 4, kDim = 64, kElt = 4, kDtype = 0;
+constexpr int kBlockTokens = 16;
 constexpr std::uint64_t kSeed = 0x5EEDC0DE;
 
 Trace chat_trace(std::uint64_t seed) {
@@ -172,6 +175,13 @@ int main(int argc, char** argv) {
     if (!std::strcmp(argv[i], "--nodes") && i + 1 < argc) num_nodes = std::atoi(argv[++i]);
     if (!std::strcmp(argv[i], "--pages") && i + 1 < argc) pool_pages = std::atoll(argv[++i]);
     if (!std::strcmp(argv[i], "--digest")) digest = true;
+    if (!std::strcmp(argv[i], "--shape") && i + 1 < argc && !std::strcmp(argv[++i], "8b")) {
+      kLayers = 32;
+      kHeads = 8;
+      kDim = 128;
+      kElt = 2;
+      kDtype = 1;
+    }
     if (!std::strcmp(argv[i], "--disk-dir") && i + 1 < argc) disk_dir = argv[++i];
     if (!std::strcmp(argv[i], "--device-pages") && i + 1 < argc) device_pages = std::atoll(argv[++i]);
     if (!std::strcmp(argv[i], "--policy") && i + 1 < argc) policy = argv[++i];
@@ -183,7 +193,7 @@ int main(int argc, char** argv) {
   cfg.policy = policy_from(policy);
   cfg.num_nodes = num_nodes;
   cfg.gpu.num_layers = kLayers;
-  cfg.gpu.kv_bytes_per_token = static_cast<std::int64_t>(kLayers) * 2 * kHeads * kDim * 4;
+  cfg.gpu.kv_bytes_per_token = static_cast<std::int64_t>(kLayers) * 2 * kHeads * kDim * kElt;
   cfg.gpu.hbm_capacity = 80'000'000'000;
   const std::int64_t page = cfg.gpu.kv_bytes_per_token / kLayers * kBlockTokens;
   if (device_pages > 0) cfg.device_capacity = device_pages * page;  // force cooperative purges
@@ -202,7 +212,7 @@ int main(int argc, char** argv) {
   std::vector<std::unique_ptr<NodePayload>> nodes;
   PayloadOptions po;
   po.device = 0;  // both nodes on the one visible GPU (peer path = local HBM)
-  po.layout = kvx_page_layout{kHeads, kDim, kBlockTokens, KVX_DTYPE_F32};
+  po.layout = kvx_page_layout{kHeads, kDim, kBlockTokens, kDtype ? KVX_DTYPE_BF16 : KVX_DTYPE_F32};
   po.device_pages = static_cast<std::uint64_t>(device_pages > 0 ? device_pages + 64 : 2048);
   po.host_pages = 4096;
   po.landing_pages = 4096;
@@ -265,7 +275,7 @@ int main(int argc, char** argv) {
 #ifdef WITH_PAYLOAD
   // Every copy on every node, bit-exact against the CPU restatement.
   std::vector<std::uint8_t> got(static_cast<std::size_t>(page)), want(static_cast<std::size_t>(page));
-  const kvxo_layout ol{kHeads, kDim, kBlockTokens, 0};
+  const kvxo_layout ol{kHeads, kDim, kBlockTokens, kDtype};
   std::size_t copies = 0, bad = 0, pages_held[4] = {0, 0, 0, 0};
   for (int n = 0; n < cfg.num_nodes; ++n) {
     const KvStore& st = sim.node(n).store();
