@@ -460,9 +460,19 @@ int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream) {
   static WaitValue32 wait_value = nullptr;
   if (!wait_value)
     if (int rc = driver_fn("cuStreamWaitValue32", &wait_value)) return rc;
-  int dev = 0, can_flush = 0;
+  // Per-device "can flush remote writes" (cached: 0 unknown, 1 no, 2 yes).
+  static std::atomic<int> flush_cap[64] = {};
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, dev);
+  std::atomic<int>& cap = flush_cap[(dev < 0 ? 0 : dev) % 64];
+  int can_flush = cap.load(std::memory_order_relaxed);
+  if (can_flush == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev);
+    can_flush = v ? 2 : 1;
+    cap.store(can_flush, std::memory_order_relaxed);
+  }
+  can_flush = can_flush == 2;
   const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
   const CUresult r = wait_value(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value, flags);
   return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_wait");
