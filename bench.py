@@ -66,6 +66,14 @@ def load_peaks():
 NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 
 
+def DECODE_FLAGS(kvx):  # noqa: N802 — a constant that needs the loaded module
+    """Every decode launch here keeps the decode-step contract of
+    KVX_ATTN_EARLY_PREFETCH (include/kvx.h): the kernel before it in the
+    stream writes no block table, no ctx_lens and no page but the one holding
+    position ctx-1, so tables and first pages are fetched before the PDL wait."""
+    return kvx.ATTN_EARLY_PREFETCH
+
+
 class ClockSampler:
     """NVML sampler thread: SM clock and clock-event reasons during timing."""
 
@@ -323,7 +331,7 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
         reps = max(sets, 16 if batch < 64 else 4)
 
         def timed(splits, merge=kvx.MERGE_AUTO):
-            att = kvx.Attention(layout, 32, blocks, num_splits=splits, split_merge=merge)
+            att = kvx.Attention(layout, 32, blocks, num_splits=splits, split_merge=merge, flags=DECODE_FLAGS(kvx))
             ws = torch.zeros(max(att.workspace_bytes(batch, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
             return graph_time_ms(torch, lambda i: att(pool, tables[i % sets], ctx, q, out, batch, cfg["ctx"], ws),
                                  reps, max(3, min(args.steps, 20)))
@@ -353,7 +361,7 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
         out = torch.empty(batch, 32, 128, dtype=torch.float32, device=dev)
         slots = torch.full((batch,), (cfg["ctx"] - 1) % cfg["block_tokens"], dtype=torch.int32, device=dev)
         last = [t[:, (cfg["ctx"] - 1) // cfg["block_tokens"]].contiguous() for t in tables]
-        att = kvx.Attention(layout, 32, blocks)
+        att = kvx.Attention(layout, 32, blocks, flags=DECODE_FLAGS(kvx))
         ws = torch.zeros(max(att.workspace_bytes(batch, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
         reps, replays = max(sets, 16), max(3, min(args.steps, 20))
 
@@ -377,7 +385,7 @@ def bench_attention(args, torch, np, kvx, dev, hbm_peak):
         q = (torch.randn(batch, 64, 128, device=dev) * 0.5).to(torch.bfloat16)
         out = torch.empty(batch, 64, 128, dtype=torch.float32, device=dev)
         kv_bytes = batch * c70["ctx"] * 2 * c70["kv_heads"] * c70["head_dim"] * 2
-        att = kvx.Attention(layout, 64, blocks70)
+        att = kvx.Attention(layout, 64, blocks70, flags=DECODE_FLAGS(kvx))
         ws = torch.zeros(max(att.workspace_bytes(batch, c70["ctx"]), 1), dtype=torch.uint8, device=dev)
         t = graph_time_ms(torch, lambda i: att(pool, tables[i % sets], ctx, q, out, batch, c70["ctx"], ws),
                           max(sets, 8), max(3, min(args.steps, 20)))
@@ -417,7 +425,7 @@ def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
     ctx = torch.full((B,), cfg["ctx"], dtype=torch.int32, device=dev)
     q = (torch.randn(B, 32, 128, device=dev) * 0.5).to(torch.bfloat16)
     out = torch.empty(B, 32, 128, dtype=torch.float32, device=dev)
-    att = kvx.Attention(layout, 32, blocks)
+    att = kvx.Attention(layout, 32, blocks, flags=DECODE_FLAGS(kvx))
     ws = torch.zeros(max(att.workspace_bytes(B, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
 
     n = L * blocks
@@ -431,7 +439,7 @@ def bench_overlap(args, torch, np, kvx, dev, hbm_peak):
     q1 = q[:1].contiguous()
     out1 = torch.empty(1, 32, 128, dtype=torch.float32, device=dev)
     ctx1 = ctx[:1].contiguous()
-    att1 = kvx.Attention(layout, 32, blocks)
+    att1 = kvx.Attention(layout, 32, blocks, flags=DECODE_FLAGS(kvx))
     ws1 = torch.zeros(max(att1.workspace_bytes(1, cfg["ctx"]), 1), dtype=torch.uint8, device=dev)
     mig_tables = [dst[l * blocks:(l + 1) * blocks].view(1, blocks).contiguous() for l in range(L)]
     torch.cuda.synchronize()
@@ -955,7 +963,7 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
         ctx_t = torch.full((B,), ctx, dtype=torch.int32, device=dev)
         q = (torch.randn(B, hq, 128, device=dev) * 0.5).to(torch.bfloat16)
         out = torch.empty(B, hq, 128, dtype=torch.float32, device=dev)
-        att = kvx.Attention(layout, hq, blocks)
+        att = kvx.Attention(layout, hq, blocks, flags=DECODE_FLAGS(kvx))
         ws = torch.zeros(max(att.workspace_bytes(B, ctx), 1), dtype=torch.uint8, device=dev)
 
     def decode(st):
@@ -1096,7 +1104,7 @@ def bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_
     ctx_t = torch.full((1,), ctx, dtype=torch.int32, device=dev)
     q = (torch.randn(1, 64, 128, device=dev) * 0.5).to(torch.bfloat16)
     out = torch.empty(1, 64, 128, dtype=torch.float32, device=dev)
-    att = kvx.Attention(layout, 64, blocks)
+    att = kvx.Attention(layout, 64, blocks, flags=DECODE_FLAGS(kvx))
     ws = torch.zeros(max(att.workspace_bytes(1, ctx), 1), dtype=torch.uint8, device=dev)
 
     def send(step=None, timing=None):

@@ -85,7 +85,16 @@ typedef struct {
   int32_t num_splits;  /* split-K over context; 0 = auto                  */
   float scale;         /* softmax scale; 0 = 1/sqrt(head_dim)             */
   int32_t split_merge; /* KVX_MERGE_*: how split-K partials are combined  */
+  int32_t flags;       /* KVX_ATTN_* bits                                  */
 } kvx_attn_params;
+
+/* The caller guarantees that, in the stream, the kernel launched just before
+ * this one writes neither the block tables, nor ctx_lens, nor any page other
+ * than the one holding position ctx_lens[b] - 1 (true for a decode step,
+ * which only appends its token): the block table and each warp's first
+ * pages are then fetched before waiting on that kernel (programmatic
+ * dependent launch), overlapping its tail. */
+#define KVX_ATTN_EARLY_PREFETCH 1
 
 /* Split-K merge strategies (both in-kernel, one launch). AUTO picks CLUSTER
  * when the splits of each (request, kv head) fit one thread-block cluster

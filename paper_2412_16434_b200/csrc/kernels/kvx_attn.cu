@@ -150,6 +150,7 @@ struct AttnArgs {
   float* part_ml;     // [B][Hq][S][2]
   uint32_t* arrivals; // [B][H] split counters; zero between launches
   int cluster_merge;  // 1: the splits of a (request, kv head) form one cluster; merge over DSMEM
+  int early_prefetch; // KVX_ATTN_EARLY_PREFETCH: table + first pages before griddepcontrol.wait
   int heads;          // kv heads
   int group;          // q heads per kv head
   int max_blocks;
@@ -190,9 +191,14 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   // Programmatic dependent launch: this CTA may be resident before the
   // previous kernel on the stream (e.g. the prior layer, or the append of
   // this step's K/V) has finished; everything we read may be its output, so
-  // wait here — what overlaps is launch, rasterisation and CTA setup.
+  // wait here — what overlaps is launch, rasterisation and CTA setup. With
+  // KVX_ATTN_EARLY_PREFETCH the caller promises that the block tables,
+  // ctx_lens and every page except the one holding position ctx-1 are not
+  // written by that kernel (a decode step only appends its token), so the
+  // table and each warp's first pages are fetched before the wait.
+  const bool early = a.early_prefetch != 0;
   KVX_TRACE(0);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
   KVX_TRACE(1);
   const int ctx = a.ctx_lens[b];
   const int n_pages = (ctx + kT - 1) / kT;
@@ -201,10 +207,9 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   const int p_end = min(n_pages, p_begin + per_split);
   const uint32_t* table = a.tables + static_cast<uint64_t>(b) * a.max_blocks;
   const int hq0 = h * a.group;
-  // Q as mma A fragments (issued first: its latency overlaps the table read)
-  // Rows = the group's query heads, zero-padded to 16.
+  // Q as mma A fragments. Rows = the group's query heads, zero-padded to 16.
   uint32_t qa[kD / 16][4];
-  {
+  auto load_q = [&]() {
     const int r0 = lane >> 2, c = (lane & 3) * 2;
     const uint16_t* q0 = a.q + (static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r0) * kD;
     const uint16_t* q8 = q0 + 8 * kD;
@@ -216,7 +221,8 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
       qa[kk][2] = v0 ? *reinterpret_cast<const uint32_t*>(q0 + kk * 16 + c + 8) : 0u;
       qa[kk][3] = v8 ? *reinterpret_cast<const uint32_t*>(q8 + kk * 16 + c + 8) : 0u;
     }
-  }
+  };
+  if (!early) load_q();  // issued first: its latency overlaps the table read
 
   // Stage this CTA's slice of the block table once (one coalesced read
   // instead of a dependent global load in front of every page fetch).
@@ -226,28 +232,6 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     s_pages[i] = page;
   }
   __syncthreads();
-  if (a.new_k != nullptr && p_begin < p_end && p_end == n_pages) {
-    // Fused append (the decode step's append_blocks(1), kvstore.cpp:202-271 /
-    // engine.cpp:132-166): this CTA streams the request's last page, so it
-    // writes this step's K and V row of kv head h into their slot first;
-    // no other CTA reads that page, and the barrier below makes the rows
-    // visible to this CTA's page loads.
-    if (threadIdx.x < 32) {
-      const int t = ctx - 1, slot = t - (n_pages - 1) * kT;
-      uint8_t* page = const_cast<uint8_t*>(a.pool) + static_cast<uint64_t>(s_pages[n_pages - 1 - p_begin]) * a.page_bytes;
-      const int kv = threadIdx.x >> 4, c = threadIdx.x & 15;  // lanes 0-15: K row, 16-31: V row (16 x 16 B)
-      const uint16_t* src = (kv ? a.new_v : a.new_k) + (static_cast<uint64_t>(b) * a.heads + h) * kD;
-      uint8_t* dst = page + static_cast<uint64_t>((kv * a.heads + h) * kT + slot) * (kD * 2);
-      reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
-    }
-    __syncthreads();
-  }
-  KVX_TRACE(2);
-
-  float o[kD / 8][4];
-#pragma unroll
-  for (int i = 0; i < kD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_r = -INFINITY, m_r8 = -INFINITY, l_r = 0.f, l_r8 = 0.f;
 
   uint8_t* ring = smem + warp * (kStages * kStageBytes);
   const uint32_t ring_s = smem_u32(ring);
@@ -274,9 +258,47 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
     }
     cp_async_commit();
   };
-
+  // Early prefetch of this warp's first pages unless one of them is the
+  // request's last page (the one this step's token goes into).
+  const int last_i = (n_pages - 1 - my_first) / W;
+  const bool holds_last = my_count > 0 && n_pages - 1 >= my_first && (n_pages - 1 - my_first) % W == 0 &&
+                          last_i < kStages - 1;
+  const bool prefetched = early && !holds_last;
+  if (prefetched) {
 #pragma unroll
-  for (int i = 0; i < kStages - 1; ++i) issue(i);
+    for (int i = 0; i < kStages - 1; ++i) issue(i);
+  }
+  if (early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    load_q();
+  }
+
+  if (a.new_k != nullptr && p_begin < p_end && p_end == n_pages) {
+    // Fused append (the decode step's append_blocks(1), kvstore.cpp:202-271 /
+    // engine.cpp:132-166): this CTA streams the request's last page, so it
+    // writes this step's K and V row of kv head h into their slot first;
+    // no other CTA reads that page, and the barrier below makes the rows
+    // visible to this CTA's page loads.
+    if (threadIdx.x < 32) {
+      const int t = ctx - 1, slot = t - (n_pages - 1) * kT;
+      uint8_t* page = const_cast<uint8_t*>(a.pool) + static_cast<uint64_t>(s_pages[n_pages - 1 - p_begin]) * a.page_bytes;
+      const int kv = threadIdx.x >> 4, c = threadIdx.x & 15;  // lanes 0-15: K row, 16-31: V row (16 x 16 B)
+      const uint16_t* src = (kv ? a.new_v : a.new_k) + (static_cast<uint64_t>(b) * a.heads + h) * kD;
+      uint8_t* dst = page + static_cast<uint64_t>((kv * a.heads + h) * kT + slot) * (kD * 2);
+      reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
+    }
+    __syncthreads();
+  }
+  KVX_TRACE(2);
+  if (!prefetched) {
+#pragma unroll
+    for (int i = 0; i < kStages - 1; ++i) issue(i);
+  }
+
+  float o[kD / 8][4];
+#pragma unroll
+  for (int i = 0; i < kD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r = -INFINITY, m_r8 = -INFINITY, l_r = 0.f, l_r8 = 0.f;
 
   for (int i = 0; i < my_count; ++i) {
     issue(i + kStages - 1);
@@ -814,6 +836,7 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     a.splits = splits;
     a.scale_log2 = scale * kvx::kLog2e;
     a.cluster_merge = plan.cluster ? 1 : 0;
+    a.early_prefetch = (params->flags & KVX_ATTN_EARLY_PREFETCH) ? 1 : 0;
     if (splits > 1 && !plan.cluster) {
       const uint64_t rows = static_cast<uint64_t>(batch) * Hq;
       if (!d_workspace || workspace_bytes < kvx::workspace_for(batch, Hq, H, splits))

@@ -17,6 +17,7 @@ F32, BF16 = 0, 1
 FILL_BITS, FILL_VALUES = 0, 1
 COPY_AUTO, COPY_SM, COPY_TMA, COPY_CE = 0, 1, 2, 3
 MERGE_AUTO, MERGE_GLOBAL, MERGE_CLUSTER = 0, 1, 2
+ATTN_EARLY_PREFETCH = 1
 
 
 class KvxError(RuntimeError):
@@ -37,7 +38,7 @@ class BlockTag(C.Structure):
 
 class AttnParams(C.Structure):
     _fields_ = [("num_q_heads", C.c_int32), ("max_blocks", C.c_int32), ("num_splits", C.c_int32),
-                ("scale", C.c_float), ("split_merge", C.c_int32)]
+                ("scale", C.c_float), ("split_merge", C.c_int32), ("flags", C.c_int32)]
 
 
 _LIB: Optional[C.CDLL] = None
@@ -281,9 +282,11 @@ class Attention:
     num_splits: int = 0
     scale: float = 0.0
     split_merge: int = MERGE_AUTO
+    flags: int = 0  # ATTN_EARLY_PREFETCH: decode-step contract (see include/kvx.h)
 
     def params(self) -> AttnParams:
-        return AttnParams(self.num_q_heads, self.max_blocks, self.num_splits, self.scale, self.split_merge)
+        return AttnParams(self.num_q_heads, self.max_blocks, self.num_splits, self.scale, self.split_merge,
+                          self.flags)
 
     def workspace_bytes(self, batch: int, max_ctx: int) -> int:
         p = self.params()

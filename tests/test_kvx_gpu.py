@@ -198,6 +198,41 @@ def test_device_signal_orders_streams(dev):
         kvx.signal_write(flag.data_ptr() + 2, 1, prod)  # misaligned flag
 
 
+@pytest.mark.parametrize("batch,ctx", [(1, 8192), (3, 1000), (16, 4096)])
+def test_early_prefetch_is_bit_identical(dev, batch, ctx):
+    """KVX_ATTN_EARLY_PREFETCH (table + first pages fetched before the PDL
+    wait) changes timing only: back-to-back launches — plain and fused-append
+    steps — give the same outputs and pool bytes as without it."""
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    mb = (ctx + 15) // 16
+    pages = batch * mb + 4
+    rng = np.random.default_rng(batch)
+    tables = to_dev(rng.permutation(pages)[:batch * mb].astype(np.int32).reshape(batch, mb), dev)
+    lens = to_dev(np.full(batch, ctx, np.int32) - rng.integers(0, 16, batch).astype(np.int32), dev)
+    ids = torch.arange(pages, dtype=torch.int32, device=dev)
+    tags = torch.stack([ids * 0 + 2, ids * 0, ids], -1).contiguous()
+    q = torch.randn(batch, 32, 128, device=dev).to(torch.bfloat16)
+    nk = torch.randn(batch, 8, 128, device=dev).to(torch.bfloat16)
+    results = []
+    for flags in (0, kvx.ATTN_EARLY_PREFETCH):
+        pool = kvx.Pool(pages, pb, device=0)
+        kvx.fill_pages(pool, ids, tags, pages, 3, layout, kvx.FILL_VALUES)
+        att = kvx.Attention(layout, 32, mb, flags=flags)
+        ws = torch.zeros(max(att.workspace_bytes(batch, ctx), 1), dtype=torch.uint8, device=dev)
+        outs = [torch.empty(batch, 32, 128, dtype=torch.float32, device=dev) for _ in range(4)]
+        for i, o in enumerate(outs):  # back to back on one stream: PDL overlaps consecutive launches
+            if i % 2:
+                att(pool, tables, lens, q, o, batch, ctx, ws, new_k=nk, new_v=nk)
+            else:
+                att(pool, tables, lens, q, o, batch, ctx, ws)
+        torch.cuda.synchronize()
+        results.append((outs, pool.as_tensor().clone()))
+    for a, b in zip(results[0][0], results[1][0]):
+        assert torch.equal(a, b)
+    assert torch.equal(results[0][1], results[1][1])
+
+
 def test_attention_rejects_context_beyond_the_table(dev):
     """max_ctx larger than a block-table row could read past it: refused."""
     layout = LLAMA8B

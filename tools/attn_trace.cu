@@ -6,7 +6,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude \
 //     tools/attn_trace.cu paper_2412_16434_b200/csrc/kernels/kvx_pool.cu \
 //     paper_2412_16434_b200/csrc/kernels/kvx_copy.cu -lcuda -o build/attn_trace
-//   build/attn_trace BATCH CTX [SPLITS [MERGE [Q_HEADS]]]   (Q_HEADS 32: Llama-3.1-8B, 64: 70B)
+//   build/attn_trace BATCH CTX [SPLITS [MERGE [Q_HEADS [FLAGS]]]]   (Q_HEADS 32: Llama-3.1-8B, 64: 70B; FLAGS 1 = early prefetch)
 #include <cstdint>
 __device__ unsigned long long kvx_attn_trace[32 * 65536];
 #define KVX_ATTN_TRACE 1
@@ -68,7 +68,8 @@ int main(int argc, char** argv) {
   cudaMemcpy(d_q, q.data(), q.size() * 2, cudaMemcpyHostToDevice);
   float* d_out;
   cudaMalloc(&d_out, q.size() * 4);
-  kvx_attn_params prm{Hq, blocks, splits_req, 0.f, merge};
+  const int flags = argc > 6 ? atoi(argv[6]) : 0;  // KVX_ATTN_* (1 = early prefetch)
+  kvx_attn_params prm{Hq, blocks, splits_req, 0.f, merge, flags};
   const uint64_t ws_bytes = std::max<uint64_t>(16, kvx_decode_attention_workspace(&lay, &prm, batch, ctx));
   void* d_ws;
   cudaMalloc(&d_ws, ws_bytes);

@@ -46,5 +46,8 @@ for layout in (kvx.PageLayout(8, 128, 16, kvx.BF16), kvx.PageLayout(4, 64, 16, k
         att(pool, tables, lens, q, out, batch, ctx, ws)
         nk = torch.randn(batch, layout.num_kv_heads, layout.head_dim, device=dev).to(elt)
         att(pool, tables, lens, q, out, batch, ctx, ws, new_k=nk, new_v=nk)  # fused append + attend
+        early = kvx.Attention(layout, hq, blocks, num_splits=splits, split_merge=merge, flags=kvx.ATTN_EARLY_PREFETCH)
+        early(pool, tables, lens, q, out, batch, ctx, ws)
+        early(pool, tables, lens, q, out, batch, ctx, ws, new_k=nk, new_v=nk)
 torch.cuda.synchronize()
 print("sanitize driver done")
