@@ -151,6 +151,7 @@ struct AttnArgs {
   uint32_t* arrivals; // [B][H] split counters; zero between launches
   int cluster_merge;  // 1: the splits of a (request, kv head) form one cluster; merge over DSMEM
   int early_prefetch; // KVX_ATTN_EARLY_PREFETCH: table + first pages before griddepcontrol.wait
+  int signal_early;   // cluster launches: launch_dependents after the page loop (else after the merge)
   int heads;          // kv heads
   int group;          // q heads per kv head
   int max_blocks;
@@ -390,10 +391,11 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   KVX_TRACE(4);
   KVX_TRACE_IF(lane == 0, 16 + warp);  // per-warp loop end (slots 16..16+W-1)
   // All our global reads of the pool are done: let the next kernel's CTAs
-  // start launching into SMs as ours drain. Cluster launches signal only at
-  // the very end (below): dependents placed while these clusters still hold
-  // their SMs fragment the GPCs and the next launch loses co-residence.
-  if (!a.cluster_merge) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // start launching into SMs as ours drain. Cluster launches with many CTAs
+  // each streaming a long slice signal only at the very end (below): there,
+  // dependents resident this early cost more than their early start gains
+  // (host-side choice, signal_early; profiles/attn_trace/r01_cluster_signal.log).
+  if (!a.cluster_merge || a.signal_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Full row sums across the 4 lanes sharing a row.
   l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
       a.out[(static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
     }
     KVX_TRACE(6);
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (!a.signal_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
   for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
@@ -837,6 +839,18 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     a.scale_log2 = scale * kvx::kLog2e;
     a.cluster_merge = plan.cluster ? 1 : 0;
     a.early_prefetch = (params->flags & KVX_ATTN_EARLY_PREFETCH) ? 1 : 0;
+    {
+      // Measured with early prefetch on (32 / 64 q heads, batch 1-8,
+      // 8K-131K): signalling dependents right after the page loop wins 5-11%
+      // when the grid is small (<= 80 CTAs) or each CTA's slice is short
+      // (<= 256 pages); with ~100+ CTAs each streaming 340+ pages the late
+      // signal is 2-3% better. Without early prefetch the early-resident
+      // dependents only spin and the late signal wins everywhere.
+      const int pages = std::max(1, (max_ctx + kvx::kT - 1) / kvx::kT);
+      const int per_cta = (pages + splits - 1) / splits;
+      const long ctas = static_cast<long>(splits) * H * batch;
+      a.signal_early = (a.early_prefetch && (ctas <= 80 || per_cta <= 256)) ? 1 : 0;
+    }
     if (splits > 1 && !plan.cluster) {
       const uint64_t rows = static_cast<uint64_t>(batch) * Hq;
       if (!d_workspace || workspace_bytes < kvx::workspace_for(batch, Hq, H, splits))
