@@ -87,7 +87,18 @@ __device__ __forceinline__ void item_addr(const MoveArgs& a, uint64_t item, cons
 
 // LDG.128 / STG.128: every thread issues kVecUnroll independent loads before
 // its stores, so one 256-thread CTA keeps 16 KiB in flight.
+// Both movers are launched with programmatic dependent launch: the next
+// kernel in the stream may be scheduled as soon as this grid starts (it
+// waits in griddepcontrol.wait for our completion before touching memory),
+// and this grid's wait covers whatever wrote our sources. Hides the launch
+// gap between back-to-back moves (pack -> unpack, per-layer migrations).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kVecThreads) page_move_vec(MoveArgs a) {
+  pdl_enter();
   const uint64_t items = a.n_pages * a.chunks_per_page;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint8_t* s8;
@@ -115,6 +126,7 @@ __global__ void __launch_bounds__(kVecThreads) page_move_vec(MoveArgs a) {
 __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kBulkMaxStages];
+  pdl_enter();
   const int S = a.stages;
   const uint32_t slot = a.chunk_bytes;
   if (threadIdx.x != 0) return;
@@ -152,6 +164,22 @@ __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
   bulk_wait<0>();
 }
 
+// Launch with programmatic stream serialization (PDL).
+template <typename Kernel>
+void launch_pdl(Kernel kernel, unsigned grid, unsigned block, uint32_t smem, cudaStream_t stream, const MoveArgs& a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 // AUTO picks the TMA bulk mover when both sides are in this GPU's HBM (measured
 // faster: ~95% vs ~88% of the copy roofline, profiles/), and the SM vector
 // mover for peer (NVLink) or mapped-host (PCIe) endpoints.
@@ -186,14 +214,14 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
     unsigned grid =
         static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * geo.ctas_per_sm));
     if (max_ctas && grid > max_ctas) grid = max_ctas;
-    page_move_bulk<<<grid, 32, smem, stream>>>(a);
+    launch_pdl(page_move_bulk, grid, 32, smem, stream, a);
   } else if (mode == KVX_COPY_SM) {
     a.chunk_bytes = kVecChunk;
     a.chunks_per_page = static_cast<uint32_t>((a.page_bytes + kVecChunk - 1) / kVecChunk);
     const uint64_t items = a.n_pages * a.chunks_per_page;
     unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * 8));
     if (max_ctas && grid > max_ctas) grid = max_ctas;
-    page_move_vec<<<grid, kVecThreads, 0, stream>>>(a);
+    launch_pdl(page_move_vec, grid, kVecThreads, 0, stream, a);
   } else {
     set_error(std::string(who) + ": unsupported copy mode");
     return KVX_ERR_UNSUPPORTED;
