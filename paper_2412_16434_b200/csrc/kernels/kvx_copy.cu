@@ -270,6 +270,7 @@ __global__ void __launch_bounds__(256) fill_pages_kernel(uint8_t* base, uint64_t
 __global__ void __launch_bounds__(128) append_kv_kernel(uint8_t* base, uint64_t page_bytes, const uint32_t* ids,
                                                         const int32_t* slots, const uint8_t* k, const uint8_t* v,
                                                         int heads, int tokens, int row_bytes) {
+  pdl_enter();  // the attention launched next may prefetch every page but this step's
   const uint64_t i = blockIdx.x;
   uint8_t* page = base + static_cast<uint64_t>(ids[i]) * page_bytes;
   const int slot = slots[i];
@@ -408,9 +409,20 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
   if (row_bytes % 16 != 0) return kvx::fail_arg("kvx_append_kv: head_dim * sizeof(dtype) must be a multiple of 16");
   if (n == 0) return KVX_OK;
   kvx::DeviceGuard guard(pool->device);
-  kvx::append_kv_kernel<<<static_cast<unsigned>(n), 128, 0, kvx::as_stream(stream)>>>(
-      pool->base, pool->page_bytes, d_page_ids, d_slots, static_cast<const uint8_t*>(d_k),
-      static_cast<const uint8_t*>(d_v), layout->num_kv_heads, layout->block_tokens, row_bytes);
+  {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(n));
+    cfg.blockDim = dim3(128);
+    cfg.stream = kvx::as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL, as the movers
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kvx::append_kv_kernel, pool->base, pool->page_bytes, d_page_ids, d_slots,
+                       static_cast<const uint8_t*>(d_k), static_cast<const uint8_t*>(d_v), layout->num_kv_heads,
+                       layout->block_tokens, row_bytes);
+  }
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_append_kv");
   return KVX_OK;
 }
