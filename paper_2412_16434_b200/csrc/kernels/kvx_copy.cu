@@ -87,11 +87,11 @@ __device__ __forceinline__ void item_addr(const MoveArgs& a, uint64_t item, cons
 
 // LDG.128 / STG.128: every thread issues kVecUnroll independent loads before
 // its stores, so one 256-thread CTA keeps 16 KiB in flight.
-// Both movers are launched with programmatic dependent launch: the next
-// kernel in the stream may be scheduled as soon as this grid starts (it
-// waits in griddepcontrol.wait for our completion before touching memory),
-// and this grid's wait covers whatever wrote our sources. Hides the launch
-// gap between back-to-back moves (pack -> unpack, per-layer migrations).
+// The movers can be launched with programmatic dependent launch (launch_pdl,
+// KVX_MOVER_PDL=1): the next kernel in the stream may then be scheduled as
+// soon as this grid starts (it waits in griddepcontrol.wait for our
+// completion before touching memory), and this grid's wait covers whatever
+// wrote our sources. Without the attribute both instructions are no-ops.
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -174,7 +174,12 @@ void launch_pdl(Kernel kernel, unsigned grid, unsigned block, uint32_t smem, cud
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  // Off by default: an early-resident successor mover holds its SM's shared
+  // memory while it waits, which delays decode kernels running beside a
+  // migration (event-gated decode of a migrating session: 577-596 -> 718 us)
+  // for a 3% gain on back-to-back moves alone. KVX_MOVER_PDL=1 turns it on.
+  static const char* env = std::getenv("KVX_MOVER_PDL");
+  attr[0].val.programmaticStreamSerializationAllowed = (env && env[0] == '1') ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, a);
