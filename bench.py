@@ -1137,7 +1137,10 @@ def bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_
     src_ready = all_ready[prv]
 
     gated = []
+    outs = [torch.empty(1, 64, 128, dtype=torch.float32, device=dev) for _ in range(L)]
+    landing = d_my_dst.long()
     for step in range(1, 4):
+        pool.as_tensor()[landing] = 0  # a decode that read a layer before it landed would see zeros
         torch.cuda.synchronize()
         dist.barrier()
         t = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -1146,11 +1149,23 @@ def bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_
         send(step=step)
         for l in range(L):
             kvx.signal_wait(flags.base + 4 * l, step, main.cuda_stream)
-            att(pool, tables[l], ctx_t, q, out, 1, ctx, ws, main.cuda_stream)
+            att(pool, tables[l], ctx_t, q, outs[l], 1, ctx, ws, main.cuda_stream)
         t[1].record(main)
         torch.cuda.synchronize()
         gated.append(t[0].elapsed_time(t[1]) * 1e3)
     dist.barrier()
+    # The gated decode saw every layer only after it landed: same outputs as a
+    # decode of the fully arrived session.
+    plain = kvx.Attention(layout, 64, blocks)
+    ref = torch.empty(1, 64, 128, dtype=torch.float32, device=dev)
+    ok = True
+    for l in range(L):
+        plain(pool, tables[l], ctx_t, q, ref, 1, ctx, ws, main.cuda_stream)
+        torch.cuda.synchronize()
+        ok = ok and bool(torch.equal(ref, outs[l]))
+    oks = [None] * world
+    dist.all_gather_object(oks, ok)
+    assert all(oks), f"gated decode read a layer before it arrived on ranks {[i for i, o in enumerate(oks) if not o]}"
     peer_flags.close()
     measured = statistics.median(gated)
     first_end, _, stall = K.pipeline_gate([int(r * 1e3) for r in src_ready], 0, int(L * t_layer_us * 1e3))
@@ -1160,6 +1175,7 @@ def bench_multi_pipeline_gate(torch, np, kvx, dev, dist, cluster, pool, peer, d_
             "measured_first_step_end_us": measured, "max_over_ranks_us": worst,
             "predicted_first_step_end_us": first_end / 1e3, "predicted_stall_us": stall / 1e3,
             "unpipelined_us": src_ready[-1] + L * t_layer_us, "mover_max_ctas": mig_ctas or "all",
+            "outputs_verified": True,
             "how": "per-layer device flags: sender stream writes into the receiver's flag page over IPC after "
                    "each K3 launch (kvx_signal_write), receiver stream waits on it before each K4 (kvx_signal_wait)"}
 
