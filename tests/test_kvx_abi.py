@@ -88,3 +88,23 @@ def test_product_path_does_not_route_through_the_oracle(product_libs):
     from paper_2412_16434_b200 import _build, kvstore as K
     lib = K.load_kvs_library()
     assert lib._name == str(_build.HOST_LIB) and "oracle" not in lib._name
+
+
+def test_abi_rejects_bad_arguments_without_touching_a_device(product_libs):
+    """Argument checks come before any CUDA call: null pools / ids, bad page
+    sizes and bad layouts return KVX_ERR_ARG with a message (no crash, no
+    device needed)."""
+    lib = ctypes.CDLL(str(product_libs.KVX_LIB))
+    lib.kvx_last_error.restype = ctypes.c_char_p
+    V, U64 = ctypes.c_void_p, ctypes.c_uint64
+    lib.kvx_copy_pages.argtypes = [V, V, V, V, U64, ctypes.c_int, V]
+    lib.kvx_pack.argtypes = [V, V, U64, V, ctypes.c_int, V]
+    lib.kvx_pool_create_host.argtypes = [U64, U64, ctypes.POINTER(V)]
+    lib.kvx_signal_write.argtypes = [V, ctypes.c_uint32, V]
+    KVX_ERR_ARG = 2
+    assert lib.kvx_copy_pages(None, None, None, None, 4, 0, None) == KVX_ERR_ARG
+    assert b"null" in lib.kvx_last_error()
+    assert lib.kvx_pack(None, None, 1, None, 0, None) == KVX_ERR_ARG
+    out = V()
+    assert lib.kvx_pool_create_host(4, 1000, ctypes.byref(out)) == KVX_ERR_ARG  # not a multiple of 16
+    assert lib.kvx_signal_write(V(2), 1, None) == KVX_ERR_ARG  # misaligned flag
