@@ -1,27 +1,32 @@
 #!/usr/bin/env python
 """bench.py — KV migration hot path on B200 (Symphony, arXiv 2412.16434).
 
-Metric (BASELINE.json): "KV migrate GB/s (% HBM/NVLink roofline)".
-`value` = session KV bytes relocated per second, whole job (each byte of the
-session counted once; GB = 1e9 B).
+Metric (BASELINE.json, verbatim): "KV migrate GB/s (% HBM/NVLink roofline);
+requests/s at equal p50 latency". `value` = session KV bytes relocated per
+second, whole job (each byte of the session counted once; GB = 1e9 B); the
+roofline fraction is the `roofline` object; requests/s at equal p50 comes
+from the calibrated serving sweeps in profiles/.
 
 N=1 (config 2, Llama-3.1-8B KV shape @ 8K: 32 layers x 512 pages x 64 KiB =
 1 GiB): one step packs every page of the session (K1, gather by block table
 into the contiguous migration buffer) and unpacks it into a second page
 permutation (K2) — the device half of a layer-wise migration. Inputs are
 1 GiB, larger than the 126 MB L2, so no flush is needed between steps.
-Also reported: the fused page->page mover (K3), the TMA variant, paged decode
-attention (K4) at batch 1/8/64, the end-to-end path through the C ABI with
-pinned HOST buffers (H2D + unpack + pack + D2H, every step), and the CPU
-restatement on the host cores.
+Also reported: the fused page->page mover (K3), the other mover variant,
+paged decode attention (K4: 8B @8K batch 1/8/64, 70B @32K batch 1/4, the
+fused decode step), migration beside decode, the DISK tier as files, `e2e`
+through the store's own API (Symphony's swap: offload A + advised load B
+between pinned HOST and HBM pages, every step) with the raw kvx round trip
+in `detail`, and the CPU restatement on the host cores.
 
 N>1 (config 3, Llama-3.1-70B KV shape @ 32K, ~10.7 GB per session):
 migration-plus-serving. Every rank decodes a batch of 70B @32K requests on
 its main stream while its own session migrates to rank (r+1) % N on a side
 stream, the K3 kernel storing straight into the peer's page pool over NVLink
-(CUDA IPC) — a point-to-point exchange, no collective; weak scaling.
-`--migrate-mode nccl` swaps in pack + ncclSend/ncclRecv + unpack for
-comparison.
+(CUDA IPC) — a point-to-point exchange, no collective; weak scaling. Also the
+layer-wise pipeline gate across GPUs (device-side flags) and a HOST-tier to
+HOST-tier e2e. `--migrate-mode nccl` swaps in pack + ncclSend/ncclRecv +
+unpack for comparison.
 
 `--impl reference` times the reference's CPU path on the host cores: the
 reference KvStore's migration bookkeeping (oracle/_ref, 1 thread, as the
