@@ -30,6 +30,7 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -168,6 +169,7 @@ int main(int argc, char** argv) {
   int zipf_sessions = 0, sharegpt_sessions = 0, users = 64, num_nodes = 2;
   std::int64_t pool_pages = 0;  // --pages: per-node DEVICE / HOST / landing pages (and the store's capacities)
   bool digest = false;          // --digest: hashes of the ledger and records instead of every row
+  std::uint64_t trace_seed = 0; // --seed: base seed of the --zipf / --sharegpt generators (0 = fixed default)
   for (int i = 1; i < argc; ++i) {
     if (!std::strcmp(argv[i], "--zipf") && i + 1 < argc) zipf_sessions = std::atoi(argv[++i]);
     if (!std::strcmp(argv[i], "--sharegpt") && i + 1 < argc) sharegpt_sessions = std::atoi(argv[++i]);
@@ -175,6 +177,7 @@ int main(int argc, char** argv) {
     if (!std::strcmp(argv[i], "--nodes") && i + 1 < argc) num_nodes = std::atoi(argv[++i]);
     if (!std::strcmp(argv[i], "--pages") && i + 1 < argc) pool_pages = std::atoll(argv[++i]);
     if (!std::strcmp(argv[i], "--digest")) digest = true;
+    if (!std::strcmp(argv[i], "--seed") && i + 1 < argc) trace_seed = std::strtoull(argv[++i], nullptr, 10);
     if (!std::strcmp(argv[i], "--shape") && i + 1 < argc && !std::strcmp(argv[++i], "8b")) {
       kLayers = 32;
       kHeads = 8;
@@ -203,8 +206,8 @@ int main(int argc, char** argv) {
     cfg.host_capacity = pool_pages * page;
   }
   cfg.sample_period = ns_from_sec(5);
-  const Trace trace = zipf_sessions > 0      ? zipf_trace(zipf_sessions, users, 505)
-                      : sharegpt_sessions > 0 ? sharegpt_trace(sharegpt_sessions, users, 404)
+  const Trace trace = zipf_sessions > 0      ? zipf_trace(zipf_sessions, users, trace_seed ? trace_seed : 505)
+                      : sharegpt_sessions > 0 ? sharegpt_trace(sharegpt_sessions, users, trace_seed ? trace_seed : 404)
                                               : chat_trace(20260417);
 
 #ifdef WITH_PAYLOAD
