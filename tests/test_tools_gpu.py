@@ -1,5 +1,5 @@
 """The measurement tools keep working (they are what a multi-GPU round runs
-first): the NVLink probe in its same-GPU self-test mode and the PCIe mover
+first) and the C++ example host: the NVLink probe in its same-GPU self-test mode and the PCIe mover
 probe, each verifying every variant bit-exact."""
 import json
 import subprocess
@@ -32,3 +32,17 @@ def test_pcie_mover_probe():
     d = _run([str(ROOT / "tools" / "pcie_mover_probe.py"), "--pages", "1024"])
     assert len(d["variants"]) == 12
     assert all(v.get("verified", False) for v in d["variants"] if "error" not in v)
+
+
+def test_cpp_example_host():
+    """examples/decode_step.cpp drives migrate -> fused decode step through the
+    C ABI alone (no Python, no CUDA headers) and checks fused == two-launch."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = ROOT / "examples" / "decode_step"
+    if not exe.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "examples")], check=True, timeout=300)
+    proc = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert proc.returncode == 0, proc.stdout + proc.stderr
+    assert "bit-identical" in proc.stdout and "identical" in proc.stdout
