@@ -32,6 +32,8 @@ def test_pcie_mover_probe():
     d = _run([str(ROOT / "tools" / "pcie_mover_probe.py"), "--pages", "1024"])
     assert len(d["variants"]) == 12
     assert all(v.get("verified", False) for v in d["variants"] if "error" not in v)
+    assert len(d["bidirectional"]) == 6
+    assert all(v.get("verified", False) for v in d["bidirectional"] if "error" not in v)
 
 
 def test_cpp_example_host():

@@ -3,7 +3,8 @@ HBM pages to / from scattered pages of a pinned, device-mapped HOST pool —
 copy engines (one descriptor per run of consecutive ids), the SM vector
 mover storing straight into mapped host memory, and the TMA mover — so the
 HOST-tier moves (SwapOut / HostCopy / LoadH2D) can pick the mover that does
-not collapse when free lists are fragmented. Bytes verified.
+not collapse when free lists are fragmented — one direction at a time, then
+both at once (the ceiling for a swap). Bytes verified.
 
 usage: python tools/pcie_mover_probe.py [--pages 16384]
 """
@@ -74,6 +75,48 @@ def main():
                                             "gbs": round(n * pb / (ms * 1e-3) / 1e9, 1), "verified": ok})
                 except Exception as ex:  # noqa: BLE001 — a mover that cannot reach mapped host memory
                     res["variants"].append({"pool": frag, "mover": name, "dir": direction, "error": str(ex)[:200]})
+        # Both directions at once (what a swap — offload one session while
+        # loading another — sees): half the pages go down, half come up, on
+        # two streams; GB/s counts both directions.
+        half = n // 2
+        st2 = torch.cuda.Stream(dev)
+        for name, down_mode, up_mode in (("ce+ce", kvx.COPY_CE, kvx.COPY_CE), ("ce-d2h+sm-h2d", kvx.COPY_CE, kvx.COPY_SM),
+                                         ("sm-d2h+ce-h2d", kvx.COPY_SM, kvx.COPY_CE)):
+            def ids(mode, a, sl):  # host ids for the copy engines, device ids for the SM mover
+                return (np.ascontiguousarray(a[sl]) if mode == kvx.COPY_CE else
+                        torch.from_numpy(np.ascontiguousarray(a[sl]).view(np.int32)).to(dev))
+            down = (ids(down_mode, d_ids, slice(0, half)), ids(down_mode, h_ids, slice(0, half)))
+            up = (ids(up_mode, h_ids, slice(half, n)), ids(up_mode, d_ids, slice(half, n)))
+
+            def both():
+                kvx.copy_pages(dpool, down[0], hpool, down[1], half, down_mode, st)
+                kvx.copy_pages(hpool, up[0], dpool, up[1], n - half, up_mode, st2)
+            try:
+                kvx.fill_pages(dpool, dd, torch.stack([dd * 0, dd * 0, dd], -1).contiguous(), n, 5, layout,
+                               kvx.FILL_BITS)
+                torch.cuda.synchronize(dev)
+                both()
+                torch.cuda.synchronize(dev)
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+                e[0].record(st)
+                st2.wait_event(e[0])
+                for _ in range(3):
+                    both()
+                e[1].record(st2)
+                st.wait_event(e[1])
+                e[2].record(st)
+                torch.cuda.synchronize(dev)
+                ms = e[0].elapsed_time(e[2]) / 3
+                hp = hpool.as_tensor().numpy()
+                dp = dpool.as_tensor()
+                probe = rng.integers(0, n, 64)
+                ok = bool(np.array_equal(hp[h_ids[probe]],
+                                         dp[torch.from_numpy(d_ids[probe].astype(np.int64)).to(dev)].cpu().numpy()))
+                res.setdefault("bidirectional", []).append(
+                    {"pool": frag, "movers": name, "ms": round(ms, 3), "gbs": round(n * pb / (ms * 1e-3) / 1e9, 1),
+                     "verified": ok})
+            except Exception as ex:  # noqa: BLE001
+                res.setdefault("bidirectional", []).append({"pool": frag, "movers": name, "error": str(ex)[:200]})
     print(json.dumps(res))
     return 0
 
