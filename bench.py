@@ -912,9 +912,28 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
 
     peer = None
     if args.migrate_mode == "p2p":
-        peers = cluster.exchange_pool_handles(dist, rank, pool.ipc_export(), 2 * n, pb)
-        peer = kvx.Pool.ipc_open(peers[nxt].handle, peers[nxt].num_pages, pb, dev.index)
+        # Every rank opens its receiver's pool over CUDA IPC; if any rank
+        # cannot (no peer access between these GPUs), all ranks agree to run
+        # the NCCL path instead and the JSON says why.
+        err = None
+        try:
+            peers = cluster.exchange_pool_handles(dist, rank, pool.ipc_export(), 2 * n, pb)
+            if os.environ.get("BENCH_FAIL_IPC_RANK") == str(rank):  # test hook for the fallback below
+                raise RuntimeError("peer open refused (BENCH_FAIL_IPC_RANK)")
+            peer = kvx.Pool.ipc_open(peers[nxt].handle, peers[nxt].num_pages, pb, dev.index)
+        except Exception as e:  # noqa: BLE001 — reported, and the bench continues over NCCL
+            err = f"rank {rank}: {e}"[:200]
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        errs = [e for e in errs if e]
+        if errs:
+            if peer is not None:
+                peer.close()
+            peer = None
+            args.migrate_mode = "nccl"
+            args.p2p_unavailable = errs[0]
 
+    if args.migrate_mode == "p2p":
         def migrate(st, src=d_src, dst=d_peer_dst):
             for l in range(L):
                 kvx.copy_pages(pool, src[sl[l]], peer, dst[sl[l]], blocks, mode, st.cuda_stream,
@@ -1462,6 +1481,8 @@ def main():
             if res["e2e"] is not None:
                 line["e2e"] = res["e2e"]
             line["config"]["migrate_mode"] = args.migrate_mode
+            if getattr(args, "p2p_unavailable", None):
+                line["config"]["p2p_unavailable"] = args.p2p_unavailable
         if world == 1:
             line["e2e"] = res["e2e"]
             line["decode_attention"] = res["attention"]

@@ -24,27 +24,34 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+@pytest.mark.parametrize("mode", ["p2p", "nccl", "p2p-refused"])
 def test_two_process_migration_plus_serving_on_one_gpu(mode):
     """p2p: K3 stores into the peer process's pool (IPC). nccl: the
     comparison path (pack, send/recv, unpack) — here over gloo with host
     staging, since NCCL refuses two ranks on one GPU. Both run a decode batch
-    beside the migration and verify what landed bit for bit."""
+    beside the migration and verify what landed bit for bit. p2p-refused: one
+    rank cannot open its peer's pool, so both agree to migrate over the
+    collective path instead and the line says why."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3",
-           "--warmup", "3", "--same-device", "--dist-backend", "gloo", "--layers", "2", "--migrate-mode", mode,
+           "--warmup", "3", "--same-device", "--dist-backend", "gloo", "--layers", "2", "--migrate-mode",
+           mode.split("-")[0],
            "--serve-batch", "2"]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
-                          env={**os.environ, "OMP_NUM_THREADS": "1"})
+                          env={**os.environ, "OMP_NUM_THREADS": "1",
+                               **({"BENCH_FAIL_IPC_RANK": "1"} if mode == "p2p-refused" else {})})
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-5000:]
     lines = [ln for ln in proc.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, proc.stdout
     res = json.loads(lines[0])
     assert res["n_gpus"] == 2 and res["value"] > 0
     assert res["roofline"]["bound"] == "nvlink"
+    if mode == "p2p-refused":
+        assert res["config"]["migrate_mode"] == "nccl" and "rank 1" in res["config"]["p2p_unavailable"]
+        mode = "nccl"
     assert res["config"]["layers"] == 2 and res["config"]["migrate_mode"] == mode
     sv = res["serving"]
     assert sv["decode_steps_per_migration"] >= 1 and sv["decode_step_ms_alone"] > 0
