@@ -310,7 +310,7 @@ def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0, merge=kvx.MERGE
     return out.cpu().numpy().astype(np.float64), expect
 
 
-@pytest.mark.parametrize("ctx_lens", [[384], [1, 17, 200, 384], [16, 33]])
+@pytest.mark.parametrize("ctx_lens", [[384], [1, 17, 200, 384], [16, 33], [0, 17, 0]])
 def test_attention_tiny_fp32(dev, ctx_lens):
     got, ref = _attention_case(dev, TINY, 8, ctx_lens)
     assert np.all(np.abs(got - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref))), np.abs(got - ref).max()
@@ -320,6 +320,7 @@ def test_attention_tiny_fp32(dev, ctx_lens):
 @pytest.mark.parametrize("hq,ctx_lens,splits", [
     (32, [8192], 0), (32, [1, 15, 16, 17, 500, 1031], 0), (64, [4096, 33], 0), (8, [700], 1),
     (32, [3000, 2999, 64], 7), (128, [257], 0), (32, [8192] * 8, 0),
+    (32, [0, 300, 0], 0), (32, [0, 4096], 5),  # empty requests (a session with no tokens yet) -> zeros
 ])
 def test_attention_bf16_d128(dev, hq, ctx_lens, splits, merge):
     got, ref = _attention_case(dev, LLAMA8B, hq, ctx_lens, splits, seed=len(ctx_lens) + hq, merge=merge)
@@ -330,7 +331,7 @@ def test_attention_bf16_d128(dev, hq, ctx_lens, splits, merge):
 
 @pytest.mark.parametrize("hq,ctx_lens,splits", [
     (32, [8192], 16), (32, [8192], 2), (32, [5000, 16], 9), (32, [100], 16), (64, [1, 2, 3, 4], 4),
-    (4, [16 * 1024 * 16], 16),
+    (4, [16 * 1024 * 16], 16), (32, [0, 5000, 0], 4),
 ])
 def test_attention_cluster_merge(dev, hq, ctx_lens, splits):
     """Split-K partials merged over DSMEM inside a thread-block cluster
