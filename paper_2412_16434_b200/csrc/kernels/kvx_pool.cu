@@ -473,7 +473,7 @@ int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream) {
     cap.store(can_flush, std::memory_order_relaxed);
   }
   can_flush = can_flush == 2;
-  const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+  const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? static_cast<unsigned>(CU_STREAM_WAIT_VALUE_FLUSH) : 0u);
   const CUresult r = wait_value(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value, flags);
   return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_wait");
 }
