@@ -126,6 +126,11 @@ int kvx_pool_create_host(uint64_t num_pages, uint64_t page_bytes, kvx_pool** out
 int kvx_pool_create_file(const char* path, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
 /* 1 if the pool's file was opened with O_DIRECT, 0 if buffered, -1 if not a file pool. */
 int kvx_pool_file_direct(const kvx_pool* pool);
+/* The sticky errno of the first failed read/write on a file pool (0: none,
+ * or not a file pool). File I/O runs as host callbacks in stream order, so a
+ * failure does not fail the stream: callers that install pages after a sync
+ * (NodePayload's DISK-lane applies) check this first. */
+int kvx_pool_io_error(const kvx_pool* pool);
 /* Wraps caller-owned device memory (not freed by kvx_pool_destroy). */
 int kvx_pool_wrap(int device, void* base, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out);
 int kvx_pool_destroy(kvx_pool* pool);
@@ -170,6 +175,13 @@ int kvx_stream_wait_event(void* stream, void* event);
  * (pipeline_gate, kvstore.cpp:46-59) across GPUs. */
 int kvx_signal_write(void* d_flag, uint32_t value, void* stream);
 int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream);
+/* 1 if the device of `stream` can flush remote writes at a wait
+ * (cudaDevAttrCanFlushRemoteWrites), 0 if not, -1 on error. kvx_signal_wait
+ * requests the flush on the stream's device when available; without it the
+ * writer's system-scope barrier is the only ordering of the peer's data
+ * before the flag, and callers should report a gate built on it as
+ * unverified (or hand off through an event / the host). */
+int kvx_signal_flush_supported(void* stream);
 
 /* ---- page movement (K1-K3) ---------------------------------------------- */
 /* dst[i * page_bytes ...] = page(ids[i]) for i < n. ids in device memory. */
@@ -208,7 +220,12 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
  * partials plus per-(request, kv head) arrival counters for the GLOBAL merge;
  * it must be zero-filled before its first use, and every launch leaves the
  * counters zeroed again (the last split of each group merges all splits
- * in-kernel). The CLUSTER merge does not touch it. */
+ * in-kernel). The CLUSTER merge does not touch it.
+ * Preconditions: 0 <= ctx_lens[b] <= max_ctx <= max_blocks * block_tokens
+ * for every request, every table entry < the pool's page count, and
+ * 0 <= num_splits <= 256. Host-checkable ones return KVX_ERR_ARG; a device
+ * table or ctx_lens entry that breaks them traps the kernel (the stream
+ * fails with a CUDA error) rather than reading or writing out of bounds. */
 uint64_t kvx_decode_attention_workspace(const kvx_page_layout* layout, const kvx_attn_params* params,
                                         int32_t batch, int32_t max_ctx);
 int kvx_decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* params,

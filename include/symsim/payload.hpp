@@ -194,6 +194,7 @@ class NodePayload final : public TierBackend {
   void move_now(std::uint32_t session, std::uint16_t layer, Tier tier, BlockEvent why,
                 const std::vector<std::uint32_t>& blocks);
   std::uint32_t* device_ids(Lane& lane, const std::vector<std::uint32_t>& ids, int slot);
+  void check_file_io() const;
 
   PayloadCluster* cluster_;
   int node_;
@@ -214,7 +215,11 @@ class NodePayload final : public TierBackend {
   std::uint64_t moved_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   // free-running state
   std::unordered_map<std::uint64_t, InFlight> inflight_;        // by transfer id
-  std::unordered_map<std::uint64_t, std::uint64_t> inflight_by_block_;  // key*4+tier -> transfer id
+  struct InFlightSlot {
+    std::uint64_t id;      // transfer
+    std::uint32_t index;   // position of the block in that transfer's InFlight lists
+  };
+  std::unordered_map<std::uint64_t, InFlightSlot> inflight_by_block_;  // key*4+tier -> slot
   std::uint64_t applying_ = 0;
   bool applying_valid_ = false;
   std::uint64_t apply_wait_ns_ = 0;

@@ -266,13 +266,10 @@ bool NodePayload::inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_
     if (t == exclude_tier) continue;
     const auto it = inflight_by_block_.find(key(s, l, b) * 4 + t);
     if (it == inflight_by_block_.end()) continue;
-    const InFlight& f = inflight_.at(it->second);
-    for (std::size_t i = 0; i < f.blocks.size(); ++i)
-      if (f.blocks[i] == b) {
-        *page = f.pages[i];
-        *event = f.event;
-        return true;
-      }
+    const InFlight& f = inflight_.at(it->second.id);
+    *page = f.pages[it->second.index];  // the slot recorded at posting: O(1)
+    *event = f.event;
+    return true;
   }
   return false;
 }
@@ -333,8 +330,11 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
       kvx_pool* from = src_node.pools_[sp];
       kvx_pool* to = pools_[dp];
       const bool on_device = (sp == kDevicePool || sp == kLandingPool) && (dp == kDevicePool || dp == kLandingPool);
-      const bool file_hop = !opts_.disk_path.empty() && (sp == kDiskPool || dp == kDiskPool) &&
-                            (sp == kDevicePool || sp == kLandingPool || dp == kDevicePool || dp == kLandingPool);
+      // A file pool on either side (the source node's DISK copy may be a file
+      // even when ours is not) with HBM on the other goes through a bounce.
+      const bool file_side = kvx_pool_file_direct(from) >= 0 || kvx_pool_file_direct(to) >= 0;
+      const bool hbm_side = sp == kDevicePool || sp == kLandingPool || dp == kDevicePool || dp == kLandingPool;
+      const bool file_hop = file_side && hbm_side;
       if (on_device) {
         const std::uint32_t* ds = runner.device_ids(L, s_ids, 0);
         const std::uint32_t* dd = runner.device_ids(L, d_ids, 1);
@@ -420,10 +420,13 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
   applying_valid_ = false;
   std::vector<bool> used(f.blocks.size(), false);
   std::vector<std::uint32_t> missing;
+  // f.blocks ascends (posted over block_lo..block_hi in order), so each
+  // gained block is found by bisection: O(n log n) per layer, not O(n^2)
+  // (2,048-block layers at Llama-3.1-70B @32K).
   for (std::uint32_t b : blocks) {
-    std::size_t i = 0;
-    while (i < f.blocks.size() && f.blocks[i] != b) ++i;
-    if (i == f.blocks.size()) {
+    const auto pos = std::lower_bound(f.blocks.begin(), f.blocks.end(), b);
+    const std::size_t i = static_cast<std::size_t>(pos - f.blocks.begin());
+    if (pos == f.blocks.end() || *pos != b) {
       missing.push_back(b);  // its source appeared only after scheduling
       continue;
     }
@@ -477,6 +480,22 @@ void NodePayload::move_now(std::uint32_t session, std::uint16_t layer, Tier tier
   }
   issue(src, dst, *src_node, push, {});
   (push ? *src_node : *this).synchronize();
+  check_file_io();
+}
+
+// Sticky file-pool I/O errors (kvx_pool_io_error) of this node and of every
+// node it may read from, raised before a move's pages are installed.
+void NodePayload::check_file_io() const {
+  auto check = [](const NodePayload& n) {
+    const kvx_pool* disk = n.pools_[kDiskPool];
+    if (const int e = disk ? kvx_pool_io_error(disk) : 0)
+      throw std::runtime_error("payload: node " + std::to_string(n.node_) + " disk-tier file I/O failed (errno " +
+                               std::to_string(e) + "); the move's pages are not valid");
+  };
+  check(*this);
+  if (cluster_)
+    for (const NodePayload* n : cluster_->nodes())
+      if (n != this) check(*n);
 }
 
 void NodePayload::tier_lost(std::uint32_t session, std::uint16_t layer, Tier tier,
@@ -545,7 +564,8 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
   void* lane_stream = issue(src, dst, *src_node, push, waits);
   kvx_check(kvx_event_create(&f.event), "event");
   kvx_check(kvx_event_record(f.event, lane_stream), "event record");
-  for (std::uint32_t b : f.blocks) inflight_by_block_[key(tr.session, tr.layer, b) * 4 + t] = tr.id;
+  for (std::size_t i = 0; i < f.blocks.size(); ++i)
+    inflight_by_block_[key(tr.session, tr.layer, f.blocks[i]) * 4 + t] = InFlightSlot{tr.id, static_cast<std::uint32_t>(i)};
   moved_[7] += f.blocks.size() * page_bytes_;  // bytes issued ahead of their apply
   inflight_.emplace(tr.id, std::move(f));
   ++posted_;
@@ -564,11 +584,14 @@ void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
     nvtxRangePop();
     apply_wait_ns_ += now_ns() - t0;
   }
+  // A failed pread / pwrite does not fail the stream (host callback): check
+  // the file pools before the store installs these pages as valid.
+  if (!voided) check_file_io();
   // Later moves touching these pages are ordered by the pages' fences.
   for (std::uint32_t b : f.blocks) {
     const auto k = key(f.session, f.layer, b) * 4 + f.tier;
     const auto jt = inflight_by_block_.find(k);
-    if (jt != inflight_by_block_.end() && jt->second == id) inflight_by_block_.erase(jt);
+    if (jt != inflight_by_block_.end() && jt->second.id == id) inflight_by_block_.erase(jt);
   }
   if (voided) {
     for (const Ref& r : f.pages) release(r);

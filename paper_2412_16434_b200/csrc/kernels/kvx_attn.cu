@@ -51,6 +51,10 @@ constexpr int kStageBytes = 2 * kTileBytes;
 constexpr int smem_bytes(int stages, int warps) { return warps * stages * kStageBytes; }
 constexpr int kMaxPagesPerCta = 1024;  // block-table slice staged in smem (4 KiB)
 constexpr int kMaxClusterSplits = 16;  // DSMEM split merge: one cluster per (request, kv head)
+// Upper bound on split-K (auto and explicit): the GLOBAL merge stages
+// splits x 32 + 16 floats of (m, l) in the page ring's shared memory.
+constexpr int kMaxSplits = 256;
+static_assert(kMaxSplits * 32 + 16 <= 3 * 4 * 8192 / 4, "merge staging must fit the smallest ring");
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Per-CTA timeline stamps (%globaltimer) for tools/attn_trace.cu, which
@@ -202,10 +206,15 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
   KVX_TRACE(1);
   const int ctx = a.ctx_lens[b];
+  // Precondition (kvx.h): 0 <= ctx_lens[b] <= max_ctx <= max_blocks * 16. A
+  // longer request would read past its table row and overflow the staged
+  // slice below: fail loudly instead of corrupting memory.
+  if (ctx < 0 || ctx > a.max_blocks * kT) __trap();
   const int n_pages = (ctx + kT - 1) / kT;
   const int per_split = (n_pages + a.splits - 1) / a.splits;
   const int p_begin = split * per_split;
   const int p_end = min(n_pages, p_begin + per_split);
+  if (p_end - p_begin > kMaxPagesPerCta) __trap();
   const uint32_t* table = a.tables + static_cast<uint64_t>(b) * a.max_blocks;
   const int hq0 = h * a.group;
   // Q as mma A fragments. Rows = the group's query heads, zero-padded to 16.
@@ -604,10 +613,11 @@ __device__ __forceinline__ float ld_elt<uint16_t>(const uint16_t* p) {
 }
 
 template <typename T>
-__global__ void attn_generic(const uint8_t* pool, uint64_t page_bytes, const uint32_t* tables, const int32_t* ctx_lens,
-                             const T* q, float* out, int heads, int group, int head_dim, int block_tokens,
-                             int max_blocks, float scale) {
+__global__ void attn_generic(const uint8_t* pool, uint64_t page_bytes, uint64_t pool_pages, const uint32_t* tables,
+                             const int32_t* ctx_lens, const T* q, float* out, int heads, int group, int head_dim,
+                             int block_tokens, int max_blocks, float scale) {
   const int b = blockIdx.y, hq = blockIdx.x, h = hq / group, lane = threadIdx.x;
+  if (ctx_lens[b] < 0 || ctx_lens[b] > max_blocks * block_tokens) __trap();  // past the table row
   const int per_lane = head_dim / 32;
   float qv[8], acc[8];
   const T* qrow = q + (static_cast<uint64_t>(b) * heads * group + hq) * head_dim;
@@ -619,6 +629,7 @@ __global__ void attn_generic(const uint8_t* pool, uint64_t page_bytes, const uin
   float m = -INFINITY, l = 0.f;
   for (int t = 0; t < ctx; ++t) {
     const uint32_t page = tables[static_cast<uint64_t>(b) * max_blocks + t / block_tokens];
+    if (page >= pool_pages) __trap();  // corrupt block table: fail loudly
     const int slot = t % block_tokens;
     const T* base = reinterpret_cast<const T*>(pool + static_cast<uint64_t>(page) * page_bytes);
     const T* k = base + (static_cast<uint64_t>(h) * block_tokens + slot) * head_dim;
@@ -648,6 +659,7 @@ __global__ void __launch_bounds__(128) append_from_table(uint8_t* pool, uint64_t
   const int b = blockIdx.x;
   const int t = ctx_lens[b] - 1;
   if (t < 0) return;
+  if (t / block_tokens >= max_blocks) __trap();  // past the table row
   const uint32_t page = tables[static_cast<uint64_t>(b) * max_blocks + t / block_tokens];
   if (page >= pool_pages) __trap();
   const int slot = t % block_tokens;
@@ -677,11 +689,11 @@ bool fast_path(const kvx_page_layout* l) {
 int choose_splits(int batch, int heads, int max_ctx, int requested, int sms) {
   const int pages = std::max(1, (max_ctx + kT - 1) / kT);
   const int min_splits = (pages + kMaxPagesPerCta - 1) / kMaxPagesPerCta;
-  if (requested > 0) return std::max(requested, min_splits);
+  if (requested > 0) return std::max(requested, min_splits);  // <= kMaxSplits, checked by the caller
   const int max_splits = std::max(min_splits, pages / (kWarps * 4));
   const long base = std::max(1L, static_cast<long>(batch) * heads);
   int s = std::max(min_splits, static_cast<int>(std::lround(0.65 * sms / static_cast<double>(base))));
-  s = std::max(1, std::min(s, 256));
+  s = std::max(1, std::min(s, kMaxSplits));
   if (s * base > sms && s * base < 2L * sms && pages / s >= 1024) s *= 4;
   return std::max(min_splits, std::min(max_splits, s));
 }
@@ -813,6 +825,8 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
   const cudaStream_t st = kvx::as_stream(stream);
   kvx::DeviceGuard guard(pool->device);
 
+  if (params->num_splits < 0 || params->num_splits > kvx::kMaxSplits)
+    return kvx::fail_arg("kvx_decode_attention: num_splits must be in [0, 256]");
   if (kvx::fast_path(layout) && group <= 16) {
     const int dev = pool->device < 0 ? 0 : pool->device;
     if (int rc = kvx::configure(dev)) return rc;
@@ -909,11 +923,11 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
   }
   dim3 grid(Hq, batch);
   if (layout->dtype == KVX_DTYPE_F32)
-    kvx::attn_generic<float><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, d_block_tables, d_ctx_lens,
+    kvx::attn_generic<float><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, pool->num_pages, d_block_tables, d_ctx_lens,
                                                   static_cast<const float*>(d_q), d_out, H, group, layout->head_dim,
                                                   layout->block_tokens, params->max_blocks, scale);
   else
-    kvx::attn_generic<uint16_t><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, d_block_tables, d_ctx_lens,
+    kvx::attn_generic<uint16_t><<<grid, 32, 0, st>>>(pool->base, pool->page_bytes, pool->num_pages, d_block_tables, d_ctx_lens,
                                                      static_cast<const uint16_t*>(d_q), d_out, H, group,
                                                      layout->head_dim, layout->block_tokens, params->max_blocks,
                                                      scale);

@@ -213,6 +213,11 @@ int kvx_pool_create_file(const char* path, uint64_t num_pages, uint64_t page_byt
 
 int kvx_pool_file_direct(const kvx_pool* pool) { return pool && pool->fd >= 0 ? (pool->direct ? 1 : 0) : -1; }
 
+int kvx_pool_io_error(const kvx_pool* pool) {
+  if (!pool || pool->fd < 0) return 0;
+  return pool->io_errno.load();
+}
+
 int kvx_pool_wrap(int device, void* base, uint64_t num_pages, uint64_t page_bytes, kvx_pool** out) {
   if (!out || !base || num_pages == 0 || page_bytes == 0 || page_bytes % 16 != 0 ||
       reinterpret_cast<uintptr_t>(base) % 16 != 0)
@@ -455,24 +460,43 @@ int kvx_signal_write(void* d_flag, uint32_t value, void* stream) {
   return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_write");
 }
 
+int kvx_signal_flush_supported(void* stream) {
+  // Cached per device: 0 unknown, 1 no, 2 yes.
+  static std::atomic<int> flush_cap[64] = {};
+  int dev = 0;
+  const cudaError_t e = cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &dev);
+  if (e != cudaSuccess) {
+    kvx::fail_cuda(e, "kvx_signal_flush_supported: cudaStreamGetDevice");
+    return -1;
+  }
+  std::atomic<int>& cap = flush_cap[(dev < 0 ? 0 : dev) % 64];
+  int c = cap.load(std::memory_order_relaxed);
+  if (c == 0) {
+    int v = 0;
+    const cudaError_t e2 = cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev);
+    if (e2 != cudaSuccess) {
+      kvx::fail_cuda(e2, "kvx_signal_flush_supported: cudaDevAttrCanFlushRemoteWrites");
+      return -1;
+    }
+    c = v ? 2 : 1;
+    cap.store(c, std::memory_order_relaxed);
+  }
+  return c == 2 ? 1 : 0;
+}
+
 int kvx_signal_wait(const void* d_flag, uint32_t value, void* stream) {
   if (!d_flag || reinterpret_cast<uintptr_t>(d_flag) % 4) return kvx::fail_arg("kvx_signal_wait: need a 4-B aligned flag");
   static WaitValue32 wait_value = nullptr;
   if (!wait_value)
     if (int rc = driver_fn("cuStreamWaitValue32", &wait_value)) return rc;
-  // Per-device "can flush remote writes" (cached: 0 unknown, 1 no, 2 yes).
-  static std::atomic<int> flush_cap[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::atomic<int>& cap = flush_cap[(dev < 0 ? 0 : dev) % 64];
-  int can_flush = cap.load(std::memory_order_relaxed);
-  if (can_flush == 0) {
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev);
-    can_flush = v ? 2 : 1;
-    cap.store(can_flush, std::memory_order_relaxed);
-  }
-  can_flush = can_flush == 2;
+  // The wait runs on the stream's device: FLUSH (outstanding remote writes,
+  // e.g. the peer's K3 stores that preceded the flag, become visible to the
+  // stream's later work) is requested when THAT device supports it. When it
+  // does not, the writer's system-scope barrier (kvx_signal_write) is the
+  // only ordering; kvx_signal_flush_supported() lets callers report such a
+  // gate as unverified or use an event / host handoff instead.
+  const int can_flush = kvx_signal_flush_supported(stream);
+  if (can_flush < 0) return KVX_ERR_CUDA;
   const unsigned flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? static_cast<unsigned>(CU_STREAM_WAIT_VALUE_FLUSH) : 0u);
   const CUresult r = wait_value(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(d_flag), value, flags);
   return r == CUDA_SUCCESS ? KVX_OK : fail_cu(r, "kvx_signal_wait");
