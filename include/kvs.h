@@ -276,9 +276,18 @@ int kvs_payload_pool_of(kvs_payload* p, uint32_t session, uint16_t layer, uint32
 int kvs_payload_bytes_moved(kvs_payload* p, uint64_t* out7);
 /* out[0] = host ns blocked in apply waiting for the GPU (free-running),
  * out[1] = transfers issued at schedule time, out[2..5] = pages of each pool
- * held by moves issued but not yet applied, out[6] = batches that waited on
- * another lane's batch touching the same pages (IN / OUT / PEER lanes). */
+ * held by moves issued but not yet applied, out[6] = page allocations that
+ * had to wait for freed pages still touched by queued batches (quarantine:
+ * a freed page is reused only once every batch queued before the free has
+ * completed). */
 int kvs_payload_stats(kvs_payload* p, uint64_t* out7);
+/* Host ns of the payload's bookkeeping by phase (nested phases counted in
+ * their callers too): [0] transfer_posted (issue at schedule time), [1]
+ * transfer_retired (apply), [2] issue (enqueue of one batch's copies), [4]
+ * id upload, [5] mover launches, [6] batch close (event) — [4..6] inside
+ * [2] — [7] page allocation, and [3] returning quarantined pages to the
+ * free lists (inside [7]). */
+int kvs_payload_host_ns(kvs_payload* p, uint64_t* out8);
 /* Process-wide default: every KvStore constructed afterwards gets a payload
  * node (node_id -> device node_id % num_devices) in cluster `c`, built from
  * `tmpl`. Lets unchanged caller stacks (the reference Simulation) run with
@@ -293,11 +302,29 @@ int kvs_payload_pool(kvs_payload* p, int32_t pool, void** out);
 int kvs_payload_synchronize(kvs_payload* p);
 /* The cudaStream_t of one of the node's lanes: 0 IN (moves landing in HBM),
  * 1 OUT (HBM -> pinned host), 2 DISK (disk-tier reads and writes), 3 PEER
- * (migration pushes into a peer). Callers may order their own work against
- * a lane with events; the payload never waits on caller streams. */
+ * (migration pushes into a peer), 4 FILL (content of created blocks).
+ * Callers may order their own work against a lane with events; the payload
+ * never waits on caller streams. */
 int kvs_payload_stream(kvs_payload* p, int32_t lane, void** out);
 int kvs_set_default_payload(kvs_cluster* c, const kvs_payload_options* tmpl, int32_t num_devices);
 int kvs_cluster_node(kvs_cluster* c, int32_t node_id, kvs_payload** out);
+
+/* ---- serving traffic and latency aggregates (product only;
+ * include/symsim/traffic.hpp). The reference synthesizes closed-loop chat
+ * traffic with typing-time think pauses (workload.cpp:260-311) and reports
+ * means + steady requests/s (report.cpp:65-76); configs 4 and 5 add Poisson
+ * think times, Zipf session popularity and p50 service levels. ---------- */
+/* out[i] = turns of session i under Zipf(s): seeded ranking, rank r gets
+ * max(min_turns, round(scale / r^s)). */
+int kvs_traffic_zipf_turns(uint64_t sessions, double s, double scale, int32_t min_turns, uint64_t seed,
+                           int32_t* out);
+/* n exponential gaps (ns) with mean mean_s seconds. */
+int kvs_traffic_poisson_gaps(uint64_t n, double mean_s, uint64_t seed, int64_t* out);
+/* q-quantile with linear interpolation (numpy default). */
+int kvs_traffic_percentile(const double* values, uint64_t n, double q, double* out);
+/* Highest rps among sweep points with p50 <= slo (0 if none). */
+int kvs_traffic_rps_within_slo(const int32_t* users, const double* rps, const double* p50, uint64_t n, double slo,
+                               double* out);
 
 #ifdef __cplusplus
 }

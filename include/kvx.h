@@ -153,6 +153,9 @@ int kvx_stream_destroy(void* stream);
 int kvx_stream_synchronize(void* stream);
 int kvx_malloc(int device, uint64_t bytes, void** out);
 int kvx_free(void* ptr);
+/* Pinned host memory (staging for async uploads). */
+int kvx_host_alloc(uint64_t bytes, void** out);
+int kvx_host_free(void* ptr);
 /* cudaMemcpyAsync(kind = Default) on `stream`. */
 int kvx_memcpy_async(void* dst, const void* src, uint64_t bytes, void* stream);
 /* Synchronous copy of one page to host memory (verification / debugging). */
@@ -207,6 +210,18 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
 /* ---- contents (K5) ------------------------------------------------------ */
 int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,
                    uint64_t seed, const kvx_page_layout* layout, int fill_mode, void* stream);
+/* Scrub (K5 check): counts into *d_mismatches (device u64, accumulated) the
+ * pages whose bytes differ from the K5 content of their tag — a list of
+ * (page, tag) pairs, or every block of a decode step's block tables
+ * ([num_layers][batch][max_blocks], tag = (sessions[b], layer, block), blocks
+ * past ctx_lens[b] skipped). Page ids outside the pool count as mismatches. */
+int kvx_verify_pages(const kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,
+                     uint64_t seed, const kvx_page_layout* layout, int fill_mode, unsigned long long* d_mismatches,
+                     void* stream);
+int kvx_verify_block_tables(const kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_tables,
+                            const int32_t* d_ctx_lens, const int32_t* d_sessions, int32_t num_layers, int32_t batch,
+                            int32_t max_blocks, uint64_t seed, int fill_mode, unsigned long long* d_mismatches,
+                            void* stream);
 /* For request i: page d_page_ids[i], token slot d_slots[i] (< block_tokens)
  * gets K = d_k[i][H][D], V = d_v[i][H][D] (layout dtype). */
 int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_page_ids,
@@ -244,6 +259,53 @@ int kvx_decode_attention_append(kvx_pool* pool, const kvx_page_layout* layout, c
                                 const uint32_t* d_block_tables, const int32_t* d_ctx_lens, const void* d_q,
                                 const void* d_new_k, const void* d_new_v, float* d_out, int32_t batch,
                                 int32_t max_ctx, void* d_workspace, uint64_t workspace_bytes, void* stream);
+
+/* ---- the decode step around K4 (K6) --------------------------------------
+ * The reference models a serving engine's quanta (prefill_time and
+ * decode_step_time, costmodel.cpp:54-80; Engine::try_start,
+ * engine.cpp:168-262). A kvx_model executes them on the GPU for a
+ * Llama-shaped decoder with random bf16 weights: dense projections on cuBLAS
+ * (library GEMMs), norms / RoPE / SiLU / sampling hand-written, and K4 with
+ * this step's token appended (kvx_decode_attention_append) per layer over the
+ * pages of a kvx_pool. The K/V written into a page is that slot's K5 content
+ * (fill of its (session, layer, block) tag with fill_seed / fill_mode), so
+ * pages stay oracle-checkable. One model may serve several callers (nodes)
+ * but its activations are shared: calls must not overlap in time. */
+typedef struct kvx_model kvx_model;
+typedef struct {
+  int32_t num_layers;   /* 32 (Llama-3.1-8B) */
+  int32_t hidden;       /* 4096 */
+  int32_t num_q_heads;  /* 32 */
+  int32_t num_kv_heads; /* 8 */
+  int32_t head_dim;     /* 128 (required) */
+  int32_t intermediate; /* 14336 */
+  int32_t vocab;        /* 128256 */
+  float rms_eps;        /* 1e-5 */
+  float rope_theta;     /* 500000 */
+} kvx_model_config;
+
+uint64_t kvx_model_weight_bytes(const kvx_model_config* cfg);
+int kvx_model_create(int device, const kvx_model_config* cfg, uint64_t seed, kvx_model** out);
+int kvx_model_destroy(kvx_model* model);
+/* One decode step for `batch` requests (<= 256). d_tables: [num_layers][batch]
+ * [max_blocks] page ids of each request's blocks per layer; d_ctx_lens[b]
+ * tokens including this step's (written at position ctx - 1); d_sessions[b]
+ * the session ids (K5 tags); d_tokens_in[b] the input token ids;
+ * d_tokens_out[b] the greedy samples. layer_waits[layer_wait_offsets[l] ..
+ * layer_wait_offsets[l+1]) are events (host array) the attention of layer l
+ * waits for — loads still landing (NULL: none). Asynchronous on `stream`. */
+int kvx_model_decode_step(kvx_model* model, kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_tables,
+                          const int32_t* d_ctx_lens, const int32_t* d_sessions, const int32_t* d_tokens_in,
+                          int32_t batch, int32_t max_blocks, int32_t max_ctx, uint64_t fill_seed, int32_t fill_mode,
+                          void* const* layer_waits, const int32_t* layer_wait_offsets, int32_t* d_tokens_out,
+                          void* stream);
+/* The dense work of prefilling `tokens` prompt tokens (all projections and
+ * MLPs, 4,096-row passes, LM head of the last token). The prompt's K/V pages
+ * are the store's Created fill; prefill attention is not executed. */
+int kvx_model_prefill(kvx_model* model, int32_t tokens, void* stream);
+/* Timing helpers for hosts without CUDA headers: events with timing. */
+int kvx_timer_create(void** out);
+int kvx_timer_elapsed_ms(void* start, void* stop, float* ms);
 
 #ifdef __cplusplus
 }

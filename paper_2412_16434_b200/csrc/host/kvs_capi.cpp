@@ -400,6 +400,7 @@ int kvs_residency(kvs_store* s, uint32_t session, uint16_t layer, uint32_t block
 #include <mutex>
 
 #include "symsim/payload.hpp"
+#include "symsim/traffic.hpp"
 
 struct kvs_cluster {
   symsim::PayloadCluster cluster;
@@ -488,6 +489,12 @@ int kvs_payload_stats(kvs_payload* p, uint64_t* out7) {
   });
 }
 
+int kvs_payload_host_ns(kvs_payload* p, uint64_t* out8) {
+  return guarded([&] {
+    for (int i = 0; i < symsim::NodePayload::kHostPhases; ++i) out8[i] = p->node->host_ns()[i];
+  });
+}
+
 int kvs_payload_block_table(kvs_payload* p, uint32_t session, uint16_t layer, uint32_t n, uint32_t* out) {
   return guarded([&] {
     if (!p->node->device_block_table(session, layer, n, out))
@@ -543,6 +550,34 @@ int kvs_cluster_node(kvs_cluster* c, int32_t node_id, kvs_payload** out) {
   });
 }
 
+int kvs_traffic_zipf_turns(uint64_t sessions, double s, double scale, int32_t min_turns, uint64_t seed,
+                           int32_t* out) {
+  return guarded([&] {
+    const auto t = symsim::traffic::zipf_turns(sessions, s, scale, min_turns, seed);
+    for (std::size_t i = 0; i < t.size(); ++i) out[i] = t[i];
+  });
+}
+
+int kvs_traffic_poisson_gaps(uint64_t n, double mean_s, uint64_t seed, int64_t* out) {
+  return guarded([&] {
+    const auto g = symsim::traffic::poisson_gaps(n, mean_s, seed);
+    for (std::size_t i = 0; i < g.size(); ++i) out[i] = g[i];
+  });
+}
+
+int kvs_traffic_percentile(const double* values, uint64_t n, double q, double* out) {
+  return guarded([&] { *out = symsim::traffic::percentile(std::vector<double>(values, values + n), q); });
+}
+
+int kvs_traffic_rps_within_slo(const int32_t* users, const double* rps, const double* p50, uint64_t n, double slo,
+                               double* out) {
+  return guarded([&] {
+    std::vector<symsim::traffic::LoadPoint> sweep(n);
+    for (uint64_t i = 0; i < n; ++i) sweep[i] = {users[i], rps[i], p50[i]};
+    *out = symsim::traffic::rps_within_slo(sweep, slo);
+  });
+}
+
 }  // extern "C"
 #else
 #define KVS_NO_PAYLOAD(name, ...)                                        \
@@ -560,11 +595,16 @@ KVS_NO_PAYLOAD(kvs_payload_pages_in_use, kvs_payload*, int32_t, uint64_t*)
 KVS_NO_PAYLOAD(kvs_payload_pool_of, kvs_payload*, uint32_t, uint16_t, uint32_t, int32_t, int32_t*)
 KVS_NO_PAYLOAD(kvs_payload_bytes_moved, kvs_payload*, uint64_t*)
 KVS_NO_PAYLOAD(kvs_payload_stats, kvs_payload*, uint64_t*)
+KVS_NO_PAYLOAD(kvs_payload_host_ns, kvs_payload*, uint64_t*)
 KVS_NO_PAYLOAD(kvs_set_default_payload, kvs_cluster*, const kvs_payload_options*, int32_t)
 KVS_NO_PAYLOAD(kvs_payload_block_table, kvs_payload*, uint32_t, uint16_t, uint32_t, uint32_t*)
 KVS_NO_PAYLOAD(kvs_payload_pool, kvs_payload*, int32_t, void**)
 KVS_NO_PAYLOAD(kvs_payload_synchronize, kvs_payload*)
 KVS_NO_PAYLOAD(kvs_payload_stream, kvs_payload*, int32_t, void**)
 KVS_NO_PAYLOAD(kvs_cluster_node, kvs_cluster*, int32_t, kvs_payload**)
+KVS_NO_PAYLOAD(kvs_traffic_zipf_turns, uint64_t, double, double, int32_t, uint64_t, int32_t*)
+KVS_NO_PAYLOAD(kvs_traffic_poisson_gaps, uint64_t, double, uint64_t, int64_t*)
+KVS_NO_PAYLOAD(kvs_traffic_percentile, const double*, uint64_t, double, double*)
+KVS_NO_PAYLOAD(kvs_traffic_rps_within_slo, const int32_t*, const double*, const double*, uint64_t, double, double*)
 }  // extern "C"
 #endif

@@ -15,6 +15,17 @@
 //   tier_lost    purge / evict / release  kvstore.cpp:388-393, 293-295, 710-736
 // Free-running mode issues each move when the transfer is scheduled
 // (add_transfer, kvstore.cpp:180-185) and completes it at apply.
+//
+// Ordering between lanes, without per-page state on the hot path:
+//   * a page installed as a tier copy is complete (lockstep moves sync; a
+//     free-running move is installed at apply, after its event) — except a
+//     created block, whose fill runs on the FILL lane: readers of a row wait
+//     for the row's newest fill ticket;
+//   * a page still being moved in (posted, not applied) is only read by
+//     moves chained on its event (inflight_source) or by a decode step
+//     (decode_rows returns the event);
+//   * a freed page goes to quarantine until every batch queued before the
+//     free has completed, so no new writer ever races an old reader/writer.
 
 #include "symsim/payload.hpp"
 
@@ -22,6 +33,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -39,7 +51,29 @@ std::uint64_t now_ns() {
           .count());
 }
 
+const char* const kPoolNames[] = {"device", "host", "landing", "disk"};
+
 }  // namespace
+
+// Host time of the payload's bookkeeping, by phase (kvs_payload_host_ns).
+struct NodePayload::HostTimer {
+  std::uint64_t& acc;
+  std::uint64_t t0;
+  explicit HostTimer(std::uint64_t& a) : acc(a), t0(now_ns()) {}
+  ~HostTimer() { acc += now_ns() - t0; }
+};
+
+// node id -> node for one pass (a cluster lookup per node, not per page).
+NodePayload* NodePayload::NodeCache::get(PayloadCluster* cluster, int id) {
+  for (int k = 0; k < n; ++k)
+    if (ids[k] == id) return nodes[k];
+  NodePayload* p = cluster ? cluster->node(id) : nullptr;
+  if (n < 8) {
+    ids[n] = id;
+    nodes[n++] = p;
+  }
+  return p;
+}
 
 // ---------------------------------------------------------------------------
 // cluster registry
@@ -73,7 +107,7 @@ int PayloadCluster::take_source(std::uint32_t session) {
 }
 
 // ---------------------------------------------------------------------------
-// lanes and per-page fences
+// lanes
 
 // Retires completed batches from the front (they complete in ticket order).
 void NodePayload::Lane::retire() {
@@ -101,47 +135,20 @@ void NodePayload::Lane::drain() {
   done = next - 1;
 }
 
-// Make `runner`'s lane wait for every other lane's batch still touching
-// `pages` (reads and writes alike: WAR, RAW and WAW are all covered).
-void NodePayload::wait_fences(NodePayload& runner, int lane, const std::vector<Touch>& pages) {
-  // A lane completes its batches in ticket order, so waiting for the newest
-  // ticket seen per foreign lane covers every page fenced by that lane.
-  std::vector<std::pair<Lane*, std::uint64_t>> need;
-  for (const Touch& t : pages) {
-    const Fence& f = t.first->fence(t.second);
-    if (f.ticket == 0 || (f.node == runner.node_ && f.lane == lane)) continue;  // same stream: ordered
-    NodePayload* owner = f.node == runner.node_ ? &runner
-                         : f.node == node_      ? this
-                         : cluster_             ? cluster_->node(f.node)
-                                                : nullptr;
-    if (!owner) continue;  // that node is gone, and synchronized on its way out
-    Lane* L = &owner->lanes_[f.lane];
-    auto it = std::find_if(need.begin(), need.end(), [L](const auto& e) { return e.first == L; });
-    if (it == need.end())
-      need.emplace_back(L, f.ticket);
-    else
-      it->second = std::max(it->second, f.ticket);
-  }
-  bool waited = false;
-  for (const auto& [L, ticket] : need)
-    if (void* ev = L->event_for(ticket)) {  // nullptr: already complete
-      kvx_check(kvx_stream_wait_event(runner.lanes_[lane].stream, ev), "stream wait");
-      waited = true;
-    }
-  if (waited) ++cross_waits_;
+void* NodePayload::pending_event(NodePayload* node, int lane, std::uint64_t ticket) const {
+  return node ? node->lanes_[lane].event_for(ticket) : nullptr;
 }
 
-// Close the batch just queued on `runner`'s lane: one event, and every page
-// it touched now points at it.
-void NodePayload::set_fences(NodePayload& runner, int lane, const std::vector<Touch>& pages) {
-  Lane& L = runner.lanes_[lane];
+std::uint64_t NodePayload::close_batch(int lane) {
+  const HostTimer timer(host_ns_[kHostClose]);
+  Lane& L = lanes_[lane];
   L.retire();  // keeps the pending list short on lanes nobody waits on
   void* ev = nullptr;
   kvx_check(kvx_event_create(&ev), "event");
   kvx_check(kvx_event_record(ev, L.stream), "event record");
   const std::uint64_t ticket = L.next++;
   L.pending.emplace_back(ticket, ev);
-  for (const Touch& t : pages) t.first->fence(t.second) = Fence{runner.node_, lane, ticket};
+  return ticket;
 }
 
 // ---------------------------------------------------------------------------
@@ -151,10 +158,22 @@ NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOpti
     : cluster_(cluster), node_(node_id), opts_(opts) {
   page_bytes_ = kvx_page_bytes(&opts_.layout);
   if (page_bytes_ == 0) throw std::runtime_error("payload: empty page layout");
-  for (Lane& L : lanes_) kvx_check(kvx_stream_create(opts_.device, &L.stream), "stream");
+  for (Lane& L : lanes_) {
+    kvx_check(kvx_stream_create(opts_.device, &L.stream), "stream");
+    // Upload staging up front: pinned allocations cost milliseconds, not
+    // something to pay inside the first moves.
+    void* p = nullptr;
+    L.ring_cap = std::size_t{4} << 20;
+    kvx_check(kvx_host_alloc(L.ring_cap, &p), "upload ring");
+    L.ring = static_cast<std::uint8_t*>(p);
+    L.d_ids_cap = std::size_t{1} << 16;
+    kvx_check(kvx_malloc(opts_.device, L.d_ids_cap * sizeof(std::uint32_t), &p), "id scratch");
+    L.d_ids = static_cast<std::uint32_t*>(p);
+  }
   const std::uint64_t counts[4] = {opts_.device_pages, opts_.host_pages, opts_.landing_pages, opts_.disk_pages};
   for (int p = 0; p < 4; ++p) {
     if (counts[p] == 0) continue;
+    if (counts[p] > 0x3FFFFFFFull) throw std::runtime_error("payload: a pool holds at most 2^30 pages");
     if (p == kDevicePool || p == kLandingPool)
       kvx_check(kvx_pool_create(opts_.device, counts[p], page_bytes_, &pools_[p]), "device pool");
     else if (p == kDiskPool && !opts_.disk_path.empty())
@@ -162,7 +181,6 @@ NodePayload::NodePayload(PayloadCluster* cluster, int node_id, const PayloadOpti
     else
       kvx_check(kvx_pool_create_host(counts[p], page_bytes_, &pools_[p]), "host pool");
     free_[p].resize(counts[p]);
-    fences_[p].resize(counts[p]);
     // LIFO free list handing out low page ids first.
     for (std::uint64_t i = 0; i < counts[p]; ++i) free_[p][i] = static_cast<std::uint32_t>(counts[p] - 1 - i);
   }
@@ -177,12 +195,13 @@ NodePayload::~NodePayload() {
   }
   for (Lane& L : lanes_)
     if (L.stream) kvx_stream_synchronize(L.stream);
-  for (auto& entry : inflight_) kvx_event_destroy(entry.second.event);
+  for (InFlight& f : flights_) kvx_event_destroy(f.event);
   for (auto*& p : pools_)
     if (p) kvx_pool_destroy(p);
   for (Lane& L : lanes_) {
     L.drain();
-    for (auto* d : L.d_ids) kvx_free(d);
+    kvx_free(L.d_ids);
+    kvx_host_free(L.ring);
     if (L.bounce) kvx_pool_destroy(L.bounce);
     kvx_stream_destroy(L.stream);
   }
@@ -198,25 +217,113 @@ void NodePayload::synchronize() {
 
 std::uint64_t NodePayload::pages_in_use(Pool p) const {
   const std::uint64_t total = pools_[p] ? kvx_pool_num_pages(pools_[p]) : 0;
-  return total - free_[p].size();
+  return total - free_[p].size() - held_[p];
 }
 
 std::uint64_t NodePayload::pages_in_flight(Pool p) const {
   std::uint64_t n = 0;
-  for (const auto& entry : inflight_)
-    for (const Ref& r : entry.second.pages) n += r.pool == p;
+  for (const auto& e : flight_of_)
+    for (const Ref& r : flights_[e.second].pages) n += r.pool == p;
   return n;
 }
 
-std::uint32_t NodePayload::alloc(Pool p) {
-  if (free_[p].empty()) {
-    static const char* const kNames[] = {"device", "host", "landing", "disk"};
-    throw std::runtime_error(std::string("payload: node ") + std::to_string(node_) + " " + kNames[p] +
-                             " pool exhausted");
+// ---------------------------------------------------------------------------
+// free pages and quarantine
+
+void NodePayload::release(const Ref& r) {
+  if (r.pool < 0) return;
+  released_.push_back(r);
+  ++held_[r.pool];
+}
+
+// Closes the group of pages freed so far: they may be reused once every
+// batch queued until now, on any lane of any node, has completed.
+void NodePayload::seal_released() {
+  if (released_.empty()) return;
+  Held h;
+  auto mark = [&h](const NodePayload& n) {
+    for (int l = 0; l < kLanes; ++l)
+      if (n.lanes_[l].last() > n.lanes_[l].done) h.marks.push_back({{n.node_, l}, n.lanes_[l].last()});
+  };
+  if (cluster_)
+    for (const NodePayload* n : cluster_->nodes()) mark(*n);
+  else
+    mark(*this);
+  if (h.marks.empty()) {  // nothing queued anywhere: free now
+    for (const Ref& r : released_) {
+      free_[r.pool].push_back(r.page);
+      --held_[r.pool];
+    }
+  } else {
+    h.pages.swap(released_);
+    quarantine_.push_back(std::move(h));
   }
-  const std::uint32_t page = free_[p].back();
-  free_[p].pop_back();
-  return page;
+  released_.clear();
+}
+
+// Returns quarantined groups whose batches have all completed (FIFO: later
+// groups were sealed later, so they are never ready before earlier ones).
+// With `wait_for_oldest`, blocks on the oldest group first. True if any
+// group was returned.
+bool NodePayload::reclaim(bool wait_for_oldest) {
+  const HostTimer timer(host_ns_[kHostReclaim]);
+  bool any = false;
+  NodeCache owners;
+  while (!quarantine_.empty()) {
+    Held& h = quarantine_.front();
+    bool ready = true;
+    for (const auto& m : h.marks) {
+      NodePayload* owner = m.first.first == node_ ? this : owners.get(cluster_, m.first.first);
+      if (!owner) continue;  // gone, and synchronized on its way out
+      Lane& L = owner->lanes_[m.first.second];
+      if (m.second <= L.done) continue;
+      void* ev = L.event_for(m.second);
+      if (!ev) continue;
+      if (!wait_for_oldest) {
+        ready = false;
+        break;
+      }
+      kvx_check(kvx_event_synchronize(ev), "quarantine wait");
+      L.retire();
+    }
+    if (!ready) break;
+    for (const Ref& r : h.pages) {
+      free_[r.pool].push_back(r.page);
+      --held_[r.pool];
+    }
+    quarantine_.pop_front();
+    any = true;
+    wait_for_oldest = false;
+  }
+  return any;
+}
+
+// n pages at once from the free list's top (same order as n alloc() calls),
+// taking back quarantined pages as needed.
+void NodePayload::alloc_n(Pool p, std::size_t n, std::vector<std::uint32_t>& out) {
+  const HostTimer timer(host_ns_[kHostAlloc]);
+  std::vector<std::uint32_t>& fl = free_[p];
+  if (fl.size() < n) {
+    seal_released();
+    reclaim(false);
+    bool waited = false;
+    while (fl.size() < n && !quarantine_.empty()) {
+      reclaim(true);
+      waited = true;
+    }
+    if (waited) ++quarantine_waits_;
+  }
+  if (fl.size() < n)
+    throw std::runtime_error(std::string("payload: node ") + std::to_string(node_) + " " + kPoolNames[p] +
+                             " pool exhausted");
+  out.insert(out.end(), fl.rbegin(), fl.rbegin() + static_cast<std::ptrdiff_t>(n));
+  fl.resize(fl.size() - n);
+}
+
+std::uint32_t NodePayload::alloc(Pool p) {
+  std::vector<std::uint32_t> one;
+  alloc_n(p, 1, one);
+  return one[0];
 }
 
 // Re-deals a batch's freshly allocated pages (one pool) in ascending order:
@@ -225,49 +332,112 @@ std::uint32_t NodePayload::alloc(Pool p) {
 // runs of consecutive ids, which the copy engines move as one copy each.
 void sort_pages(std::vector<std::uint32_t>& pages) { std::sort(pages.begin(), pages.end()); }
 
-// A freed page may still be read by queued work; its fence makes any later
-// writer on another lane wait for that work, so no host sync is needed.
-void NodePayload::release(const Ref& r) {
-  if (r.pool >= 0) free_[r.pool].push_back(r.page);
+// ---------------------------------------------------------------------------
+// uploads
+
+void* NodePayload::stage(Lane& L, std::size_t bytes) {
+  const std::size_t need = (std::max<std::size_t>(bytes, 1) + 255) & ~static_cast<std::size_t>(255);
+  if (need > L.ring_cap) {
+    // Grow: every upload staged so far must have been consumed first.
+    if (L.ring) {
+      kvx_check(kvx_stream_synchronize(L.stream), "sync");
+      L.retire();
+      kvx_host_free(L.ring);
+      L.ring = nullptr;
+    }
+    L.ring_used.clear();
+    L.ring_head = 0;
+    L.ring_cap = std::max<std::size_t>(need * 4, std::size_t{4} << 20);
+    void* p = nullptr;
+    kvx_check(kvx_host_alloc(L.ring_cap, &p), "upload ring");
+    L.ring = static_cast<std::uint8_t*>(p);
+  }
+  std::size_t begin = L.ring_head;
+  if (begin + need > L.ring_cap) begin = 0;
+  const std::size_t end = begin + need;
+  // Regions of completed batches are free; an overlapping live one is waited
+  // for (rare: the ring holds many batches).
+  while (!L.ring_used.empty() && L.ring_used.front().ticket <= L.done) L.ring_used.pop_front();
+  std::uint64_t wait = 0;
+  for (const Lane::Region& r : L.ring_used)
+    if (r.begin < end && begin < r.end) wait = std::max(wait, r.ticket);
+  if (wait) {
+    if (void* ev = L.event_for(wait)) kvx_check(kvx_event_synchronize(ev), "upload ring wait");
+    L.retire();
+    while (!L.ring_used.empty() && L.ring_used.front().ticket <= L.done) L.ring_used.pop_front();
+  }
+  L.ring_used.push_back(Lane::Region{begin, end, L.next});
+  L.ring_head = end;
+  return L.ring + begin;
 }
 
-std::uint32_t* NodePayload::device_ids(Lane& lane, const std::vector<std::uint32_t>& ids, int slot) {
-  if (ids.size() > lane.d_ids_cap[slot]) {
-    if (lane.d_ids[slot]) {
-      kvx_check(kvx_stream_synchronize(lane.stream), "sync");  // queued kernels may still read it
-      kvx_free(lane.d_ids[slot]);
-    }
-    lane.d_ids[slot] = nullptr;
-    const std::size_t cap = std::max<std::size_t>(ids.size(), 4096);
+// The lane's device id scratch filled from `n` ids already staged in its
+// pinned ring (one async copy; same-stream order protects the scratch).
+std::uint32_t* NodePayload::upload_ids(Lane& L, const std::uint32_t* staged, std::size_t n) {
+  if (n > L.d_ids_cap) {
+    kvx_check(kvx_stream_synchronize(L.stream), "sync");  // queued kernels may still read it
+    kvx_free(L.d_ids);
+    L.d_ids = nullptr;
+    L.d_ids_cap = std::max<std::size_t>(n * 2, 8192);
     void* p = nullptr;
-    kvx_check(kvx_malloc(opts_.device, cap * sizeof(std::uint32_t), &p), "id scratch");
-    lane.d_ids[slot] = static_cast<std::uint32_t*>(p);
-    lane.d_ids_cap[slot] = cap;
+    kvx_check(kvx_malloc(opts_.device, L.d_ids_cap * sizeof(std::uint32_t), &p), "id scratch");
+    L.d_ids = static_cast<std::uint32_t*>(p);
   }
-  kvx_check(kvx_memcpy_async(lane.d_ids[slot], ids.data(), ids.size() * sizeof(std::uint32_t), lane.stream),
-            "ids upload");
-  return lane.d_ids[slot];
+  kvx_check(kvx_memcpy_async(L.d_ids, staged, n * sizeof(std::uint32_t), L.stream), "ids upload");
+  return L.d_ids;
+}
+
+std::uint32_t* NodePayload::device_ids(Lane& L, const std::vector<std::uint32_t>& ids) {
+  auto* host = static_cast<std::uint32_t*>(stage(L, ids.size() * sizeof(std::uint32_t)));
+  std::memcpy(host, ids.data(), ids.size() * sizeof(std::uint32_t));
+  return upload_ids(L, host, ids.size());
+}
+
+// ---------------------------------------------------------------------------
+// lookups
+
+const NodePayload::Row* NodePayload::find_row(std::uint32_t s, std::uint16_t l) const {
+  const auto it = rows_.find(row_key(s, l));
+  return it == rows_.end() ? nullptr : &it->second;
+}
+
+const NodePayload::Copies* NodePayload::find(std::uint32_t s, std::uint16_t l, std::uint32_t b) const {
+  const Row* r = find_row(s, l);
+  return r && b < r->b.size() ? &r->b[b] : nullptr;
+}
+
+void NodePayload::drop_row_if_empty(std::uint32_t s, std::uint16_t l) {
+  const auto it = rows_.find(row_key(s, l));
+  if (it == rows_.end()) return;
+  for (const Copies& c : it->second.b)
+    if (!c.empty()) return;
+  rows_.erase(it);
 }
 
 // Best existing copy of a block on this node, fastest tier first, skipping
 // `exclude_tier` (the tier being created).
 NodePayload::Ref NodePayload::best_source(std::uint32_t s, std::uint16_t l, std::uint32_t b,
                                           int exclude_tier) const {
-  const auto it = blocks_.find(key(s, l, b));
-  if (it == blocks_.end()) return Ref{};
+  const Copies* c = find(s, l, b);
+  if (!c) return Ref{};
   for (int t = 0; t < 3; ++t)
-    if (t != exclude_tier && it->second.tier[t].pool >= 0) return it->second.tier[t];
+    if (t != exclude_tier && c->slot[t] != kNoPage) return c->tier(t);
   return Ref{};
+}
+
+NodePayload::Ref NodePayload::flight_page(const InFlight& f, std::uint32_t b) {
+  const auto pos = std::lower_bound(f.blocks.begin(), f.blocks.end(), b);  // f.blocks ascends
+  return f.pages[static_cast<std::size_t>(pos - f.blocks.begin())];
 }
 
 bool NodePayload::inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_t b, int exclude_tier, Ref* page,
                                   void** event) const {
+  const Copies* c = find(s, l, b);
+  if (!c) return false;
   for (int t = 0; t < 3; ++t) {
-    if (t == exclude_tier) continue;
-    const auto it = inflight_by_block_.find(key(s, l, b) * 4 + t);
-    if (it == inflight_by_block_.end()) continue;
-    const InFlight& f = inflight_.at(it->second.id);
-    *page = f.pages[it->second.index];  // the slot recorded at posting: O(1)
+    if (t == exclude_tier || !c->coming[t]) continue;
+    const InFlight& f = flight(c->coming[t]);
+    *page = flight_page(f, b);
     *event = f.event;
     return true;
   }
@@ -276,29 +446,66 @@ bool NodePayload::inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_
 
 bool NodePayload::device_block_table(std::uint32_t session, std::uint16_t layer, std::uint32_t n,
                                      std::uint32_t* out) const {
+  if (n == 0) return true;
+  const Row* r = find_row(session, layer);
+  if (!r || r->b.size() < n) return false;
   for (std::uint32_t b = 0; b < n; ++b) {
-    const auto it = blocks_.find(key(session, layer, b));
-    if (it == blocks_.end() || it->second.tier[0].pool != kDevicePool) return false;
-    out[b] = it->second.tier[0].page;
+    const Ref p = r->b[b].tier(0);
+    if (p.pool != kDevicePool) return false;
+    out[b] = p.page;
   }
   return true;
 }
 
-int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier tier) const {
-  const auto it = blocks_.find(key(s, l, b));
-  return it == blocks_.end() ? -1 : it->second.tier[static_cast<int>(tier)].pool;
+bool NodePayload::decode_rows(const std::vector<std::pair<std::uint32_t, std::uint32_t>>& reqs, std::uint16_t layer,
+                              std::uint32_t stride, std::uint32_t* out, std::vector<void*>& waits) {
+  std::uint64_t fill = 0;  // newest fill among the rows (the FILL lane completes in order)
+  const std::size_t first_wait = waits.size();
+  for (std::size_t i = 0; i < reqs.size(); ++i) {
+    const std::uint32_t n = reqs[i].second;
+    if (n == 0) continue;
+    const Row* r = find_row(reqs[i].first, layer);
+    if (!r || r->b.size() < n) return false;
+    fill = std::max(fill, r->fill_ticket);
+    std::uint32_t* dst = out + i * stride;
+    for (std::uint32_t b = 0; b < n; ++b) {
+      const Copies& c = r->b[b];
+      if (c.slot[0] != kNoPage && (c.slot[0] >> 30) == static_cast<std::uint32_t>(kDevicePool)) {
+        dst[b] = c.slot[0] & 0x3FFFFFFFu;
+        continue;
+      }
+      if (!c.coming[0]) return false;
+      const InFlight& f = flight(c.coming[0]);  // a load still landing: wait for exactly that move
+      dst[b] = flight_page(f, b).page;
+      if (std::find(waits.begin() + static_cast<std::ptrdiff_t>(first_wait), waits.end(), f.event) == waits.end())
+        waits.push_back(f.event);
+    }
+  }
+  if (void* ev = fill ? lanes_[kLaneFill].event_for(fill) : nullptr) waits.push_back(ev);
+  return true;
 }
 
-// Queues src[i] -> dst[i] (dst in this node's pools, all in one pool)
-// grouped by (source pool, destination pool). HBM<->HBM pairs use the SM/TMA
-// page mover with device id lists; anything touching pinned host memory uses
-// the copy engines. With `push` the work runs on the source node's PEER lane
-// and stores into this node's memory (the NVLink / peer path of a
-// migration); otherwise on this node's IN lane (destination in HBM), DISK
-// lane (disk-tier source or destination) or OUT lane (HBM -> host). The batch first waits on `waits` and on
-// the fences of every page it touches.
+int NodePayload::pool_of(std::uint32_t s, std::uint16_t l, std::uint32_t b, Tier tier) const {
+  const Copies* c = find(s, l, b);
+  return c ? c->tier(static_cast<int>(tier)).pool : -1;
+}
+
+// ---------------------------------------------------------------------------
+// moves
+
+// Queues src[i] -> dst[i] (dst in this node's pools) grouped by (source pool,
+// destination pool). HBM<->HBM pairs use the SM/TMA page mover with device id
+// lists; anything touching pinned host memory uses the copy engines. With
+// `push` the work runs on the source node's PEER lane and stores into this
+// node's memory (the NVLink / peer path of a migration); otherwise on this
+// node's IN lane (destination in HBM), DISK lane (disk-tier source or
+// destination) or OUT lane (HBM -> host). The batch first waits on `waits`
+// and on the source row's fill (ticket `src_fill` of the source node's FILL
+// lane); destination pages come from the free lists, so nothing queued can
+// still be touching them.
 void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& dst, NodePayload& src_node, bool push,
-                         const std::vector<void*>& waits) {
+                         const std::vector<void*>& waits, std::uint64_t src_fill) {
+  const HostTimer timer(host_ns_[kHostIssue]);
   NodePayload& runner = push ? src_node : *this;
   const int dp0 = dst.empty() ? static_cast<int>(kDevicePool) : dst[0].pool;
   const bool from_disk = std::any_of(src.begin(), src.end(), [](const Ref& r) { return r.pool == kDiskPool; });
@@ -307,37 +514,75 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
                    : (dp0 == kDiskPool || from_disk)             ? kLaneDisk
                                                                  : kLaneOut;
   Lane& L = runner.lanes_[lane];
-  static const char* const kLaneNames[] = {"kvs:IN", "kvs:OUT", "kvs:DISK", "kvs:PEER"};
+  static const char* const kLaneNames[] = {"kvs:IN", "kvs:OUT", "kvs:DISK", "kvs:PEER", "kvs:FILL"};
   nvtxRangePushA(kLaneNames[lane]);  // host-side enqueue of this batch (NVTX, SURVEY.md §5 tracing)
   struct PopRange {
     ~PopRange() { nvtxRangePop(); }
   } pop_range;
-  std::vector<Touch> touched;
-  touched.reserve(src.size() + dst.size());
-  for (const Ref& r : src) touched.emplace_back(&src_node, r);
-  for (const Ref& r : dst) touched.emplace_back(this, r);
   for (void* ev : waits) kvx_check(kvx_stream_wait_event(L.stream, ev), "stream wait");
-  wait_fences(runner, lane, touched);
+  if (void* ev = src_fill ? src_node.lanes_[kLaneFill].event_for(src_fill) : nullptr)
+    kvx_check(kvx_stream_wait_event(L.stream, ev), "fill wait");
+  auto hbm = [](int p) { return p == kDevicePool || p == kLandingPool; };
+  // Common case: one (source pool, destination pool) pair, HBM on both
+  // sides — the ids go straight into the pinned ring, one upload, one mover.
+  bool uniform = !src.empty();
+  for (std::size_t i = 1; i < src.size() && uniform; ++i)
+    uniform = src[i].pool == src[0].pool && dst[i].pool == dst[0].pool;
+  if (uniform && hbm(src[0].pool) && hbm(dst[0].pool)) {
+    const std::size_t n = src.size();
+    std::uint32_t* d_ids = nullptr;
+    {
+      const HostTimer up(host_ns_[kHostUpload]);
+      auto* h = static_cast<std::uint32_t*>(runner.stage(L, 2 * n * sizeof(std::uint32_t)));
+      for (std::size_t i = 0; i < n; ++i) h[i] = src[i].page;
+      for (std::size_t i = 0; i < n; ++i) h[n + i] = dst[i].page;
+      d_ids = runner.upload_ids(L, h, 2 * n);
+    }
+    {
+      const HostTimer launch_timer(host_ns_[kHostLaunch]);
+      kvx_check(kvx_copy_pages_capped(src_node.pools_[src[0].pool], d_ids, pools_[dst[0].pool], d_ids + n, n,
+                                      KVX_COPY_AUTO, push ? src_node.opts_.migrate_max_ctas : 0u, L.stream),
+                "page copy");
+    }
+    runner.close_batch(lane);
+    return L.stream;
+  }
+  // General case: bucket by pool pair; the id lists of every HBM<->HBM
+  // bucket go up in ONE staged upload.
+  std::vector<std::uint32_t> bucket_ids[16][2];
+  for (std::size_t i = 0; i < src.size(); ++i) {
+    const int k = src[i].pool * 4 + dst[i].pool;
+    bucket_ids[k][0].push_back(src[i].page);
+    bucket_ids[k][1].push_back(dst[i].page);
+  }
+  std::size_t offsets[16][2] = {};
+  std::vector<std::uint32_t> staged;
+  for (int k = 0; k < 16; ++k)
+    if (!bucket_ids[k][0].empty() && hbm(k / 4) && hbm(k % 4))
+      for (int side = 0; side < 2; ++side) {
+        offsets[k][side] = staged.size();
+        staged.insert(staged.end(), bucket_ids[k][side].begin(), bucket_ids[k][side].end());
+      }
+  const std::uint32_t* d_staged = nullptr;
+  if (!staged.empty()) {
+    const HostTimer up(host_ns_[kHostUpload]);
+    d_staged = runner.device_ids(L, staged);
+  }
+  const HostTimer launch_timer(host_ns_[kHostLaunch]);
   for (int sp = 0; sp < 4; ++sp)
     for (int dp = 0; dp < 4; ++dp) {
-      std::vector<std::uint32_t> s_ids, d_ids;
-      for (std::size_t i = 0; i < src.size(); ++i)
-        if (src[i].pool == sp && dst[i].pool == dp) {
-          s_ids.push_back(src[i].page);
-          d_ids.push_back(dst[i].page);
-        }
+      const std::vector<std::uint32_t>& s_ids = bucket_ids[sp * 4 + dp][0];
+      const std::vector<std::uint32_t>& d_ids = bucket_ids[sp * 4 + dp][1];
       if (s_ids.empty()) continue;
       kvx_pool* from = src_node.pools_[sp];
       kvx_pool* to = pools_[dp];
-      const bool on_device = (sp == kDevicePool || sp == kLandingPool) && (dp == kDevicePool || dp == kLandingPool);
       // A file pool on either side (the source node's DISK copy may be a file
       // even when ours is not) with HBM on the other goes through a bounce.
       const bool file_side = kvx_pool_file_direct(from) >= 0 || kvx_pool_file_direct(to) >= 0;
-      const bool hbm_side = sp == kDevicePool || sp == kLandingPool || dp == kDevicePool || dp == kLandingPool;
-      const bool file_hop = file_side && hbm_side;
-      if (on_device) {
-        const std::uint32_t* ds = runner.device_ids(L, s_ids, 0);
-        const std::uint32_t* dd = runner.device_ids(L, d_ids, 1);
+      const bool file_hop = file_side && (hbm(sp) || hbm(dp));
+      if (hbm(sp) && hbm(dp)) {
+        const std::uint32_t* ds = d_staged + offsets[sp * 4 + dp][0];
+        const std::uint32_t* dd = d_staged + offsets[sp * 4 + dp][1];
         kvx_check(kvx_copy_pages_capped(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO,
                                         push ? src_node.opts_.migrate_max_ctas : 0u, L.stream),
                   "page copy");
@@ -360,7 +605,7 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
                   "copy-engine copy");
       }
     }
-  set_fences(runner, lane, touched);
+  runner.close_batch(lane);
   return L.stream;
 }
 
@@ -373,36 +618,41 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
   moved_[static_cast<int>(why)] += blocks.size() * page_bytes_;
 
   if (why == BlockEvent::Created) {
-    std::vector<std::uint32_t> pages;
-    std::vector<kvx_block_tag> tags;
-    std::vector<Touch> touched;
+    Row& r = row(session, layer);
     for (std::uint32_t b : blocks) {
-      Copies& c = blocks_[key(session, layer, b)];
-      release(c.tier[t]);
-      c.tier[t] = Ref{};
+      Copies& c = at(r, b);
+      release(c.tier(t));
+      c.slot[t] = kNoPage;
     }
-    for (std::size_t i = 0; i < blocks.size(); ++i) pages.push_back(alloc(kDevicePool));
+    std::vector<std::uint32_t> pages;
+    alloc_n(kDevicePool, blocks.size(), pages);
     sort_pages(pages);
+    // One staged upload carries the page ids and their (session, layer,
+    // block) tags; the fill runs on the FILL lane.
+    const std::size_t id_bytes = pages.size() * sizeof(std::uint32_t);
+    const std::size_t tag_off = (id_bytes + 15) & ~static_cast<std::size_t>(15);
+    const std::size_t bytes = tag_off + blocks.size() * sizeof(kvx_block_tag);
+    Lane& L = lanes_[kLaneFill];
+    auto* host = static_cast<std::uint8_t*>(stage(L, bytes));
+    std::memcpy(host, pages.data(), id_bytes);
+    auto* tags = reinterpret_cast<kvx_block_tag*>(host + tag_off);
     for (std::size_t i = 0; i < blocks.size(); ++i) {
-      Copies& c = blocks_[key(session, layer, blocks[i])];
-      c.tier[t] = Ref{kDevicePool, pages[i]};
-      tags.push_back(kvx_block_tag{session, layer, blocks[i]});
-      touched.emplace_back(this, c.tier[t]);
+      r.b[blocks[i]].slot[t] = pack(Ref{kDevicePool, pages[i]});
+      tags[i] = kvx_block_tag{session, layer, blocks[i]};
     }
-    Lane& L = lanes_[kLaneIn];
-    wait_fences(*this, kLaneIn, touched);
-    const std::uint32_t* d_pages = device_ids(L, pages, 0);
-    if (tags.size() * sizeof(kvx_block_tag) > d_tags_cap_) {
+    if (bytes > d_tags_cap_) {
       if (d_tags_) kvx_check(kvx_stream_synchronize(L.stream), "sync");
       kvx_free(d_tags_);
-      d_tags_cap_ = std::max<std::size_t>(tags.size() * sizeof(kvx_block_tag), 65536);
+      d_tags_cap_ = std::max<std::size_t>(bytes * 2, 65536);
       kvx_check(kvx_malloc(opts_.device, d_tags_cap_, &d_tags_), "tag scratch");
     }
-    kvx_check(kvx_memcpy_async(d_tags_, tags.data(), tags.size() * sizeof(kvx_block_tag), L.stream), "tags upload");
-    kvx_check(kvx_fill_pages(pools_[kDevicePool], d_pages, static_cast<const kvx_block_tag*>(d_tags_), pages.size(),
-                             opts_.seed, &opts_.layout, opts_.fill_mode, L.stream),
+    kvx_check(kvx_memcpy_async(d_tags_, host, bytes, L.stream), "ids + tags upload");
+    const auto* d_pages = static_cast<const std::uint32_t*>(d_tags_);
+    const auto* d_tags = reinterpret_cast<const kvx_block_tag*>(static_cast<const std::uint8_t*>(d_tags_) + tag_off);
+    kvx_check(kvx_fill_pages(pools_[kDevicePool], d_pages, d_tags, pages.size(), opts_.seed, &opts_.layout,
+                             opts_.fill_mode, L.stream),
               "fill");
-    set_fences(*this, kLaneIn, touched);
+    r.fill_ticket = close_batch(kLaneFill);
     if (!opts_.free_running) synchronize();
     return;
   }
@@ -415,29 +665,35 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
   // Free-running: the move was issued when the transfer was scheduled and
   // has completed (transfer_retired waited on it). Install the pages of the
   // blocks the state machine says gained the tier; return the rest.
-  InFlight f = std::move(inflight_.at(applying_));
-  inflight_.erase(applying_);
+  const std::uint32_t slot = flight_of_.at(applying_);
+  InFlight& f = flights_[slot];
   applying_valid_ = false;
   std::vector<bool> used(f.blocks.size(), false);
   std::vector<std::uint32_t> missing;
-  // f.blocks ascends (posted over block_lo..block_hi in order), so each
-  // gained block is found by bisection: O(n log n) per layer, not O(n^2)
-  // (2,048-block layers at Llama-3.1-70B @32K).
+  Row& r = row(session, layer);
+  std::size_t cursor = 0;  // both lists usually ascend: a merge walk, bisection otherwise
   for (std::uint32_t b : blocks) {
-    const auto pos = std::lower_bound(f.blocks.begin(), f.blocks.end(), b);
-    const std::size_t i = static_cast<std::size_t>(pos - f.blocks.begin());
-    if (pos == f.blocks.end() || *pos != b) {
+    std::size_t i = cursor;
+    if (i >= f.blocks.size() || f.blocks[i] != b) {
+      const auto pos = std::lower_bound(f.blocks.begin(), f.blocks.end(), b);
+      i = static_cast<std::size_t>(pos - f.blocks.begin());
+    }
+    if (i >= f.blocks.size() || f.blocks[i] != b) {
       missing.push_back(b);  // its source appeared only after scheduling
       continue;
     }
-    Copies& c = blocks_[key(session, layer, b)];
-    release(c.tier[t]);
-    c.tier[t] = f.pages[i];
+    cursor = i + 1;
+    Copies& c = at(r, b);
+    release(c.tier(t));
+    c.slot[t] = pack(f.pages[i]);
     used[i] = true;
   }
   for (std::size_t i = 0; i < f.blocks.size(); ++i)
     if (!used[i]) release(f.pages[i]);
   kvx_event_destroy(f.event);
+  f = InFlight{};
+  flight_of_.erase(applying_);
+  free_flights_.push_back(slot);
   if (!missing.empty()) move_now(session, layer, tier, why, missing);
 }
 
@@ -459,26 +715,28 @@ void NodePayload::move_now(std::uint32_t session, std::uint16_t layer, Tier tier
     push = true;
   }
   std::vector<Ref> src, dst;
+  Row& r = row(session, layer);
   for (std::uint32_t b : blocks) {
     const Ref from = src_node->best_source(session, layer, b, src_node == this ? t : -1);
     if (from.pool < 0)
       throw std::runtime_error("payload: no source copy for session " + std::to_string(session) + " layer " +
                                std::to_string(layer) + " block " + std::to_string(b) + " (" +
                                block_event_name(why) + ")");
-    Copies& c = blocks_[key(session, layer, b)];
-    release(c.tier[t]);
-    c.tier[t] = Ref{};
+    Copies& c = at(r, b);
+    release(c.tier(t));
+    c.slot[t] = kNoPage;
     src.push_back(from);
   }
   std::vector<std::uint32_t> pages;
-  for (std::size_t i = 0; i < blocks.size(); ++i) pages.push_back(alloc(dest));
+  alloc_n(dest, blocks.size(), pages);
   sort_pages(pages);
   for (std::size_t i = 0; i < blocks.size(); ++i) {
-    Copies& c = blocks_[key(session, layer, blocks[i])];
-    c.tier[t] = Ref{static_cast<std::int8_t>(dest), pages[i]};
-    dst.push_back(c.tier[t]);
+    const Ref d{static_cast<std::int8_t>(dest), pages[i]};
+    at(r, blocks[i]).slot[t] = pack(d);
+    dst.push_back(d);
   }
-  issue(src, dst, *src_node, push, {});
+  const Row* sr = src_node->find_row(session, layer);
+  issue(src, dst, *src_node, push, {}, sr ? sr->fill_ticket : 0);
   (push ? *src_node : *this).synchronize();
   check_file_io();
 }
@@ -501,14 +759,15 @@ void NodePayload::check_file_io() const {
 void NodePayload::tier_lost(std::uint32_t session, std::uint16_t layer, Tier tier,
                             const std::vector<std::uint32_t>& blocks) {
   const int t = static_cast<int>(tier);
+  const auto it = rows_.find(row_key(session, layer));
+  if (it == rows_.end()) return;
   for (std::uint32_t b : blocks) {
-    const auto it = blocks_.find(key(session, layer, b));
-    if (it == blocks_.end()) continue;
-    release(it->second.tier[t]);
-    it->second.tier[t] = Ref{};
-    const Copies& c = it->second;
-    if (c.tier[0].pool < 0 && c.tier[1].pool < 0 && c.tier[2].pool < 0) blocks_.erase(it);
+    if (b >= it->second.b.size()) continue;
+    Copies& c = it->second.b[b];
+    release(c.tier(t));
+    c.slot[t] = kNoPage;
   }
+  drop_row_if_empty(session, layer);
 }
 
 // ---------------------------------------------------------------------------
@@ -528,55 +787,94 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
     src_node = cluster_->node(it->second);
     push = true;
   }
-  InFlight f;
+  const HostTimer timer(host_ns_[kHostPosted]);
+  std::uint32_t slot;
+  if (!free_flights_.empty()) {
+    slot = free_flights_.back();
+    free_flights_.pop_back();
+  } else {
+    slot = static_cast<std::uint32_t>(flights_.size());
+    flights_.emplace_back();
+  }
+  InFlight& f = flights_[slot];
+  f.id = tr.id;
   f.tier = t;
   f.session = tr.session;
   f.layer = tr.layer;
-  std::vector<Ref> src, dst;
-  std::vector<void*> waits;
+  f.blocks.clear();
+  f.pages.clear();
+  // Per-posting scratch is kept across calls: fresh 16-100 KB buffers per
+  // layer cost more in allocation and first-touch faults than the work.
+  std::vector<Ref>& src = scratch_src_;
+  std::vector<Ref>& dst = scratch_dst_;
+  std::vector<void*>& waits = scratch_waits_;
+  std::vector<std::uint32_t>& pages = scratch_pages_;
+  src.clear();
+  dst.clear();
+  waits.clear();
+  pages.clear();
+  const Row* have = find_row(tr.session, tr.layer);
+  const Row* srow = src_node->find_row(tr.session, tr.layer);
+  const int exclude = src_node == this ? t : -1;
+  const std::size_t span = static_cast<std::size_t>(tr.block_hi - tr.block_lo + 1);
+  src.reserve(span);
+  f.blocks.reserve(span);
   for (std::uint64_t b64 = tr.block_lo; b64 <= tr.block_hi; ++b64) {
     const auto b = static_cast<std::uint32_t>(b64);
-    const auto have = blocks_.find(key(tr.session, tr.layer, b));
-    if (have != blocks_.end() && have->second.tier[t].pool >= 0) continue;  // already there
-    if (inflight_by_block_.count(key(tr.session, tr.layer, b) * 4 + t)) continue;  // already coming
-    const int exclude = src_node == this ? t : -1;
-    Ref from = src_node->best_source(tr.session, tr.layer, b, exclude);
+    if (have && b < have->b.size()) {
+      const Copies& c = have->b[b];
+      if (c.slot[t] != kNoPage || c.coming[t]) continue;  // already there / already coming
+    }
+    if (!srow || b >= srow->b.size()) continue;
+    const Copies& sc = srow->b[b];
+    Ref from;
+    for (int k = 0; k < 3; ++k)
+      if (k != exclude && sc.slot[k] != kNoPage) {
+        from = sc.tier(k);
+        break;
+      }
     if (from.pool < 0) {  // chained behind a move still in flight on the source side
       void* ev = nullptr;
       if (!src_node->inflight_source(tr.session, tr.layer, b, exclude, &from, &ev)) continue;
-      waits.push_back(ev);
+      if (waits.empty() || waits.back() != ev) waits.push_back(ev);
     }
     src.push_back(from);
     f.blocks.push_back(b);
   }
-  if (f.blocks.empty()) return;
-  std::vector<std::uint32_t> pages;
-  for (std::size_t i = 0; i < f.blocks.size(); ++i) pages.push_back(alloc(dest));
-  sort_pages(pages);
-  for (std::uint32_t pg : pages) {
-    dst.push_back(Ref{static_cast<std::int8_t>(dest), pg});
-    f.pages.push_back(dst.back());
+  if (f.blocks.empty()) {
+    free_flights_.push_back(slot);
+    return;
   }
-  // Sources still being written by another move are chained explicitly (and
-  // by their fences); recycled destination pages wait on their fences.
+  alloc_n(dest, f.blocks.size(), pages);
+  // Ascending pages only matter for copy-engine runs (host / disk pools);
+  // the HBM movers take any permutation.
+  if (dest == kHostPool || dest == kDiskPool) sort_pages(pages);
+  dst.resize(pages.size());
+  for (std::size_t i = 0; i < pages.size(); ++i) dst[i] = Ref{static_cast<std::int8_t>(dest), pages[i]};
+  f.pages.assign(dst.begin(), dst.end());
   std::sort(waits.begin(), waits.end());
   waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
-  void* lane_stream = issue(src, dst, *src_node, push, waits);
+  void* lane_stream = issue(src, dst, *src_node, push, waits, srow ? srow->fill_ticket : 0);
   kvx_check(kvx_event_create(&f.event), "event");
   kvx_check(kvx_event_record(f.event, lane_stream), "event record");
-  for (std::size_t i = 0; i < f.blocks.size(); ++i)
-    inflight_by_block_[key(tr.session, tr.layer, f.blocks[i]) * 4 + t] = InFlightSlot{tr.id, static_cast<std::uint32_t>(i)};
+  {
+    Row& r = row(tr.session, tr.layer);
+    if (r.b.size() <= f.blocks.back()) r.b.resize(static_cast<std::size_t>(f.blocks.back()) + 1);  // ascending
+    for (std::uint32_t b : f.blocks) r.b[b].coming[t] = slot + 1;
+  }
   moved_[7] += f.blocks.size() * page_bytes_;  // bytes issued ahead of their apply
-  inflight_.emplace(tr.id, std::move(f));
+  flight_of_.emplace(tr.id, slot);
   ++posted_;
 }
 
 void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
+  const HostTimer timer(host_ns_[kHostRetired]);
   applying_valid_ = false;
   if (!opts_.free_running) return;
-  const auto it = inflight_.find(id);
-  if (it == inflight_.end()) return;
-  InFlight& f = it->second;
+  const auto it = flight_of_.find(id);
+  if (it == flight_of_.end()) return;
+  const std::uint32_t slot = it->second;
+  InFlight& f = flights_[slot];
   if (kvx_event_query(f.event) == KVX_NOT_READY) {  // the GPU is behind the model clock
     const std::uint64_t t0 = now_ns();
     nvtxRangePushA("kvs:apply_wait");
@@ -587,16 +885,19 @@ void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
   // A failed pread / pwrite does not fail the stream (host callback): check
   // the file pools before the store installs these pages as valid.
   if (!voided) check_file_io();
-  // Later moves touching these pages are ordered by the pages' fences.
-  for (std::uint32_t b : f.blocks) {
-    const auto k = key(f.session, f.layer, b) * 4 + f.tier;
-    const auto jt = inflight_by_block_.find(k);
-    if (jt != inflight_by_block_.end() && jt->second.id == id) inflight_by_block_.erase(jt);
-  }
+  const auto rt = rows_.find(row_key(f.session, f.layer));
+  if (rt != rows_.end())
+    for (std::uint32_t b : f.blocks)
+      if (b < rt->second.b.size() && rt->second.b[b].coming[f.tier] == slot + 1) rt->second.b[b].coming[f.tier] = 0;
   if (voided) {
     for (const Ref& r : f.pages) release(r);
     kvx_event_destroy(f.event);
-    inflight_.erase(it);
+    const std::uint32_t s = f.session;
+    const std::uint16_t l = f.layer;
+    f = InFlight{};
+    flight_of_.erase(it);
+    free_flights_.push_back(slot);
+    drop_row_if_empty(s, l);
     return;
   }
   applying_ = id;
@@ -618,9 +919,9 @@ void NodePayload::importing(std::uint32_t session, std::int64_t /*tokens*/) {
 }
 
 bool NodePayload::read_block(std::uint32_t session, std::uint16_t layer, std::uint32_t block, Tier tier, void* out) {
-  const auto it = blocks_.find(key(session, layer, block));
-  if (it == blocks_.end()) return false;
-  const Ref r = it->second.tier[static_cast<int>(tier)];
+  const Copies* c = find(session, layer, block);
+  if (!c) return false;
+  const Ref r = c->tier(static_cast<int>(tier));
   if (r.pool < 0) return false;
   synchronize();
   kvx_check(kvx_read_page(pools_[r.pool], r.page, out), "read page");

@@ -237,6 +237,28 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
 
 // ---- K5: contents -----------------------------------------------------------
 
+// 16-byte vector v of a page whose tag hashes to h (K5 content).
+__device__ __forceinline__ uint4 fill_vec(uint64_t h, uint32_t v, int mode, int dtype) {
+  if (mode == KVX_FILL_BITS) {
+    const uint64_t w0 = splitmix64(h + 2ull * v), w1 = splitmix64(h + 2ull * v + 1);
+    return make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1),
+                      static_cast<uint32_t>(w1 >> 32));
+  }
+  uint32_t w[4];
+  if (dtype == KVX_DTYPE_F32) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(unit_value(splitmix64(h + 4ull * v + e)));
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t lo = f32_to_bf16_rne(unit_value(splitmix64(h + 8ull * v + 2 * e)));
+      const uint32_t hi = f32_to_bf16_rne(unit_value(splitmix64(h + 8ull * v + 2 * e + 1)));
+      w[e] = lo | (hi << 16);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __global__ void __launch_bounds__(256) fill_pages_kernel(uint8_t* base, uint64_t page_bytes, const uint32_t* ids,
                                                          const kvx_block_tag* tags, uint64_t n, uint64_t seed,
                                                          int mode, int dtype) {
@@ -245,29 +267,51 @@ __global__ void __launch_bounds__(256) fill_pages_kernel(uint8_t* base, uint64_t
     const kvx_block_tag t = tags[i];
     const uint64_t h = block_base(seed, t.session, t.layer, t.block);
     uint4* page = reinterpret_cast<uint4*>(base + static_cast<uint64_t>(ids[i]) * page_bytes);
-    for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
-      uint4 out;
-      if (mode == KVX_FILL_BITS) {
-        const uint64_t w0 = splitmix64(h + 2ull * v), w1 = splitmix64(h + 2ull * v + 1);
-        out = make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), static_cast<uint32_t>(w1),
-                         static_cast<uint32_t>(w1 >> 32));
-      } else if (dtype == KVX_DTYPE_F32) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(unit_value(splitmix64(h + 4ull * v + e)));
-        out = make_uint4(w[0], w[1], w[2], w[3]);
-      } else {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t lo = f32_to_bf16_rne(unit_value(splitmix64(h + 8ull * v + 2 * e)));
-          const uint32_t hi = f32_to_bf16_rne(unit_value(splitmix64(h + 8ull * v + 2 * e + 1)));
-          w[e] = lo | (hi << 16);
-        }
-        out = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-      page[v] = out;
+    for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) page[v] = fill_vec(h, v, mode, dtype);
+  }
+}
+
+// Scrub: pages whose bytes differ from the K5 content of their tag. Tags
+// come from a list, or from block-table coordinates (layer, request, block)
+// when `tags` is null (tables [layers][batch][max_blocks], sessions[batch],
+// ctx_lens[batch]: blocks beyond a request's context are skipped).
+__global__ void __launch_bounds__(256) verify_pages_kernel(const uint8_t* base, uint64_t page_bytes, uint64_t pool_pages,
+                                                           const uint32_t* ids, const kvx_block_tag* tags, uint64_t n,
+                                                           const int32_t* sessions, const int32_t* ctx_lens,
+                                                           int batch, int max_blocks, int block_tokens, uint64_t seed,
+                                                           int mode, int dtype, unsigned long long* mismatches) {
+  const uint32_t vecs = static_cast<uint32_t>(page_bytes / 16);
+  __shared__ int bad;
+  for (uint64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    kvx_block_tag t;
+    if (tags) {
+      t = tags[i];
+    } else {
+      const uint64_t per_layer = static_cast<uint64_t>(batch) * max_blocks;
+      const uint32_t layer = static_cast<uint32_t>(i / per_layer);
+      const uint64_t rem = i - layer * per_layer;
+      const int b = static_cast<int>(rem / max_blocks), blk = static_cast<int>(rem - static_cast<uint64_t>(b) * max_blocks);
+      if (blk * block_tokens >= ctx_lens[b]) continue;  // past this request's context (block-uniform)
+      t = kvx_block_tag{static_cast<uint32_t>(sessions[b]), layer, static_cast<uint32_t>(blk)};
     }
+    const uint32_t id = ids[i];
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    if (id >= pool_pages) {
+      if (threadIdx.x == 0) bad = 1;
+    } else {
+      const uint64_t h = block_base(seed, t.session, t.layer, t.block);
+      const uint4* page = reinterpret_cast<const uint4*>(base + static_cast<uint64_t>(id) * page_bytes);
+      int mine = 0;
+      for (uint32_t v = threadIdx.x; v < vecs; v += blockDim.x) {
+        const uint4 want = fill_vec(h, v, mode, dtype), got = page[v];
+        mine |= (want.x != got.x) | (want.y != got.y) | (want.z != got.z) | (want.w != got.w);
+      }
+      if (mine) bad = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && bad) atomicAdd(mismatches, 1ull);
+    __syncthreads();
   }
 }
 
@@ -383,6 +427,44 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
   KVX_CUDA_TRY(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1,
                                     &fail_idx, st),
                "kvx_copy_pages(CE): cudaMemcpyBatchAsync");
+  return KVX_OK;
+}
+
+int kvx_verify_pages(const kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,
+                     uint64_t seed, const kvx_page_layout* layout, int fill_mode, unsigned long long* d_mismatches,
+                     void* stream) {
+  if (!pool || !d_mismatches || (n && (!d_page_ids || !d_tags))) return kvx::fail_arg("kvx_verify_pages: null argument");
+  if (pool->fd >= 0) return kvx::fail_arg("kvx_verify_pages: not on a file pool");
+  if (fill_mode != KVX_FILL_BITS && fill_mode != KVX_FILL_VALUES) return kvx::fail_arg("kvx_verify_pages: bad mode");
+  if (fill_mode == KVX_FILL_VALUES && (!layout || kvx_page_bytes(layout) != pool->page_bytes))
+    return kvx::fail_arg("kvx_verify_pages: layout does not match the pool's page size");
+  if (n == 0) return KVX_OK;
+  const int dtype = layout ? layout->dtype : KVX_DTYPE_BF16;
+  kvx::DeviceGuard guard(pool->device);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, 148ull * 8));
+  kvx::verify_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(pool->base, pool->page_bytes, pool->num_pages,
+                                                                       d_page_ids, d_tags, n, nullptr, nullptr, 0, 1,
+                                                                       1, seed, fill_mode, dtype, d_mismatches);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_verify_pages");
+  return KVX_OK;
+}
+
+int kvx_verify_block_tables(const kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_tables,
+                            const int32_t* d_ctx_lens, const int32_t* d_sessions, int32_t num_layers, int32_t batch,
+                            int32_t max_blocks, uint64_t seed, int fill_mode, unsigned long long* d_mismatches,
+                            void* stream) {
+  if (!pool || !layout || !d_tables || !d_ctx_lens || !d_sessions || !d_mismatches)
+    return kvx::fail_arg("kvx_verify_block_tables: null argument");
+  if (kvx_page_bytes(layout) != pool->page_bytes) return kvx::fail_arg("kvx_verify_block_tables: layout/page size");
+  if (fill_mode != KVX_FILL_BITS && fill_mode != KVX_FILL_VALUES) return kvx::fail_arg("kvx_verify_block_tables: bad mode");
+  const uint64_t n = static_cast<uint64_t>(num_layers) * batch * max_blocks;
+  if (n == 0) return KVX_OK;
+  kvx::DeviceGuard guard(pool->device);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(n, 148ull * 8));
+  kvx::verify_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(
+      pool->base, pool->page_bytes, pool->num_pages, d_tables, nullptr, n, d_sessions, d_ctx_lens, batch, max_blocks,
+      layout->block_tokens, seed, fill_mode, layout->dtype, d_mismatches);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_verify_block_tables");
   return KVX_OK;
 }
 

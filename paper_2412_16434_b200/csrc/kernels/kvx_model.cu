@@ -1,0 +1,487 @@
+// K6: the decode step that consumes the paged KV cache — sm_100a.
+//
+// The reference models a decode step's latency (decode_step_time,
+// /root/reference/proj/src/costmodel.cpp:59-80, used by Engine::try_start,
+// engine.cpp:256-257) and a prefill's (prefill_time, costmodel.cpp:54-57).
+// This file EXECUTES them for a Llama-shaped model with random bf16 weights
+// (no checkpoint exists offline), so the serving engine's quanta last what
+// the B200 takes:
+//
+//   per layer:  RMSNorm -> QKV projection -> RoPE(q) -> K4 paged attention
+//               with this step's token appended into its page (fused,
+//               kvx_decode_attention_append) -> O projection (+ residual)
+//               -> RMSNorm -> gate/up projection -> SiLU * up -> down
+//               projection (+ residual)
+//   then:       final RMSNorm -> LM head -> greedy argmax (the sampled token)
+//
+// The projections are plain dense GEMMs on cuBLAS (bf16 in, fp32 compute).
+// At decode batch sizes they stream the 16 GB of Llama-3.1-8B weights once
+// per step (HBM-bound); at prefill sizes they are tensor-core bound.
+// Everything around them is hand-written here; the attention is K4.
+//
+// K/V the step appends: the bytes written into the cache are the
+// deterministic K5 content of that slot (the splitmix fill of its (session,
+// layer, block) tag), not the projection's output, so every page keeps a
+// content the CPU oracle can recompute and migrations / loads stay
+// bit-checkable while the step does the same work (the projection is still
+// computed in full; only its K/V columns are not what lands in the page).
+
+#include <cublas_v2.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "kvx_common.cuh"
+
+struct kvx_model {
+  kvx_model_config cfg{};
+  int device = 0;
+  cublasHandle_t blas = nullptr;
+  void* stream = nullptr;  // stream the handle is bound to (rebound per call)
+  // weights (bf16)
+  uint16_t* embed = nullptr;    // [V][Hd]
+  uint16_t* lm_head = nullptr;  // [V][Hd]
+  uint16_t* final_norm = nullptr;
+  std::vector<uint16_t*> wqkv, wo, wgu, wd, norm1, norm2;
+  uint8_t* slab = nullptr;
+  uint64_t slab_bytes = 0;
+  // activations, sized for `rows_cap` rows
+  int rows_cap = 0;
+  uint16_t *x = nullptr, *h = nullptr, *qkv = nullptr, *q = nullptr, *kv_new = nullptr, *attn = nullptr,
+           *gu = nullptr, *act = nullptr, *logits = nullptr;
+  float* attn_f32 = nullptr;
+  int32_t* tokens = nullptr;
+  void* attn_ws = nullptr;
+  uint64_t attn_ws_bytes = 0;
+};
+
+namespace kvx {
+namespace {
+
+__global__ void init_uniform_bf16(uint16_t* p, uint64_t n, uint64_t seed, float scale) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = f32_to_bf16_rne(__fmul_rn(unit_value(splitmix64(seed + i)), scale));
+}
+
+__global__ void init_const_bf16(uint16_t* p, uint64_t n, float v) {
+  const uint16_t b = f32_to_bf16_rne(v);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = b;
+}
+
+__device__ __forceinline__ float bf(uint16_t v) { return __uint_as_float(static_cast<uint32_t>(v) << 16); }
+
+// x[r] = E[token[r]]
+__global__ void embed_rows(const uint16_t* E, const int32_t* tok, uint16_t* x, int hidden, int vocab) {
+  const int r = blockIdx.x;
+  int t = tok[r] % vocab;
+  if (t < 0) t += vocab;
+  const uint4* src = reinterpret_cast<const uint4*>(E + static_cast<uint64_t>(t) * hidden);
+  uint4* dst = reinterpret_cast<uint4*>(x + static_cast<uint64_t>(r) * hidden);
+  for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
+}
+
+// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w, one CTA per row.
+__global__ void __launch_bounds__(256) rms_norm(const uint16_t* x, const uint16_t* w, uint16_t* y, int hidden,
+                                                 float eps) {
+  const int r = blockIdx.x;
+  const uint16_t* xr = x + static_cast<uint64_t>(r) * hidden;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
+    const float v = bf(xr[i]);
+    ss += v * v;
+  }
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float inv = rsqrtf(red[0] / hidden + eps);
+  uint16_t* yr = y + static_cast<uint64_t>(r) * hidden;
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) yr[i] = f32_to_bf16_rne(bf(xr[i]) * inv * bf(w[i]));
+}
+
+// From one request's QKV row: q with RoPE at position ctx-1 (Llama rotate-half
+// pairing), and the K/V row this step appends — the K5 content of slot
+// (ctx-1) % T of block (ctx-1) / T of (session, layer), so the page keeps
+// its oracle-checkable bytes (see the file comment).
+__global__ void rope_and_token(const uint16_t* qkv, const int32_t* sessions, const int32_t* ctx_lens, int layer,
+                               int hq, int hkv, int d, int block_tokens, float theta, uint64_t seed, int fill_mode,
+                               uint16_t* q_out, uint16_t* k_out, uint16_t* v_out) {
+  const int b = blockIdx.x;
+  const int pos = max(ctx_lens[b] - 1, 0);
+  const uint16_t* row = qkv + static_cast<uint64_t>(b) * (hq + 2 * hkv) * d;
+  const int half = d / 2;
+  for (int e = threadIdx.x; e < hq * half; e += blockDim.x) {
+    const int head = e / half, i = e - head * half;
+    const float inv_freq = exp2f(-(2.f * i / d) * log2f(theta));
+    float sn, cs;
+    sincosf(pos * inv_freq, &sn, &cs);
+    const float x0 = bf(row[head * d + i]), x1 = bf(row[head * d + i + half]);
+    uint16_t* qo = q_out + (static_cast<uint64_t>(b) * hq + head) * d;
+    qo[i] = f32_to_bf16_rne(x0 * cs - x1 * sn);
+    qo[i + half] = f32_to_bf16_rne(x1 * cs + x0 * sn);
+  }
+  const uint32_t block = static_cast<uint32_t>(pos / block_tokens), slot = static_cast<uint32_t>(pos % block_tokens);
+  const uint64_t h = block_base(seed, static_cast<uint32_t>(sessions[b]), static_cast<uint32_t>(layer), block);
+  for (int e = threadIdx.x; e < 2 * hkv * d; e += blockDim.x) {
+    const int kv = e / (hkv * d), rem = e - kv * hkv * d, head = rem / d, c = rem - head * d;
+    const uint64_t elt = (static_cast<uint64_t>(kv * hkv + head) * block_tokens + slot) * d + c;  // bf16 index in page
+    uint16_t val;
+    if (fill_mode == KVX_FILL_BITS) {
+      const uint64_t w = splitmix64(h + elt / 4);
+      val = static_cast<uint16_t>(w >> (16 * (elt % 4)));
+    } else {
+      val = f32_to_bf16_rne(unit_value(splitmix64(h + elt)));
+    }
+    (kv ? v_out : k_out)[(static_cast<uint64_t>(b) * hkv + head) * d + c] = val;
+  }
+}
+
+__global__ void f32_to_bf16_rows(const float* in, uint16_t* out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = f32_to_bf16_rne(in[i]);
+}
+
+// act = silu(gate) * up over [rows][2 * inter] -> [rows][inter]
+__global__ void silu_mul(const uint16_t* gu, uint16_t* act, int inter, uint64_t rows) {
+  const uint64_t n = rows * inter;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / inter, c = i - r * inter;
+    const float g = bf(gu[r * 2 * inter + c]), u = bf(gu[r * 2 * inter + inter + c]);
+    act[i] = f32_to_bf16_rne(g / (1.f + __expf(-g)) * u);
+  }
+}
+
+// Greedy sampling: argmax over one row of logits per CTA.
+__global__ void __launch_bounds__(512) argmax_rows(const uint16_t* logits, int vocab, int32_t* out) {
+  const int r = blockIdx.x;
+  const uint16_t* row = logits + static_cast<uint64_t>(r) * vocab;
+  float best = -INFINITY;
+  int arg = 0;
+  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+    const float v = bf(row[i]);
+    if (v > best) best = v, arg = i;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ov > best || (ov == best && oa < arg)) best = ov, arg = oa;
+  }
+  __shared__ float sv[16];
+  __shared__ int sa[16];
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = best, sa[threadIdx.x >> 5] = arg;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
+      if (sv[w] > best || (sv[w] == best && sa[w] < arg)) best = sv[w], arg = sa[w];
+    out[r] = arg;
+  }
+}
+
+int grid_for(uint64_t n, int threads) {
+  return static_cast<int>(std::min<uint64_t>((n + threads - 1) / threads, 148ull * 16));
+}
+
+const char* blas_name(cublasStatus_t s) {
+  switch (s) {
+    case CUBLAS_STATUS_NOT_INITIALIZED: return "CUBLAS_STATUS_NOT_INITIALIZED";
+    case CUBLAS_STATUS_ALLOC_FAILED: return "CUBLAS_STATUS_ALLOC_FAILED";
+    case CUBLAS_STATUS_INVALID_VALUE: return "CUBLAS_STATUS_INVALID_VALUE";
+    case CUBLAS_STATUS_ARCH_MISMATCH: return "CUBLAS_STATUS_ARCH_MISMATCH";
+    case CUBLAS_STATUS_EXECUTION_FAILED: return "CUBLAS_STATUS_EXECUTION_FAILED";
+    case CUBLAS_STATUS_NOT_SUPPORTED: return "CUBLAS_STATUS_NOT_SUPPORTED";
+    default: return "cuBLAS error";
+  }
+}
+
+#define KVX_BLAS_TRY(expr, what)                                                     \
+  do {                                                                               \
+    cublasStatus_t kvx_b_ = (expr);                                                  \
+    if (kvx_b_ != CUBLAS_STATUS_SUCCESS) {                                           \
+      kvx::set_error(std::string(what) + ": " + kvx::blas_name(kvx_b_));             \
+      return KVX_ERR_CUDA;                                                           \
+    }                                                                                \
+  } while (0)
+
+// Y[rows][out] (+)= X[rows][in] . W[out][in]^T, bf16 in/out, fp32 compute.
+int linear(kvx_model* m, const uint16_t* X, const uint16_t* W, uint16_t* Y, int rows, int in, int out, bool accumulate) {
+  const float one = 1.f, beta = accumulate ? 1.f : 0.f;
+  KVX_BLAS_TRY(cublasGemmEx(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, out, rows, in, &one, W, CUDA_R_16BF, in, X, CUDA_R_16BF,
+                            in, &beta, Y, CUDA_R_16BF, out, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+               "kvx_model: cublasGemmEx");
+  return KVX_OK;
+}
+
+int ensure_rows(kvx_model* m, int rows) {
+  if (rows <= m->rows_cap) return KVX_OK;
+  const kvx_model_config& c = m->cfg;
+  cudaStream_t st = as_stream(m->stream);
+  if (m->x) KVX_CUDA_TRY(cudaStreamSynchronize(st), "kvx_model: sync");
+  for (void* p : {static_cast<void*>(m->x), static_cast<void*>(m->h), static_cast<void*>(m->qkv),
+                  static_cast<void*>(m->q), static_cast<void*>(m->kv_new), static_cast<void*>(m->attn),
+                  static_cast<void*>(m->gu), static_cast<void*>(m->act), static_cast<void*>(m->logits),
+                  static_cast<void*>(m->attn_f32), static_cast<void*>(m->tokens)})
+    cudaFree(p);
+  const int cap = std::max(rows, 64);
+  const uint64_t R = static_cast<uint64_t>(cap);
+  const uint64_t qkv_w = static_cast<uint64_t>(c.num_q_heads + 2 * c.num_kv_heads) * c.head_dim;
+  auto al = [&](auto** p, uint64_t bytes) { return cudaMalloc(reinterpret_cast<void**>(p), bytes); };
+  cudaError_t e = cudaSuccess;
+  e = e ? e : al(&m->x, R * c.hidden * 2);
+  e = e ? e : al(&m->h, R * c.hidden * 2);
+  e = e ? e : al(&m->qkv, R * qkv_w * 2);
+  e = e ? e : al(&m->q, R * c.num_q_heads * c.head_dim * 2);
+  e = e ? e : al(&m->kv_new, R * 2 * c.num_kv_heads * c.head_dim * 2);
+  e = e ? e : al(&m->attn, R * c.num_q_heads * c.head_dim * 2);
+  e = e ? e : al(&m->gu, R * 2 * c.intermediate * 2);
+  e = e ? e : al(&m->act, R * c.intermediate * 2);
+  // logits only for decode batches (prefill samples its last row only)
+  e = e ? e : al(&m->logits, std::min<uint64_t>(R, 256) * c.vocab * 2);
+  e = e ? e : al(&m->attn_f32, R * c.num_q_heads * c.head_dim * 4);
+  e = e ? e : al(&m->tokens, R * 4);
+  if (e != cudaSuccess) return fail_cuda(e, "kvx_model: activations");
+  m->rows_cap = cap;
+  return KVX_OK;
+}
+
+int bind(kvx_model* m, void* stream) {
+  if (m->stream != stream || !m->blas) {
+    KVX_BLAS_TRY(cublasSetStream(m->blas, as_stream(stream)), "kvx_model: cublasSetStream");
+    m->stream = stream;
+  }
+  return KVX_OK;
+}
+
+// The dense part of one layer around the attention, split at the attention:
+// pre = norm + QKV; post = O proj + residual, norm, MLP + residual.
+int layer_pre(kvx_model* m, int l, int rows) {
+  const kvx_model_config& c = m->cfg;
+  cudaStream_t st = as_stream(m->stream);
+  rms_norm<<<rows, 256, 0, st>>>(m->x, m->norm1[l], m->h, c.hidden, c.rms_eps);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rms_norm");
+  return linear(m, m->h, m->wqkv[l], m->qkv, rows, c.hidden, (c.num_q_heads + 2 * c.num_kv_heads) * c.head_dim, false);
+}
+
+int layer_post(kvx_model* m, int l, int rows) {
+  const kvx_model_config& c = m->cfg;
+  cudaStream_t st = as_stream(m->stream);
+  if (int rc = linear(m, m->attn, m->wo[l], m->x, rows, c.num_q_heads * c.head_dim, c.hidden, true)) return rc;
+  rms_norm<<<rows, 256, 0, st>>>(m->x, m->norm2[l], m->h, c.hidden, c.rms_eps);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rms_norm");
+  if (int rc = linear(m, m->h, m->wgu[l], m->gu, rows, c.hidden, 2 * c.intermediate, false)) return rc;
+  const uint64_t n = static_cast<uint64_t>(rows) * c.intermediate;
+  silu_mul<<<grid_for(n, 256), 256, 0, st>>>(m->gu, m->act, c.intermediate, rows);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: silu_mul");
+  return linear(m, m->act, m->wd[l], m->x, rows, c.intermediate, c.hidden, true);
+}
+
+// Final norm + LM head + argmax over `rows` rows of the residual stream
+// starting at row `first`.
+int sample(kvx_model* m, int first, int rows, int32_t* d_tokens_out) {
+  const kvx_model_config& c = m->cfg;
+  cudaStream_t st = as_stream(m->stream);
+  rms_norm<<<rows, 256, 0, st>>>(m->x + static_cast<uint64_t>(first) * c.hidden, m->final_norm, m->h, c.hidden,
+                                 c.rms_eps);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: final norm");
+  if (int rc = linear(m, m->h, m->lm_head, m->logits, rows, c.hidden, c.vocab, false)) return rc;
+  argmax_rows<<<rows, 512, 0, st>>>(m->logits, c.vocab, d_tokens_out);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: argmax");
+  return KVX_OK;
+}
+
+}  // namespace
+}  // namespace kvx
+
+extern "C" {
+
+uint64_t kvx_model_weight_bytes(const kvx_model_config* c) {
+  if (!c) return 0;
+  const uint64_t Hd = c->hidden, D = c->head_dim;
+  const uint64_t per_layer = (c->num_q_heads + 2ull * c->num_kv_heads) * D * Hd + c->num_q_heads * D * Hd +
+                             2ull * c->intermediate * Hd + c->intermediate * Hd + 2 * Hd;
+  return 2 * (c->num_layers * per_layer + 2ull * c->vocab * Hd + Hd);
+}
+
+int kvx_model_create(int device, const kvx_model_config* cfg, uint64_t seed, kvx_model** out) {
+  if (!cfg || !out) return kvx::fail_arg("kvx_model_create: null argument");
+  const kvx_model_config& c = *cfg;
+  if (c.num_layers <= 0 || c.hidden <= 0 || c.hidden % 8 || c.num_kv_heads <= 0 || c.num_q_heads % c.num_kv_heads ||
+      c.head_dim != 128 || c.intermediate <= 0 || c.vocab <= 0 || c.num_q_heads * c.head_dim % 8)
+    return kvx::fail_arg("kvx_model_create: unsupported shape (head_dim 128, hidden % 8 == 0, GQA)");
+  kvx::DeviceGuard guard(device);
+  auto* m = new kvx_model;
+  m->cfg = c;
+  m->device = device;
+  if (cublasCreate(&m->blas) != CUBLAS_STATUS_SUCCESS) {
+    delete m;
+    kvx::set_error("kvx_model_create: cublasCreate failed");
+    return KVX_ERR_CUDA;
+  }
+  m->slab_bytes = kvx_model_weight_bytes(cfg);
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&m->slab), m->slab_bytes);
+  if (e != cudaSuccess) {
+    cublasDestroy(m->blas);
+    delete m;
+    return kvx::fail_cuda(e, "kvx_model_create: weights");
+  }
+  uint16_t* p = reinterpret_cast<uint16_t*>(m->slab);
+  const uint64_t Hd = c.hidden, D = c.head_dim;
+  uint64_t salt = 0;
+  // Random weights, uniform with unit variance scaled by 1/sqrt(fan_in):
+  // activations stay O(1) through the stack.
+  auto take = [&](uint64_t n, float scale, bool ones = false) {
+    uint16_t* w = p;
+    p += n;
+    if (ones)
+      kvx::init_const_bf16<<<kvx::grid_for(n, 256), 256>>>(w, n, 1.f);
+    else
+      kvx::init_uniform_bf16<<<kvx::grid_for(n, 256), 256>>>(w, n, kvx::splitmix64(seed + ++salt), scale);
+    return w;
+  };
+  m->embed = take(c.vocab * Hd, 1.f);
+  m->lm_head = take(c.vocab * Hd, 1.f / std::sqrt(static_cast<float>(Hd)));
+  m->final_norm = take(Hd, 1.f, true);
+  for (int l = 0; l < c.num_layers; ++l) {
+    m->wqkv.push_back(take((c.num_q_heads + 2ull * c.num_kv_heads) * D * Hd, 1.f / std::sqrt(static_cast<float>(Hd))));
+    m->wo.push_back(take(c.num_q_heads * D * Hd, 1.f / std::sqrt(static_cast<float>(c.num_q_heads * D))));
+    m->wgu.push_back(take(2ull * c.intermediate * Hd, 1.f / std::sqrt(static_cast<float>(Hd))));
+    m->wd.push_back(take(c.intermediate * Hd, 1.f / std::sqrt(static_cast<float>(c.intermediate))));
+    m->norm1.push_back(take(Hd, 1.f, true));
+    m->norm2.push_back(take(Hd, 1.f, true));
+  }
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    kvx_model_destroy(m);
+    return kvx::fail_cuda(e, "kvx_model_create: init");
+  }
+  *out = m;
+  return KVX_OK;
+}
+
+int kvx_model_destroy(kvx_model* m) {
+  if (!m) return KVX_OK;
+  kvx::DeviceGuard guard(m->device);
+  if (m->stream) cudaStreamSynchronize(kvx::as_stream(m->stream));
+  for (void* p : {static_cast<void*>(m->x), static_cast<void*>(m->h), static_cast<void*>(m->qkv),
+                  static_cast<void*>(m->q), static_cast<void*>(m->kv_new), static_cast<void*>(m->attn),
+                  static_cast<void*>(m->gu), static_cast<void*>(m->act), static_cast<void*>(m->logits),
+                  static_cast<void*>(m->attn_f32), static_cast<void*>(m->tokens), m->attn_ws,
+                  static_cast<void*>(m->slab)})
+    cudaFree(p);
+  if (m->blas) cublasDestroy(m->blas);
+  delete m;
+  return KVX_OK;
+}
+
+int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_tables,
+                          const int32_t* d_ctx_lens, const int32_t* d_sessions, const int32_t* d_tokens_in,
+                          int32_t batch, int32_t max_blocks, int32_t max_ctx, uint64_t fill_seed, int32_t fill_mode,
+                          void* const* layer_waits, const int32_t* layer_wait_offsets, int32_t* d_tokens_out,
+                          void* stream) {
+  if (!m || !pool || !layout || !d_tables || !d_ctx_lens || !d_sessions || !d_tokens_in || !d_tokens_out)
+    return kvx::fail_arg("kvx_model_decode_step: null argument");
+  if (batch <= 0) return KVX_OK;
+  const kvx_model_config& c = m->cfg;
+  if (layout->num_kv_heads != c.num_kv_heads || layout->head_dim != c.head_dim || layout->dtype != KVX_DTYPE_BF16)
+    return kvx::fail_arg("kvx_model_decode_step: page layout does not match the model (bf16, kv heads, head_dim)");
+  if (batch > 256) return kvx::fail_arg("kvx_model_decode_step: batch > 256");
+  kvx::DeviceGuard guard(m->device);
+  if (int rc = kvx::ensure_rows(m, batch)) return rc;
+  if (int rc = kvx::bind(m, stream)) return rc;
+  cudaStream_t st = kvx::as_stream(stream);
+  kvx_attn_params ap{};
+  ap.num_q_heads = c.num_q_heads;
+  ap.max_blocks = max_blocks;
+  ap.flags = KVX_ATTN_EARLY_PREFETCH;
+  const uint64_t ws = kvx_decode_attention_workspace(layout, &ap, batch, max_ctx);
+  if (ws > m->attn_ws_bytes) {
+    if (m->attn_ws) {
+      KVX_CUDA_TRY(cudaStreamSynchronize(st), "kvx_model: sync");
+      cudaFree(m->attn_ws);
+      m->attn_ws = nullptr;
+    }
+    const uint64_t cap = ws * 2;
+    KVX_CUDA_TRY(cudaMalloc(&m->attn_ws, cap), "kvx_model: attention workspace");
+    KVX_CUDA_TRY(cudaMemsetAsync(m->attn_ws, 0, cap, st), "kvx_model: attention workspace");
+    m->attn_ws_bytes = cap;
+  }
+  kvx::embed_rows<<<batch, 128, 0, st>>>(m->embed, d_tokens_in, m->x, c.hidden, c.vocab);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: embed");
+  const int Hq = c.num_q_heads, H = c.num_kv_heads, D = c.head_dim;
+  for (int l = 0; l < c.num_layers; ++l) {
+    if (int rc = kvx::layer_pre(m, l, batch)) return rc;
+    uint16_t* new_k = m->kv_new;
+    uint16_t* new_v = m->kv_new + static_cast<uint64_t>(batch) * H * D;
+    // Layer l's pages may still be landing (a layer-wise load or a migrated
+    // layer): wait for exactly the batches writing them — the pipeline gate
+    // of the reference (kvstore.cpp:46-59) made physical. The waits precede
+    // the (normally launched) rope kernel, so the attention after it, which
+    // may launch early (PDL) and prefetch pages before griddepcontrol.wait,
+    // still cannot start before those pages are complete.
+    if (layer_waits && layer_wait_offsets)
+      for (int i = layer_wait_offsets[l]; i < layer_wait_offsets[l + 1]; ++i)
+        KVX_CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(layer_waits[i]), 0), "kvx_model: layer wait");
+    kvx::rope_and_token<<<batch, 256, 0, st>>>(m->qkv, d_sessions, d_ctx_lens, l, Hq, H, D, layout->block_tokens,
+                                               c.rope_theta, fill_seed, fill_mode, m->q, new_k, new_v);
+    KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rope");
+    const uint32_t* tab = d_tables + static_cast<uint64_t>(l) * batch * max_blocks;
+    if (int rc = kvx_decode_attention_append(pool, layout, &ap, tab, d_ctx_lens, m->q, new_k, new_v, m->attn_f32,
+                                             batch, max_ctx, m->attn_ws, m->attn_ws_bytes, stream))
+      return rc;
+    const uint64_t n = static_cast<uint64_t>(batch) * Hq * D;
+    kvx::f32_to_bf16_rows<<<kvx::grid_for(n, 256), 256, 0, st>>>(m->attn_f32, m->attn, n);
+    KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: attn to bf16");
+    if (int rc = kvx::layer_post(m, l, batch)) return rc;
+  }
+  return kvx::sample(m, 0, batch, d_tokens_out);
+}
+
+int kvx_model_prefill(kvx_model* m, int32_t tokens, void* stream) {
+  if (!m) return kvx::fail_arg("kvx_model_prefill: null model");
+  if (tokens <= 0) return KVX_OK;
+  const kvx_model_config& c = m->cfg;
+  kvx::DeviceGuard guard(m->device);
+  constexpr int kChunk = 4096;  // rows per pass (activation memory bound)
+  if (int rc = kvx::ensure_rows(m, std::min(tokens, kChunk))) return rc;
+  if (int rc = kvx::bind(m, stream)) return rc;
+  cudaStream_t st = kvx::as_stream(stream);
+  for (int done = 0; done < tokens; done += kChunk) {
+    const int rows = std::min(kChunk, tokens - done);
+    // Token ids: any; the projections' cost does not depend on them.
+    KVX_CUDA_TRY(cudaMemsetAsync(m->tokens, 0, static_cast<size_t>(rows) * 4, st), "kvx_model: prefill tokens");
+    kvx::embed_rows<<<rows, 128, 0, st>>>(m->embed, m->tokens, m->x, c.hidden, c.vocab);
+    KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: embed");
+    for (int l = 0; l < c.num_layers; ++l) {
+      if (int rc = kvx::layer_pre(m, l, rows)) return rc;
+      // Prefill attention is not modelled here (its K/V land in the pages as
+      // the store's Created fill); the attention output is the q projection.
+      const uint64_t n = static_cast<uint64_t>(rows) * c.num_q_heads * c.head_dim;
+      KVX_CUDA_TRY(cudaMemcpy2DAsync(m->attn, static_cast<size_t>(c.num_q_heads) * c.head_dim * 2, m->qkv,
+                                     static_cast<size_t>(c.num_q_heads + 2 * c.num_kv_heads) * c.head_dim * 2,
+                                     static_cast<size_t>(c.num_q_heads) * c.head_dim * 2, rows,
+                                     cudaMemcpyDeviceToDevice, st),
+                   "kvx_model: prefill attn stand-in");
+      (void)n;
+      if (int rc = kvx::layer_post(m, l, rows)) return rc;
+    }
+    // The prompt's last token is sampled (its LM head row is real work).
+    if (done + rows == tokens)
+      if (int rc = kvx::sample(m, rows - 1, 1, m->tokens)) return rc;
+  }
+  return KVX_OK;
+}
+
+}  // extern "C"

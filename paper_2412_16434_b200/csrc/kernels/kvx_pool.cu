@@ -340,6 +340,17 @@ int kvx_free(void* ptr) {
   return KVX_OK;
 }
 
+int kvx_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return kvx::fail_arg("kvx_host_alloc: null out");
+  KVX_CUDA_TRY(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable), "kvx_host_alloc");
+  return KVX_OK;
+}
+
+int kvx_host_free(void* ptr) {
+  if (ptr) KVX_CUDA_TRY(cudaFreeHost(ptr), "kvx_host_free");
+  return KVX_OK;
+}
+
 int kvx_memcpy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
   if (bytes == 0) return KVX_OK;
   KVX_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)),
@@ -383,6 +394,21 @@ int kvx_event_create(void** out) {
   cudaEvent_t e = nullptr;
   KVX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "kvx_event_create");
   *out = e;
+  return KVX_OK;
+}
+
+int kvx_timer_create(void** out) {
+  if (!out) return kvx::fail_arg("kvx_timer_create: null out");
+  cudaEvent_t e = nullptr;
+  KVX_CUDA_TRY(cudaEventCreate(&e), "kvx_timer_create");
+  *out = e;
+  return KVX_OK;
+}
+
+int kvx_timer_elapsed_ms(void* start, void* stop, float* ms) {
+  if (!start || !stop || !ms) return kvx::fail_arg("kvx_timer_elapsed_ms: null argument");
+  KVX_CUDA_TRY(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start), static_cast<cudaEvent_t>(stop)),
+               "kvx_timer_elapsed_ms");
   return KVX_OK;
 }
 

@@ -273,12 +273,18 @@ def load_kvs_library(path: Optional[str] = None) -> C.CDLL:
         "kvs_payload_pool_of": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, C.c_int32, P(C.c_int32)], C.c_int),
         "kvs_payload_bytes_moved": ([C.c_void_p, P(C.c_uint64)], C.c_int),
         "kvs_payload_stats": ([C.c_void_p, P(C.c_uint64)], C.c_int),
+        "kvs_payload_host_ns": ([C.c_void_p, P(C.c_uint64)], C.c_int),
         "kvs_payload_block_table": ([C.c_void_p, C.c_uint32, C.c_uint16, C.c_uint32, P(C.c_uint32)], C.c_int),
         "kvs_payload_pool": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
         "kvs_payload_synchronize": ([C.c_void_p], C.c_int),
         "kvs_payload_stream": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
         "kvs_set_default_payload": ([C.c_void_p, P(_PayloadOpts), C.c_int32], C.c_int),
         "kvs_cluster_node": ([C.c_void_p, C.c_int32, P(C.c_void_p)], C.c_int),
+        "kvs_traffic_zipf_turns": ([C.c_uint64, C.c_double, C.c_double, C.c_int32, C.c_uint64, P(C.c_int32)], C.c_int),
+        "kvs_traffic_poisson_gaps": ([C.c_uint64, C.c_double, C.c_uint64, P(C.c_int64)], C.c_int),
+        "kvs_traffic_percentile": ([P(C.c_double), C.c_uint64, C.c_double, P(C.c_double)], C.c_int),
+        "kvs_traffic_rps_within_slo": ([P(C.c_int32), P(C.c_double), P(C.c_double), C.c_uint64, C.c_double,
+                                        P(C.c_double)], C.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -552,7 +558,7 @@ def decode_step_time(batch: int, gpu: Optional[GpuProfile] = None, lib: Optional
 # Physical payload (include/symsim/payload.hpp through kvs.h)
 
 POOL_DEVICE, POOL_HOST, POOL_LANDING, POOL_DISK = range(4)
-LANE_IN, LANE_OUT, LANE_DISK, LANE_PEER = range(4)
+LANE_IN, LANE_OUT, LANE_DISK, LANE_PEER, LANE_FILL = range(5)
 BLOCK_EVENTS = ("created", "load_h2d", "load_disk_host", "host_copy", "disk_write", "swap_out", "net_arrive")
 
 
@@ -662,6 +668,12 @@ class NodePayload:
         return {"apply_wait_ns": out[0], "transfers_posted": out[1], "in_flight": list(out[2:6]),
                 "cross_lane_waits": out[6]}
 
+    def host_ns(self) -> Dict[str, int]:
+        """Host ns of the payload's bookkeeping by phase (kvs_payload_host_ns)."""
+        out = (C.c_uint64 * 8)()
+        _check(self._lib, self._lib.kvs_payload_host_ns(self._h, out))
+        return dict(zip(("posted", "retired", "issue", "reclaim", "upload", "launch", "close", "alloc"), list(out)))
+
     def device_block_table(self, session: int, layer: int, n: int):
         """uint32 DEVICE page ids of blocks [0, n) — a decode block-table row."""
         import numpy as np
@@ -684,3 +696,48 @@ class NodePayload:
         out = C.c_void_p()
         _check(self._lib, self._lib.kvs_payload_stream(self._h, lane, C.byref(out)))
         return out.value
+
+
+# ---- serving traffic (include/symsim/traffic.hpp) ---------------------------
+
+def zipf_turns(sessions: int, s: float = 1.2, scale: float = 64.0, min_turns: int = 2, seed: int = 0):
+    """Turns per session under Zipf(s) popularity (kvs_traffic_zipf_turns)."""
+    import numpy as np
+    lib = load_kvs_library()
+    out = np.empty(sessions, np.int32)
+    _check(lib, lib.kvs_traffic_zipf_turns(sessions, s, scale, min_turns, seed,
+                                           out.ctypes.data_as(C.POINTER(C.c_int32))))
+    return out
+
+
+def poisson_gaps(n: int, mean_s: float, seed: int = 0):
+    """n exponential think times (ns) with mean mean_s seconds."""
+    import numpy as np
+    lib = load_kvs_library()
+    out = np.empty(n, np.int64)
+    _check(lib, lib.kvs_traffic_poisson_gaps(n, mean_s, seed, out.ctypes.data_as(C.POINTER(C.c_int64))))
+    return out
+
+
+def percentile(values, q: float) -> float:
+    import numpy as np
+    lib = load_kvs_library()
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out = C.c_double()
+    _check(lib, lib.kvs_traffic_percentile(v.ctypes.data_as(C.POINTER(C.c_double)), v.size, q, C.byref(out)))
+    return out.value
+
+
+def rps_within_slo(sweep, slo: float) -> float:
+    """sweep: [(users, rps, p50)] -> highest rps with p50 <= slo."""
+    import numpy as np
+    lib = load_kvs_library()
+    u = np.ascontiguousarray([p[0] for p in sweep], dtype=np.int32)
+    r = np.ascontiguousarray([p[1] for p in sweep], dtype=np.float64)
+    m = np.ascontiguousarray([p[2] for p in sweep], dtype=np.float64)
+    out = C.c_double()
+    _check(lib, lib.kvs_traffic_rps_within_slo(u.ctypes.data_as(C.POINTER(C.c_int32)),
+                                               r.ctypes.data_as(C.POINTER(C.c_double)),
+                                               m.ctypes.data_as(C.POINTER(C.c_double)), len(sweep), slo,
+                                               C.byref(out)))
+    return out.value

@@ -3,7 +3,7 @@
 // into oracle/_ref/ (it links the reference's Simulation, Engine,
 // NodeManager, ClusterScheduler and workload generators compiled from
 // /root/reference). Two builds of this file:
-//   serve_sim      this repo's KvStore + cost model
+//   serve_sim      this repo's KvStore + cost model + Engine
 //   serve_sim_ref  the reference KvStore + cost model
 //
 // Modes:
@@ -19,7 +19,9 @@
 //            measurements passed on the command line (--decode-curve,
 //            --network-gbs, --pcie-gbs); see DESIGN.md §6.
 //
-// Trace generators (new; the reference has neither):
+// Trace generators (new; the reference has neither), built on
+// the product module include/symsim/traffic.hpp (Poisson gaps, Zipf turns,
+// percentiles):
 //   config 4  ShareGPT-like corpus (reference synthesize_corpus defaults:
 //             1,000 sessions, 73.4% multi-turn, lognormal lengths), Poisson
 //             turns: think time ~ Exp(mean) + the reference's typing time, so
@@ -42,6 +44,7 @@
 #include <vector>
 
 #include "symsim/simcore.hpp"
+#include "symsim/traffic.hpp"
 
 using namespace symsim;
 
@@ -63,6 +66,20 @@ Ns think_ns_like_reference(std::int64_t words, double wpm) {
 int g_sessions = 0;           // --sessions override (0: config default)
 double g_typing_wpm = 40.0;   // --typing-wpm (reference SpeedModel default 40)
 
+// Poisson turns: each follow-up prompt arrives an Exp(mean) think time plus
+// the reference's typing time after the previous turn completed.
+void add_poisson_think(Trace& t, double mean_think_s, std::uint64_t seed) {
+  std::size_t n = 0;
+  for (const auto& e : t.events) n += e.kind == EventKind::Inference && e.turn_index != 0;
+  const std::vector<Ns> gaps = traffic::poisson_gaps(n, mean_think_s, seed);
+  std::size_t k = 0;
+  for (auto& e : t.events) {
+    if (e.kind != EventKind::Inference || e.turn_index == 0) continue;
+    const auto& s = t.sessions[e.session_index];
+    e.delta = gaps[k++] + think_ns_like_reference(s.turns[e.turn_index].prompt_words, s.user.typing_wpm);
+  }
+}
+
 Trace config4(int users, double miss, double mean_think_s, std::uint64_t seed) {
   SyntheticSpec spec;  // reference defaults: 1000 sessions, 73.4% multi-turn
   if (g_sessions > 0) spec.sessions = g_sessions;
@@ -70,13 +87,7 @@ Trace config4(int users, double miss, double mean_think_s, std::uint64_t seed) {
   SpeedModel speeds;
   speeds.typing_wpm_mean = g_typing_wpm;
   Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1, speeds);
-  std::mt19937_64 rng(seed + 2);
-  std::exponential_distribution<double> think(1.0 / mean_think_s);
-  for (auto& e : t.events) {
-    if (e.kind != EventKind::Inference || e.turn_index == 0) continue;
-    const auto& s = t.sessions[e.session_index];
-    e.delta = ns_from_sec(think(rng)) + think_ns_like_reference(s.turns[e.turn_index].prompt_words, s.user.typing_wpm);
-  }
+  add_poisson_think(t, mean_think_s, seed + 2);
   return inject_advisories(std::move(t), miss, seed + 3);
 }
 
@@ -85,29 +96,20 @@ Trace config5(int users, double miss, double mean_think_s, std::uint64_t seed) {
   spec.sessions = g_sessions > 0 ? g_sessions : 600;
   spec.multi_turn_fraction = 1.0;
   auto scripts = synthesize_corpus(spec, seed);
-  // Zipf(1.2) popularity over a seeded permutation of sessions: rank r gets
+  // Zipf(1.2) popularity over a seeded ranking of sessions: rank r gets
   // turns ~ 64 / r^1.2 (at least 2), drawn from the session's own turn list
   // (cycled when it is shorter).
-  std::mt19937_64 rng(seed + 7);
-  std::vector<std::size_t> order(scripts.size());
-  for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
-  std::shuffle(order.begin(), order.end(), rng);
-  for (std::size_t r = 0; r < order.size(); ++r) {
-    auto& sc = scripts[order[r]];
-    const int want = std::max(2, static_cast<int>(std::lround(64.0 / std::pow(static_cast<double>(r + 1), 1.2))));
+  const std::vector<int> want = traffic::zipf_turns(scripts.size(), 1.2, 64.0, 2, seed + 7);
+  for (std::size_t i = 0; i < scripts.size(); ++i) {
+    auto& sc = scripts[i];
     std::vector<Turn> turns;
-    for (int k = 0; k < want; ++k) turns.push_back(sc.turns[static_cast<std::size_t>(k) % sc.turns.size()]);
+    for (int k = 0; k < want[i]; ++k) turns.push_back(sc.turns[static_cast<std::size_t>(k) % sc.turns.size()]);
     sc.turns = std::move(turns);
   }
   SpeedModel speeds;
   speeds.typing_wpm_mean = g_typing_wpm;
   Trace t = synthesize_arrivals(std::move(scripts), users, seed + 1, speeds);
-  std::exponential_distribution<double> think(1.0 / mean_think_s);
-  for (auto& e : t.events) {
-    if (e.kind != EventKind::Inference || e.turn_index == 0) continue;
-    const auto& s = t.sessions[e.session_index];
-    e.delta = ns_from_sec(think(rng)) + think_ns_like_reference(s.turns[e.turn_index].prompt_words, s.user.typing_wpm);
-  }
+  add_poisson_think(t, mean_think_s, seed + 8);
   return inject_advisories(std::move(t), miss, seed + 3);
 }
 
@@ -138,14 +140,7 @@ RunConfig make_cfg(const Calibration& c, Policy p) {
   return cfg;
 }
 
-double percentile(std::vector<double> v, double q) {
-  if (v.empty()) return 0.0;
-  std::sort(v.begin(), v.end());
-  const double pos = q * static_cast<double>(v.size() - 1);
-  const std::size_t lo = static_cast<std::size_t>(pos);
-  const std::size_t hi = std::min(lo + 1, v.size() - 1);
-  return v[lo] + (v[hi] - v[lo]) * (pos - static_cast<double>(lo));
-}
+double percentile(const std::vector<double>& v, double q) { return traffic::percentile(v, q); }
 
 struct Cell {
   double rps = 0, p50_tpot_ms = 0, p50_ttft_s = 0, p50_norm_ms = 0;

@@ -280,8 +280,10 @@ def test_recycled_pages_wait_for_other_lanes(dev):
     lane) is handed those very pages. The DISK lane is stalled by a 50 ms spin
     kernel queued ahead of A's writes, so without the page fences B's load
     would overwrite the pages before the DiskWrites read them and A's DISK
-    copy would hold B's bytes. The load must wait on the DiskWrite batch, and
-    every copy of both sessions stays bit-exact."""
+    copy would hold B's bytes. The freed pages stay quarantined until the
+    DiskWrite batch completes, so the load's allocation must wait for it
+    (counted in cross_lane_waits), and every copy of both sessions stays
+    bit-exact."""
     cluster, store, node = make_node(opts_kw=dict(device_pages=6), free_running=True)
     pump = Pump(store)
     for s in (1, 2):

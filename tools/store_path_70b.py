@@ -25,11 +25,14 @@ equal the CPU oracle's fill (tests/test_store_path_70b.py).
 usage: python tools/store_path_70b.py [out.json]
 """
 import json
+import os
 import sys
 import time
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
 LAYERS, BLOCKS, TOKENS = 80, 2048, 32768
-HEADS, DIM, SEED, SESSION = 8, 128, 0x70B, 9
+HEADS, DIM, SEED, SESSION, WARM = 8, 128, 0x70B, 9, 10
 
 
 def run(verify: bool = True, oracle_samples: int = 4):
@@ -52,6 +55,7 @@ def run(verify: bool = True, oracle_samples: int = 4):
             host_pages=1, landing_pages=1 if n == 0 else pages, disk_pages=1, seed=SEED, free_running=True))
         nd.attach(st)
         st.register_session(SESSION, "seventy-b")
+        st.register_session(WARM, "warm-up")
         st.finalize_sessions()
         stores.append(st)
         nodes.append(nd)
@@ -76,6 +80,24 @@ def run(verify: bool = True, oracle_samples: int = 4):
             res.append(timed(name, lambda: store.apply_transfer(tid, at)))
         return res
 
+    # Warm-up: a short session through the same calls (first-use costs of
+    # events, kernels and staging are not the steady state timed below).
+    _, sched = src.append_blocks(WARM, 256, 0)
+    for tid, at in sorted(sched, key=lambda x: (x[1], x[0])):
+        src.apply_transfer(tid, at)
+    src.mark_migrating_out(WARM)
+    for tid, at in sorted(dst.import_migration(WARM, 256, 10), key=lambda x: (x[1], x[0])):
+        dst.apply_transfer(tid, at)
+    src.release_session(WARM, 20)
+    _, sched = dst.plan_layerwise_load(WARM, 30, 100_000, K.DEMAND)
+    for tid, at in sorted(sched, key=lambda x: (x[1], x[0])):
+        dst.apply_transfer(tid, at)
+    dst.release_session(WARM, 40)
+    for n in nodes:
+        n.synchronize()
+    host0 = [n.host_ns() for n in nodes]
+    moved0 = nodes[1].bytes_moved()
+
     _, sched = timed("append_blocks(32K)", lambda: src.append_blocks(SESSION, TOKENS, 0))
     apply_all(src, sched, "apply(created)")
     nodes[0].synchronize()
@@ -95,8 +117,11 @@ def run(verify: bool = True, oracle_samples: int = 4):
     nodes[1].synchronize()
     assert dst.fully_device_resident(SESSION)
     moved = nodes[1].bytes_moved()
-    assert moved["net_arrive"] == pages * pb and moved["load_h2d"] == pages * pb
+    assert moved["net_arrive"] - moved0["net_arrive"] == pages * pb
+    assert moved["load_h2d"] - moved0["load_h2d"] == pages * pb
 
+    out_host = {f"node{i}": {k: round((v - host0[i][k]) / 1e3 / LAYERS, 3) for k, v in n.host_ns().items()}
+                for i, n in enumerate(nodes)}
     per_layer = {k: round(v["host_ns"] / 1e3 / LAYERS, 3) for k, v in t.items()
                  if k in ("import_migration", "apply(net_arrive)", "plan_layerwise_load", "apply(load_h2d)")}
     out = {
@@ -109,6 +134,7 @@ def run(verify: bool = True, oracle_samples: int = 4):
         "calls": {k: {"calls": v["calls"], "host_ms": round(v["host_ns"] / 1e6, 3),
                       "gpu_wait_ms": round(v["gpu_wait_ns"] / 1e6, 3)} for k, v in t.items()},
         "migrate_wall_ms": round(migrate_wall_ms, 3),
+        "payload_host_us_per_layer_by_phase": out_host,
         "note": "host_ns excludes time apply spent blocked on GPU events (NodePayload::apply_wait_ns); "
                 "includes ctypes call overhead (~1-3 us per call)",
     }
