@@ -129,8 +129,10 @@ class NodePayload final : public TierBackend {
   // WRITING any of those pages (fills, layer-wise loads): the decode of the
   // layer waits on exactly those, which is the reference's pipeline gate
   // (kvstore.cpp:46-59) made physical. Reads of the pages (persists,
-  // migration pushes) are not waited for. False if a block has no DEVICE
-  // page at all.
+  // migration pushes) are not waited for. The handles stay valid until the
+  // next call that may retire events (any move, apply or sync); collecting
+  // every layer's waits first and then issuing them is safe. False if a
+  // block has no DEVICE page at all.
   bool decode_rows(const std::vector<std::pair<std::uint32_t, std::uint32_t>>& reqs, std::uint16_t layer,
                    std::uint32_t stride, std::uint32_t* out, std::vector<void*>& waits);
   // Which pool holds the block's `tier` copy (-1: none).
@@ -231,6 +233,7 @@ class NodePayload final : public TierBackend {
     kvx_pool* bounce = nullptr;  // pinned staging between HBM and a file-backed DISK pool
     void retire();
     void* event_for(std::uint64_t ticket);  // nullptr once complete
+    void* find_pending(std::uint64_t ticket) const;  // same, without retiring
     void drain();                           // after a stream sync: everything complete
     std::uint64_t last() const { return next - 1; }
   };

@@ -89,6 +89,7 @@ class GpuStepExecutor final : public StepExecutor {
     std::int64_t step_ns = 0, prefill_ns = 0;
     std::int64_t gated_layers = 0;      // layer attentions that waited on a load still landing
     std::int64_t attended_tokens = 0;   // sum over steps of the batch's context tokens
+    std::int64_t rows = 0;              // sum over steps of the batch size (tokens emitted)
     std::int64_t max_batch = 0;
     std::int64_t host_table_ns = 0;     // host time building the block tables
   };

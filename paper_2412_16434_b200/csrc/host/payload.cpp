@@ -123,6 +123,13 @@ void NodePayload::Lane::retire() {
 void* NodePayload::Lane::event_for(std::uint64_t ticket) {
   if (ticket <= done) return nullptr;
   retire();
+  return find_pending(ticket);
+}
+
+// Like event_for, but without retiring (destroying) completed events: a
+// caller collecting several lanes' events before using them all keeps every
+// handle alive this way.
+void* NodePayload::Lane::find_pending(std::uint64_t ticket) const {
   if (ticket <= done) return nullptr;
   const auto it = std::lower_bound(pending.begin(), pending.end(), std::make_pair(ticket, static_cast<void*>(nullptr)),
                                    [](const auto& a, const auto& b) { return a.first < b.first; });
@@ -481,7 +488,11 @@ bool NodePayload::decode_rows(const std::vector<std::pair<std::uint32_t, std::ui
         waits.push_back(f.event);
     }
   }
-  if (void* ev = fill ? lanes_[kLaneFill].event_for(fill) : nullptr) waits.push_back(ev);
+  // No retiring here: the executor collects all layers' waits before issuing
+  // them, so handles found for earlier layers must stay alive.
+  if (void* ev = fill ? lanes_[kLaneFill].find_pending(fill) : nullptr)
+    if (std::find(waits.begin() + static_cast<std::ptrdiff_t>(first_wait), waits.end(), ev) == waits.end())
+      waits.push_back(ev);
   return true;
 }
 

@@ -187,6 +187,7 @@ Ns GpuStepExecutor::decode_step(const std::vector<Row>& rows) {
     for (const auto& r : reqs) verified_pages_ += static_cast<std::uint64_t>(r.second) * L;
   }
   ++stats_.steps;
+  stats_.rows += B;
   stats_.step_ns += ns;
   stats_.max_batch = std::max<std::int64_t>(stats_.max_batch, B);
   return ns;

@@ -7,7 +7,13 @@ include/symsim/kvstore.hpp + costmodel.hpp. Every suite must give exactly the
 result it gives against the reference store itself: all pass,
 except the reference's own defect at test_engine.cpp:267 (its expected message
 predates engine.cpp:69-74 appending device_usage_debug()).
+
+The same suites are built a second time with this repo's Engine too
+(B200_ENGINE=1: include/symsim/engine.hpp + csrc/host/engine.cpp, modelled
+quanta) — test_engine, test_simcore, the property suites and the simulation
+suites then exercise the B200 engine and must give the same results.
 """
+import os
 import subprocess
 
 import pytest
@@ -29,11 +35,12 @@ SUITES = {
 }
 
 
-@pytest.fixture(scope="module")
-def harness(reference_present):
-    proc = subprocess.run(["bash", str(HARNESS), *SUITES], capture_output=True, text=True, timeout=900)
+@pytest.fixture(scope="module", params=["reference-engine", "b200-engine"])
+def harness(reference_present, request):
+    env = dict(os.environ, B200_ENGINE="1" if request.param == "b200-engine" else "0")
+    proc = subprocess.run(["bash", str(HARNESS), *SUITES], capture_output=True, text=True, timeout=900, env=env)
     assert proc.returncode == 0, proc.stdout + proc.stderr
-    return OUT
+    return OUT if request.param == "reference-engine" else ROOT / "build" / "ref_harness_b200eng"
 
 
 @pytest.mark.parametrize("suite", list(SUITES))
