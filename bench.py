@@ -15,9 +15,12 @@ permutation (K2) — the device half of a layer-wise migration. Inputs are
 Also reported: the fused page->page mover (K3), the other mover variant,
 paged decode attention (K4: 8B @8K batch 1/8/64, 70B @32K batch 1/4, the
 fused decode step), migration beside decode, the DISK tier as files, `e2e`
-through the store's own API (Symphony's swap: offload A + advised load B
-between pinned HOST and HBM pages, every step) with the raw kvx round trip
-in `detail`, and the CPU restatement on the host cores.
+through the store's own API — the reference arm's own operation, a session
+migration: mark_migrating_out -> import_migration -> apply every NetArrive
+(K3 push into the receiver's landing pool) -> release, block tables up and a
+probe page down inside the timed region — with Symphony's HOST<->HBM swap
+and the raw kvx round trip in `detail`, and the CPU restatement on the host
+cores.
 
 N>1 (config 3, Llama-3.1-70B KV shape @ 32K, ~10.7 GB per session):
 migration-plus-serving. Every rank decodes a batch of 70B @32K requests on
@@ -68,7 +71,14 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-NVLINK_PEAK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+# NVLink denominators. MEASURED_PEAKS.json (driver-written) carries no NVLink
+# figure; the profiling guide's measured peer copy (770 GB/s per direction on
+# this pool, /opt/skills/guides/B200_PROFILING.md) is the roofline
+# denominator, the north star's nominal 900 GB/s the second one.
+NVLINK_PEAK_GBS = 770.0
+NVLINK_NOMINAL_GBS = 900.0
+NVLINK_PEAK_PROVENANCE = ("measured peer copy per direction, B200_PROFILING.md (not in MEASURED_PEAKS.json); "
+                          "nominal 900 GB/s per direction reported beside it")
 
 
 def DECODE_FLAGS(kvx):  # noqa: N802 — a constant that needs the loaded module
@@ -178,14 +188,20 @@ def make_session(torch, kvx, np, cfg, seed, dev, pool_pages=None, fill=True):
     return layout, pool, d_src, d_dst, src_ids, dst_ids
 
 
+LAUNCHES = {"timed": 0}  # libkvx kernel launches inside the last time_events timed loop
+
+
 def time_events(torch, fn, steps, warmup, marks=1):
     """Runs fn(i, ev_list) steps times after warmup; fn records marks+1 events."""
+    from paper_2412_16434_b200 import kvx
     for i in range(warmup):
         fn(i, None)
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(marks + 1)] for _ in range(steps)]
+    n0 = kvx.launch_count()
     for i in range(steps):
         fn(i, evs[i])
+    LAUNCHES["timed"] = kvx.launch_count() - n0
     torch.cuda.synchronize()
     total = evs[0][0].elapsed_time(evs[-1][-1])
     parts = [[e[j].elapsed_time(e[j + 1]) for e in evs] for j in range(marks)]
@@ -214,6 +230,7 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
 
     with ClockSampler(dev.index) as clocks:
         total_ms, (pack_ms, unpack_ms) = time_events(torch, step, args.steps, args.warmup, marks=2)
+    launches = LAUNCHES["timed"]  # counted by libkvx (kvx_launch_count), not inferred
     # correctness of what was timed: the last unpack landed every page
     probe = torch.randint(0, n, (64,), device=dev)
     pv = pool.as_tensor()
@@ -259,18 +276,22 @@ def bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind):
     # sessions between the pinned HOST tier and HBM pages: Symphony's swap
     # (offload A, load advised B; 1 GiB each way, host<->device copies and
     # the store's bookkeeping inside the timed region, bytes verified).
-    e2e = None
+    # e2e (the headline against the reference arm): the same operation the
+    # reference arm times — a session's migration through the store API
+    # (mark_migrating_out -> import_migration -> apply every NetArrive ->
+    # release), with real pages moved by K3, block tables uploaded and a
+    # probe page read back inside the timed region.
+    e2e = None if args.skip_e2e else bench_store_migration(args, torch, np, kvx, dev)
     if store_cycle is not None:
         sw = store_cycle["swap"]
-        e2e = {"value": sw["value"], "unit": UNIT, "h2d_bytes_per_step": session_bytes,
-               "d2h_bytes_per_step": session_bytes, "ms_per_step": sw["ms_per_swap"], "steps": sw["swaps"],
-               "timing": "host wall clock around the store calls and the payload's completion",
-               "path": "kvs_offload_session(A: HBM pages -> pinned HOST) + kvs_plan_layerwise_load(B: pinned HOST "
-                       "-> HBM pages), NodePayload free-running, both PCIe directions"}
-        if e2e_kvx is not None:
-            extra["e2e_kvx_roundtrip"] = e2e_kvx
+        extra["e2e_store_swap"] = {
+            "value": sw["value"], "unit": UNIT, "h2d_bytes_per_step": session_bytes,
+            "d2h_bytes_per_step": session_bytes, "ms_per_step": sw["ms_per_swap"], "steps": sw["swaps"],
+            "path": "kvs_offload_session(A: HBM pages -> pinned HOST) + kvs_plan_layerwise_load(B: pinned HOST "
+                    "-> HBM pages), NodePayload free-running, both PCIe directions"}
+    if e2e_kvx is not None:
+        extra["e2e_kvx_roundtrip"] = e2e_kvx
     disk = None if args.skip_e2e else bench_disk(args, torch, np, kvx, cfg)
-    launches = 2 * args.steps
     return dict(value=value, ms_per_step=ms_per_step, extra=extra, clocks=clocks.summary(),
                 roofline={"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                           "frac": achieved / hbm_peak, "traffic": ncu_traffic(dom_name), "kernel": dom_name,
@@ -559,8 +580,10 @@ def background_migration(torch, kvx, decode, migrate, side, dev, session_bytes, 
     measured copy peak (what an ideal share of HBM would add)."""
     steps = 4
     floor = 2 * session_bytes / (hbm_peak * GB) * 1e3
-    out = {"decode_steps": steps, "decode_step_ms_alone": t_step, "nvlink_peak_gbs": NVLINK_PEAK_GBS,
-           "hbm_floor_extra_ms": floor, "variants": []}
+    out = {"decode_steps": steps, "decode_step_ms_alone": t_step, "hbm_peak_gbs": hbm_peak,
+           "hbm_floor_extra_ms": floor, "variants": [],
+           "note": "same-GPU HBM copy: hbm_frac is the migration's read + write bytes over the measured HBM copy "
+                   "peak while decode runs; no NVLink is involved on one GPU"}
     hi = torch.cuda.Stream(dev, priority=-5)   # clamped to the device's highest priority
     lo = torch.cuda.Stream(dev, priority=0)
     if sweep:
@@ -608,7 +631,7 @@ def background_migration(torch, kvx, decode, migrate, side, dev, session_bytes, 
             out["variants"].append({
                 "mover": mname, "max_ctas": cap or "all", "stage": f"{geo[0] // 1024}KiBx{geo[1]}" if geo else "default",
                 "priority_streams": prio, "migrate_ms": t_mig, "migrate_gbs": session_bytes / (t_mig * 1e-3) / GB,
-                "nvlink_frac": session_bytes / (t_mig * 1e-3) / GB / NVLINK_PEAK_GBS, "decode_ms": t_all,
+                "hbm_frac": 2 * session_bytes / (t_mig * 1e-3) / GB / hbm_peak, "decode_ms": t_all,
                 "decode_extra_ms": extra, "extra_over_floor": extra / floor})
     finally:
         for k, v in saved.items():
@@ -711,6 +734,89 @@ def bench_store_cycle(args, torch, np, kvx, dev):
            "path": "kvs_offload_session + kvs_plan_layerwise_load, NodePayload free-running (copy engines)"}
     res["swap"] = bench_store_swap(args, K, kvx, cfg, n, pb, dev)
     return res
+
+
+def bench_store_migration(args, torch, np, kvx, dev):
+    """The e2e headline, the same operation as the reference arm: a session's
+    migration through the store API (the reference's
+    Simulation::start_migration, simcore.cpp:132-141): kvs_mark_migrating_out
+    on the source node, kvs_import_migration on the receiver (one NetArrive
+    per layer, kvstore.cpp:744-789), every NetArrive applied in (complete_at,
+    id) order (kvstore.cpp:914-923), kvs_release_session on the source
+    (kvstore.cpp:710-736). With the payload free-running, each layer's arrival
+    is a K3 push of the source's HBM pages into the receiver's landing pool,
+    issued when import_migration schedules it and completed at apply. Two
+    nodes share this GPU (on a multi-GPU box the push crosses NVLink). Inside
+    the host-timed region per step: the store bookkeeping of both nodes, the
+    block-table uploads from host memory (the page-id lists of every layer,
+    H2D), the GPU moves, and a probe page read back to host memory (D2H);
+    the probe is verified against the block's content."""
+    from paper_2412_16434_b200 import kvstore as K
+    cfg = CFG_8B
+    blocks, n = session_pages(cfg)
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    gpu = K.GpuProfile(kv_bytes_per_token=cfg["layers"] * pb // cfg["block_tokens"], num_layers=cfg["layers"],
+                       hbm_capacity=100 * n * pb)
+    links = K.LinkProfile(network_bandwidth=770e9)
+    cluster = K.PayloadCluster()
+    stores, nodes = [], []
+    for node_id in range(2):
+        st = K.KvStore(gpu=gpu, links=links, opts=K.Options(node_id=node_id, write_behind=False,
+                                                           host_capacity=4 * n * pb))
+        nd = K.NodePayload(cluster, node_id, K.PayloadOptions(
+            device=dev.index, num_kv_heads=cfg["kv_heads"], head_dim=cfg["head_dim"], dtype=kvx.BF16,
+            device_pages=2 * n if node_id == 0 else 1, host_pages=1, landing_pages=2 * n if node_id else 1,
+            disk_pages=1, seed=17, free_running=True))
+        nd.attach(st)
+        stores.append(st)
+        nodes.append(nd)
+    src, dst = stores
+    steps = max(3, min(args.steps, 10))
+    for st in stores:
+        for i in range(steps + 1):
+            st.register_session(i, f"m{i}")
+        st.finalize_sessions()
+
+    def pump(store, sched):
+        for tid, at in sorted(sched, key=lambda t: (t[1], t[0])):
+            store.apply_transfer(tid, at)
+
+    layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
+    ref = kvx.Pool(1, pb, device=dev.index)
+    now, times, verified = 1_000_000, [], 0
+    rng = np.random.default_rng(3)
+    for i in range(steps + 1):
+        _, sched = src.append_blocks(i, cfg["ctx"], now)  # untimed: the session to migrate
+        pump(src, sched)
+        nodes[0].synchronize()
+        layer, block = int(rng.integers(cfg["layers"])), int(rng.integers(blocks))
+        t0 = time.perf_counter()
+        src.mark_migrating_out(i)
+        pump(dst, dst.import_migration(i, cfg["ctx"], now + 1))
+        src.release_session(i, now + 2)
+        probe = nodes[1].read_block(i, layer, block, K.HOST, pb)  # syncs the payload, D2H of one page
+        dt = time.perf_counter() - t0
+        if i:
+            times.append(dt)
+        kvx.fill_pages(ref, torch.zeros(1, dtype=torch.int32, device=dev),
+                       torch.tensor([[i, layer, block]], dtype=torch.int32, device=dev), 1, 17, layout,
+                       kvx.FILL_VALUES)
+        torch.cuda.synchronize()
+        assert probe is not None and np.array_equal(probe, ref.as_tensor().cpu().numpy()[0]), "migrated page differs"
+        verified += 1
+        dst.release_session(i, now + 3)  # untimed: frees the landing pages for the next step
+        now += 10_000_000_000
+    t = statistics.mean(times)
+    ids_bytes = 2 * n * 4  # source + destination page ids of every layer, uploaded per step
+    host = nodes[1].host_ns()
+    return {"value": n * pb / t / GB, "unit": UNIT, "h2d_bytes_per_step": ids_bytes, "d2h_bytes_per_step": pb,
+            "ms_per_step": 1e3 * t, "steps": len(times), "verified_probe_pages": verified,
+            "copies_declared": True,
+            "timing": "host wall clock around the store calls, the payload's GPU moves and the probe read",
+            "path": "kvs_mark_migrating_out(src) -> kvs_import_migration(dst) -> kvs_apply_transfer x32 "
+                    "(NetArrive: K3 push into dst's landing pool) -> kvs_release_session(src) -> probe page D2H",
+            "receiver_host_us_per_layer": {k: round(v / 1e3 / cfg["layers"] / (steps + 1), 2)
+                                           for k, v in host.items() if k in ("posted", "retired", "issue")}}
 
 
 def bench_store_swap(args, K, kvx, cfg, n, pb, dev):
@@ -861,6 +967,146 @@ def bench_e2e(args, torch, np, kvx, dev, cfg, layout, pool, d_dst):
                     "3 staging slots per direction, layers of consecutive steps streamed back to back"}
 
 
+def bench_store_ring(args, torch, np, kvx, rank, world):
+    """N>1 through the store API — the product path (config 3): the
+    reference's Simulation::start_migration (simcore.cpp:132-141) per session,
+    as the product runs it. One process drives a PayloadCluster of N nodes,
+    node i on cuda:i (rank 0; the other ranks only hold the barrier), each
+    node a KvStore + free-running NodePayload holding one Llama-3.1-70B @32K
+    session. A step migrates every session one hop around the ring at once:
+    mark_migrating_out on the holder, import_migration on the next node (80
+    NetArrives, each a K3 push of the holder's pages into the receiver's
+    landing pool, over NVLink when the nodes sit on different GPUs — peer
+    access enabled by the payload on import), every NetArrive applied in
+    (complete_at, id) order, release_session on the holder. The session
+    travels on from the receiver's landing pool in the next step.
+
+    Timing: CUDA events on each holder's PEER lane around the pushes; the
+    step time is the max over the N devices (their migrations run
+    concurrently); value = N x session bytes / that max. With --same-device
+    every node sits on cuda:0 (test mode)."""
+    import torch.distributed as dist
+    from paper_2412_16434_b200 import kvstore as K
+    cfg = dict(CFG_70B)
+    if args.layers:
+        cfg["layers"] = args.layers
+    L = cfg["layers"]
+    blocks, n = session_pages(cfg)
+    pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
+    if rank != 0:
+        dist.barrier()
+        return None
+    ndev = 1 if args.same_device else min(world, torch.cuda.device_count())
+    gpu = K.GpuProfile(kv_bytes_per_token=L * pb // cfg["block_tokens"], num_layers=L, hbm_capacity=4 * n * pb)
+    links = K.LinkProfile(network_bandwidth=NVLINK_PEAK_GBS * 1e9)
+    cluster = K.PayloadCluster()
+    stores, nodes = [], []
+    for i in range(world):
+        st = K.KvStore(gpu=gpu, links=links, opts=K.Options(node_id=i, write_behind=False, host_capacity=4 * n * pb))
+        nd = K.NodePayload(cluster, i, K.PayloadOptions(
+            device=i % ndev, num_kv_heads=cfg["kv_heads"], head_dim=cfg["head_dim"], dtype=kvx.BF16,
+            device_pages=n, host_pages=1, landing_pages=2 * n, disk_pages=1, seed=0x70B, free_running=True,
+            migrate_max_ctas=args.mig_ctas))
+        nd.attach(st)
+        for s_ in range(world):
+            st.register_session(s_, f"ring{s_}")
+        st.finalize_sessions()
+        stores.append(st)
+        nodes.append(nd)
+
+    def pump(store, sched):
+        for tid, at in sorted(sched, key=lambda t: (t[1], t[0])):
+            store.apply_transfer(tid, at)
+
+    now = 1_000_000
+    for i in range(world):  # node i creates session i (K5 fill on its GPU)
+        _, sched = stores[i].append_blocks(i, cfg["ctx"], now)
+        pump(stores[i], sched)
+    for nd in nodes:
+        nd.synchronize()
+    holder = list(range(world))  # holder[s] = node holding session s
+    peer_streams = [torch.cuda.ExternalStream(nd.stream(K.LANE_PEER), device=torch.device("cuda", nd.opts.device))
+                    for nd in nodes]
+
+    def step(timed):
+        nonlocal now
+        now += 10_000_000_000
+        evs = []
+        for s_ in range(world):
+            src = holder[s_]
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(peer_streams[src])
+                evs.append([src, e0])
+        scheds = []
+        for s_ in range(world):
+            src, dst = holder[s_], (holder[s_] + 1) % world
+            stores[src].mark_migrating_out(s_)
+            scheds.append((dst, stores[dst].import_migration(s_, cfg["ctx"], now)))  # posts the 80 pushes
+        for ev in evs:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(peer_streams[ev[0]])
+            ev.append(e1)
+        for dst, sched in scheds:
+            pump(stores[dst], sched)
+        for s_ in range(world):
+            stores[holder[s_]].release_session(s_, now + 1)
+            holder[s_] = (holder[s_] + 1) % world
+        for nd in nodes:
+            nd.synchronize()
+        return [e[1].elapsed_time(e[2]) for e in evs] if timed else None
+
+    for _ in range(max(1, args.warmup)):
+        step(False)
+    steps = max(1, min(args.steps, 10))
+    n0 = kvx.launch_count()
+    t0 = time.perf_counter()
+    per_step = [max(step(True)) for _ in range(steps)]
+    wall = (time.perf_counter() - t0) / steps
+    launches = kvx.launch_count() - n0
+    # What each node holds now is the session's creation content, bit for bit.
+    layout = kvx.PageLayout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], kvx.BF16)
+    import oracle.oracle as O  # checker only
+    rng = np.random.default_rng(11)
+    checked = 0
+    for s_ in range(world):
+        nd = nodes[holder[s_]]
+        for _ in range(4):
+            layer, block = int(rng.integers(L)), int(rng.integers(blocks))
+            want = np.zeros((1, pb), np.uint8)
+            O.fill_pages(want, pb, np.zeros(1, np.uint32), O.tags_array(s_, layer, block), 0x70B,
+                         O.Layout(cfg["kv_heads"], cfg["head_dim"], cfg["block_tokens"], 1), 1)
+            got = nd.read_block(s_, layer, block, K.HOST, pb)
+            assert got is not None and np.array_equal(got, want[0]), f"session {s_} layer {layer} block {block}"
+            checked += 1
+    del layout
+    t_mig = statistics.mean(per_step)
+    session_bytes = n * pb
+    achieved = session_bytes / (t_mig * 1e-3) / GB
+    dist.barrier()
+    host = {f"node{i}": {k: round(v / 1e3 / L / (steps + max(1, args.warmup)), 2)
+                         for k, v in nd.host_ns().items() if k in ("posted", "retired")}
+            for i, nd in enumerate(nodes)}
+    return dict(value=world * session_bytes / (t_mig * 1e-3) / GB, ms_per_step=t_mig,
+                clocks={"note": "not sampled on the store path (one process drives every device)"},
+                session_bytes=session_bytes, cfg=cfg, verified=True, serving=None,
+                e2e={"value": world * session_bytes / wall / GB, "unit": UNIT, "h2d_bytes_per_step": world * 2 * n * 4,
+                     "d2h_bytes_per_step": 0, "ms_per_step": 1e3 * wall,
+                     "path": "per session: kvs_mark_migrating_out -> kvs_import_migration -> apply x L -> "
+                             "kvs_release_session, host wall clock per ring step (all sessions)"},
+                store_path={"devices": ndev, "nodes": world, "probe_pages_checked": checked,
+                            "host_us_per_layer": host, "per_step_max_device_ms": per_step},
+                roofline={"bound": "nvlink" if ndev > 1 else "hbm", "achieved": achieved,
+                          "peak": NVLINK_PEAK_GBS if ndev > 1 else None, "unit": "GB/s",
+                          "frac": achieved / NVLINK_PEAK_GBS if ndev > 1 else None, "traffic": None,
+                          "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS if ndev > 1 else None,
+                          "peak_provenance": NVLINK_PEAK_PROVENANCE,
+                          "kernel": "kvx_copy_pages (K3 push, store NetArrive)",
+                          "algorithmic_bytes_per_launch": session_bytes // L,
+                          "note": "per session per direction; the max over devices of the push sequence"},
+                gpu_launches=launches)
+
+
 def bench_multi(args, torch, np, kvx, dev, rank, world):
     """Migration-plus-serving at N GPUs (config 3): every rank decodes a batch
     of 70B @32K requests on its main stream while its own 70B @32K session
@@ -872,8 +1118,9 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
       gathers the session's pages and stores them straight into the
       receiver's page pool over NVLink (opened through CUDA IPC): one pass,
       no staging buffer, no receiver-side kernel, no collective.
-    --migrate-mode nccl: the comparison path — K1 pack into a per-layer buffer,
-      ncclSend/ncclRecv (batch_isend_irecv, ring), K2 unpack on the receiver.
+    --migrate-mode nccl: the comparison path through the C ABI —
+      kvx_migrate_nccl: per layer K1 pack, ncclSend/ncclRecv around the ring
+      (one group), K2 unpack on the receiver (gloo test mode: host-staged).
 
     value = N x session bytes / the max over ranks of the migration time
     measured WHILE decode runs. Also reported: the migration alone, the decode
@@ -957,21 +1204,18 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
                         rcv.copy_(hbufs[1])
                         kvx.unpack(pool, dst[sl[l]], blocks, rcv, kvx.COPY_AUTO, st.cuda_stream)
                     return
-                # NCCL: software-pipelined over two buffer pairs — layer l+1 is
-                # packed on the side stream while layer l's send/recv runs on
-                # NCCL's stream; the side stream waits for l's transfer only
-                # before unpacking it. A buffer pair is reused two layers later,
-                # after its unpack (recv) and the wait on its send were queued.
-                kvx.pack(pool, src[sl[0]], blocks, bufs[0][0], kvx.COPY_AUTO, st.cuda_stream)
-                for l in range(L):
-                    snd, rcv = bufs[l % 2]
-                    works = dist.batch_isend_irecv([dist.P2POp(dist.isend, snd, nxt),
-                                                    dist.P2POp(dist.irecv, rcv, prv)])
-                    if l + 1 < L:
-                        kvx.pack(pool, src[sl[l + 1]], blocks, bufs[(l + 1) % 2][0], kvx.COPY_AUTO, st.cuda_stream)
-                    for w in works:
-                        w.wait()  # the side stream waits on the transfer, the host does not
-                    kvx.unpack(pool, dst[sl[l]], blocks, rcv, kvx.COPY_AUTO, st.cuda_stream)
+                # NCCL through the C ABI (kvx_migrate_nccl): per layer, K1 pack
+                # -> one ncclSend/ncclRecv group around the ring -> K2 unpack,
+                # on this side stream, over a communicator libkvx built.
+                kvx.migrate_nccl(pool, src, n, nxt, pool, dst, n, prv, blocks, nccl_comm, nccl_staging,
+                                 st.cuda_stream)
+
+        nccl_comm, nccl_staging = None, None
+        if not staged:
+            uid = [kvx.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            nccl_comm = kvx.nccl_comm_init_rank(world, uid[0], rank, dev.index)
+            nccl_staging = torch.empty(kvx.migrate_nccl_staging_bytes(pb, blocks), dtype=torch.uint8, device=dev)
 
     # Serving: a decode batch on every rank (70B shape: 64 q heads over 8 kv heads).
     B, hq = args.serve_batch, 64
@@ -1023,6 +1267,7 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
     dist.barrier()
 
     rows = []
+    n_launch0 = kvx.launch_count()
     with ClockSampler(dev.index) as clocks:
         for _ in range(args.steps):
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -1037,6 +1282,7 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
             e[2].record(main)
             torch.cuda.synchronize()
             rows.append((e[0].elapsed_time(e[1]), e[0].elapsed_time(e[2])))
+        LAUNCHES["multi"] = kvx.launch_count() - n_launch0  # NCCL kernels are not counted (library)
         dist.barrier()  # every sender has finished writing into its receiver
     t_mig = cluster.max_over_ranks(dist, statistics.mean(r[0] for r in rows), red_dev)
     t_win = cluster.max_over_ranks(dist, statistics.mean(r[1] for r in rows), red_dev)
@@ -1072,13 +1318,18 @@ def bench_multi(args, torch, np, kvx, dev, rank, world):
     if peer is not None:
         peer.close()
     dist.barrier()
-    launches = args.steps * (L * (1 if args.migrate_mode == "p2p" else 2) + K * L)
+    launches_mine = LAUNCHES.get("multi", 0)
+    per_rank = [None] * world
+    dist.all_gather_object(per_rank, launches_mine)
+    launches = int(sum(per_rank))  # every rank's libkvx launches in the timed loop (kvx_launch_count)
     if serving is not None and gate is not None:
         serving["pipeline_gate"] = gate
     return dict(value=value, ms_per_step=t_mig, clocks=clocks.summary(), session_bytes=session_bytes,
                 cfg=cfg, verified=True, serving=serving, e2e=e2e,
                 roofline={"bound": "nvlink", "achieved": achieved, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                           "frac": achieved / NVLINK_PEAK_GBS, "traffic": None,
+                          "frac_of_nominal_900": achieved / NVLINK_NOMINAL_GBS,
+                          "peak_provenance": NVLINK_PEAK_PROVENANCE,
                           "kernel": "kvx_copy_pages(peer)" if args.migrate_mode == "p2p" else "nccl send/recv",
                           "algorithmic_bytes_per_launch": session_bytes // L,
                           "note": "per GPU, per direction, measured while decode runs; one launch per layer",
@@ -1346,13 +1597,17 @@ def reference_state_ops(np):
     return time.perf_counter() - t0
 
 
-def arm_config(cfg, world):
+def arm_config(cfg, world, path="store"):
     """The workload both arms report (identical for --impl b200 / reference)."""
     blocks, n = session_pages(cfg)
     pb = 2 * cfg["kv_heads"] * cfg["block_tokens"] * cfg["head_dim"] * 2
     if world == 1:
         workload = (f"{cfg['model']} @{cfg['ctx']} session ({cfg['layers']} layers x {blocks} pages): pack every "
                     "page into the migration buffer + unpack into a second page permutation")
+    elif path == "store":
+        workload = (f"{cfg['model']} @{cfg['ctx']} session per node, every session migrated one hop around the "
+                    "ring per step through the store API (mark_migrating_out -> import_migration -> apply every "
+                    "NetArrive -> release)")
     else:
         workload = (f"{cfg['model']} @{cfg['ctx']} session per rank, ring migration rank r -> r+1 "
                     "(page-to-page into the receiver's pool) while every rank decodes a batch of 4 "
@@ -1411,7 +1666,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "reference",
-            "config": arm_config(cfg, world),
+            "config": arm_config(cfg, world, args.path),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -1439,6 +1694,10 @@ def main():
                     help="N>1: K3 stores into the peer pool (p2p) or pack + send/recv + unpack (nccl)")
     ap.add_argument("--mig-ctas", type=int, default=0, help="N>1: cap on the migration mover's CTAs (0 = all)")
     ap.add_argument("--serve-batch", type=int, default=4, help="N>1: decode batch run beside the migration")
+    ap.add_argument("--path", default="store", choices=["store", "kvx"],
+                    help="N>1: store = migrations through the store API (KvStore + NodePayload, one process "
+                         "driving every device: the product path); kvx = raw K3 ring over CUDA IPC with decode "
+                         "beside it (one process per GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -1464,8 +1723,11 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
-        res = bench_multi(args, torch, np, kvx, dev, rank, world)
-        cfg = res["cfg"]
+        if args.path == "store":
+            res = bench_store_ring(args, torch, np, kvx, rank, world)
+        else:
+            res = bench_multi(args, torch, np, kvx, dev, rank, world)
+        cfg = res["cfg"] if res is not None else None
     else:
         res = bench_single(args, torch, np, kvx, dev, hbm_peak, peak_kind)
         cfg = CFG_8B
@@ -1474,13 +1736,16 @@ def main():
         line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": arm_config(cfg, world),
+                "config": arm_config(cfg, world, args.path),
                 "roofline": res["roofline"], "clocks": res["clocks"], "gpu_launches": res["gpu_launches"]}
         if world > 1:
             line["serving"] = res["serving"]
             if res["e2e"] is not None:
                 line["e2e"] = res["e2e"]
-            line["config"]["migrate_mode"] = args.migrate_mode
+            line["config"]["migrate_mode"] = args.migrate_mode if args.path == "kvx" else "store-api"
+            line["config"]["path"] = args.path
+            if "store_path" in res:
+                line["store_path"] = res["store_path"]
             if getattr(args, "p2p_unavailable", None):
                 line["config"]["p2p_unavailable"] = args.p2p_unavailable
         if world == 1:

@@ -107,6 +107,11 @@ enum {
 
 const char* kvx_last_error(void);
 int kvx_version(void);
+/* Launches of this library's own kernels since load (all threads), and
+ * calls into the cuBLAS library (kvx_model's projections) — counters a
+ * host samples around a timed region. */
+uint64_t kvx_launch_count(void);
+uint64_t kvx_library_launch_count(void);
 /* Bytes of one page for `layout` (2 * H * T * D * sizeof(dtype)). */
 uint64_t kvx_page_bytes(const kvx_page_layout* layout);
 
@@ -206,6 +211,24 @@ int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, 
  * Ignored for KVX_COPY_CE. */
 int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
                           uint64_t n, int mode, uint32_t max_ctas, void* stream);
+
+/* K3 over NCCL (the collective-library migration variant):
+ * per chunk of pages_per_chunk pages — one migration layer — K1 packs the
+ * chunk of `send` pages into a staging slot, one NCCL group sends it to
+ * send_peer and receives recv_peer's chunk into the other slot, and K2
+ * unpacks it into `recv` pages. Either side may be empty (n = 0), so a ring
+ * rank both sends and receives in one call without deadlock. `comm` is an
+ * ncclComm_t (kvx_nccl_comm_init_rank or the caller's own); d_staging holds
+ * kvx_migrate_nccl_staging_bytes() bytes. NCCL is loaded at run time
+ * (libnccl.so.2); without it the calls return KVX_ERR_UNSUPPORTED. All
+ * asynchronous on `stream`. */
+uint64_t kvx_migrate_nccl_staging_bytes(uint64_t page_bytes, uint64_t pages_per_chunk);
+int kvx_migrate_nccl(const kvx_pool* send_pool, const uint32_t* d_send_ids, uint64_t n_send, int send_peer,
+                     kvx_pool* recv_pool, const uint32_t* d_recv_ids, uint64_t n_recv, int recv_peer,
+                     uint64_t pages_per_chunk, void* comm, void* d_staging, uint64_t staging_bytes, void* stream);
+int kvx_nccl_get_unique_id(void* id128);
+int kvx_nccl_comm_init_rank(void** comm, int nranks, const void* id128, int rank, int device);
+int kvx_nccl_comm_destroy(void* comm);
 
 /* ---- contents (K5) ------------------------------------------------------ */
 int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,

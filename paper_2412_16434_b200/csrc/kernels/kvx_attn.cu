@@ -140,7 +140,28 @@ __device__ __forceinline__ uint32_t swz(int row, int col16) {
   return static_cast<uint32_t>(row * 256 + ((col16 ^ (row & 7)) << 4));
 }
 
+// The TMA ring's layout: a 4 KiB tile (16 token rows x 256 B) arrives as two
+// 2 KiB boxes (columns 0-63, 64-127) written by the TMA unit with
+// SWIZZLE_128B: within a box, row r's 16-B chunk c sits at chunk c ^ (r & 7).
+// Same conflict-free property for ldmatrix as swz().
+__device__ __forceinline__ uint32_t swz_tma(int row, int col16) {
+  return static_cast<uint32_t>(((col16 >> 3) << 11) + row * 128 + (((col16 & 7) ^ (row & 7)) << 4));
+}
+
+// 2-D TMA tile load (global -> shared), completion counted on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(uint32_t smem_dst, const CUtensorMap* map, int col, int row,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(smem_dst), "l"(map), "r"(col), "r"(row), "r"(bar)
+      : "memory");
+}
+
 struct AttnArgs {
+  // The pool as a 2-D tensor for TMA (TMA variant): rows of 256 B (one token
+  // of one kv head's K or V), row of (page p, K/V kv, head h, token t) =
+  // (p * 2H + kv * H + h) * 16 + t; boxes of 64 columns x 16 rows, swizzled.
+  CUtensorMap tmap;
   const uint8_t* pool;
   uint64_t page_bytes;
   uint64_t pool_pages;  // block-table entries are checked against it
@@ -164,9 +185,14 @@ struct AttnArgs {
 };
 
 // W warps per CTA, each streaming its own pages through a kStages ring.
-template <int kStages, int W>
-__global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(AttnArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
+// kTma: each warp's ring is fed by the TMA unit (lane 0 issues four 2-D box
+// loads per page onto the stage's mbarrier) instead of 16 cp.async per lane.
+template <int kStages, int W, bool kTma>
+__global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(const __grid_constant__ AttnArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // SWIZZLE_128B boxes need 1024-B aligned destinations (the launch adds the slack).
+  uint8_t* smem = kTma ? smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023) : smem_raw;
+  __shared__ __align__(8) uint64_t s_full[kTma ? W * kStages : 1];  // per (warp, stage): TMA bytes landed
   __shared__ uint32_t s_pages[kMaxPagesPerCta];
   __shared__ int s_last;
   // Cluster merge (push): CTA s of a (request, kv head) cluster owns output
@@ -178,6 +204,14 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   __shared__ __align__(8) uint64_t s_merge_bar;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  if (kTma) {  // this warp's stage barriers (one arrival: lane 0's expect_tx; then the TMA bytes)
+    if (lane == 0) {
+#pragma unroll
+      for (int s2 = 0; s2 < kStages; ++s2) mbar_init(&s_full[warp * kStages + s2], 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+  }
   // Output slice per cluster CTA, in float4 units so no vector push straddles
   // two owners.
   const int chunk = ((a.group * kD + a.splits - 1) / a.splits + 3) & ~3;
@@ -253,6 +287,24 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
   const int my_count = my_first < p_end ? (p_end - my_first + W - 1) / W : 0;
 
   auto issue = [&](int i) {  // page i of this warp -> stage i % kStages
+    if (kTma) {
+      if (i < my_count && lane == 0) {
+        const int p = my_first + i * W;
+        const int row_k = static_cast<int>(s_pages[p - p_begin]) * (2 * a.heads * kT) + h * kT;
+        const int row_v = row_k + a.heads * kT;
+        const uint32_t st = ring_s + (i % kStages) * kStageBytes;
+        const uint32_t bar = smem_u32(&s_full[warp * kStages + (i % kStages)]);
+        // The stage was last read by this warp's ldmatrix (generic proxy):
+        // order those reads before the async-proxy writes.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&s_full[warp * kStages + (i % kStages)], kStageBytes);
+        tma_load_2d(st, &a.tmap, 0, row_k, bar);
+        tma_load_2d(st + 2048, &a.tmap, 64, row_k, bar);
+        tma_load_2d(st + kTileBytes, &a.tmap, 0, row_v, bar);
+        tma_load_2d(st + kTileBytes + 2048, &a.tmap, 64, row_v, bar);
+      }
+      return;
+    }
     if (i < my_count) {
       const int p = my_first + i * W;
       const uint8_t* page = a.pool + static_cast<uint64_t>(s_pages[p - p_begin]) * a.page_bytes;
@@ -296,6 +348,8 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
       const uint16_t* src = (kv ? a.new_v : a.new_k) + (static_cast<uint64_t>(b) * a.heads + h) * kD;
       uint8_t* dst = page + static_cast<uint64_t>((kv * a.heads + h) * kT + slot) * (kD * 2);
       reinterpret_cast<uint4*>(dst)[c] = reinterpret_cast<const uint4*>(src)[c];
+      // The page is read next by the TMA unit (async proxy).
+      if (kTma) asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
   }
@@ -312,7 +366,11 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
 
   for (int i = 0; i < my_count; ++i) {
     issue(i + kStages - 1);
-    cp_async_wait<kStages - 1>();
+    if (kTma) {
+      mbar_wait(&s_full[warp * kStages + (i % kStages)], static_cast<uint32_t>((i / kStages) & 1));
+    } else {
+      cp_async_wait<kStages - 1>();
+    }
     __syncwarp();
     if (i == 0) KVX_TRACE(3);
     const uint32_t ks = ring_s + (i % kStages) * kStageBytes;
@@ -331,7 +389,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
 #pragma unroll
       for (int kk = 0; kk < kD / 16; kk += 2) {
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(ks + swz(row, 2 * kk + (lane >> 3)), b0, b1, b2, b3);
+        ldsm_x4(ks + (kTma ? swz_tma(row, 2 * kk + (lane >> 3)) : swz(row, 2 * kk + (lane >> 3))), b0, b1, b2, b3);
         mma_bf16(s[j], qa[kk], b0, b1);
         mma_bf16(s_odd[j], qa[kk + 1], b2, b3);
       }
@@ -390,13 +448,13 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(Att
 #pragma unroll
     for (int n = 0; n < kD / 8; n += 2) {
       uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(vs + swz(vrow, n + (lane >> 4)), b0, b1, b2, b3);
+      ldsm_x4_t(vs + (kTma ? swz_tma(vrow, n + (lane >> 4)) : swz(vrow, n + (lane >> 4))), b0, b1, b2, b3);
       mma_bf16(o[n], pa, b0, b1);
       mma_bf16(o[n + 1], pa, b2, b3);
     }
     __syncwarp();
   }
-  cp_async_wait<0>();
+  if (!kTma) cp_async_wait<0>();
   KVX_TRACE(4);
   KVX_TRACE_IF(lane == 0, 16 + warp);  // per-warp loop end (slots 16..16+W-1)
   // All our global reads of the pool are done: let the next kernel's CTAs
@@ -706,34 +764,85 @@ uint64_t workspace_for(uint64_t batch, uint64_t hq, uint64_t heads, int splits) 
 // One-time per-device kernel attributes (dynamic smem, cluster sizes > 8).
 // Idempotent, so concurrent first calls from several host threads are fine;
 // the flags are atomics so the check itself is race-free.
+template <bool kTma>
+int configure_variant() {
+  constexpr int slack = kTma ? 1024 : 0;  // 1024-B alignment of the TMA ring
+  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kStagesWide, 4, kTma>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_bytes(kStagesWide, 4) + slack),
+               "kvx_decode_attention: smem attribute");
+  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW, kTma>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem_bytes(kNarrowStages, kNarrowW) + slack),
+               "kvx_decode_attention: smem attribute");
+  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW, kTma>,
+                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+               "kvx_decode_attention: cluster attribute");
+  return KVX_OK;
+}
+
 int configure(int device) {
   static std::atomic<bool> configured[64] = {};
   const int slot = device < 0 ? 0 : device % 64;
   if (configured[slot].load(std::memory_order_acquire)) return KVX_OK;
-  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kStagesWide, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem_bytes(kStagesWide, 4)),
-               "kvx_decode_attention: smem attribute");
-  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem_bytes(kNarrowStages, kNarrowW)),
-               "kvx_decode_attention: smem attribute");
-  KVX_CUDA_TRY(cudaFuncSetAttribute(attn_bf16_d128<kNarrowStages, kNarrowW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
-               "kvx_decode_attention: cluster attribute");
+  if (int rc = configure_variant<false>()) return rc;
+  if (int rc = configure_variant<true>()) return rc;
   configured[slot].store(true, std::memory_order_release);
   return KVX_OK;
 }
 
+// The pool as a 2-D tensor for K4's TMA feed: 256-B rows (one token of one
+// kv head's K or V), boxes of 64 columns x 16 rows with SWIZZLE_128B. Built
+// once per pool through the driver's cuTensorMapEncodeTiled (resolved via
+// the runtime, so libkvx needs no libcuda link). nullptr when the pool
+// cannot be described (too many rows, misaligned base).
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+const CUtensorMap* attn_tensor_map(kvx_pool* pool, int heads) {
+  std::lock_guard<std::mutex> lock(pool->tmap_mu);
+  if (pool->tmap_heads == heads) return &pool->tmap;
+  if (pool->tmap_heads == -2) return nullptr;
+  static EncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      pool->tmap_heads = -2;
+      return nullptr;
+    }
+    encode = reinterpret_cast<EncodeTiled>(fn);
+  }
+  const uint64_t rows = pool->num_pages * pool->page_bytes / 256;
+  if (pool->page_bytes % 256 || rows >= (1ull << 31) || reinterpret_cast<uintptr_t>(pool->base) % 16) {
+    pool->tmap_heads = -2;
+    return nullptr;
+  }
+  const cuuint64_t dims[2] = {kD, rows};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {64, kT};
+  const cuuint32_t elem[2] = {1, 1};
+  const CUresult r = encode(&pool->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool->base, dims, strides, box, elem,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  pool->tmap_heads = r == CUDA_SUCCESS ? heads : -2;
+  return r == CUDA_SUCCESS ? &pool->tmap : nullptr;
+}
+
 // How many clusters of `splits` one-SM CTAs (8 warps, 192 KiB smem) the
 // device runs at once (cudaOccupancyMaxActiveClusters; GPC-shape dependent).
-int cluster_capacity(int device, int splits) {
-  static std::atomic<int> cache[64][kMaxClusterSplits + 1] = {};
+int cluster_capacity(int device, int splits, bool tma) {
+  static std::atomic<int> cache[64][2][kMaxClusterSplits + 1] = {};
   const int slot = device < 0 ? 0 : device % 64;
-  std::atomic<int>& cached = cache[slot][splits];
+  std::atomic<int>& cached = cache[slot][tma ? 1 : 0][splits];
   int c = cached.load(std::memory_order_relaxed);
   if (c == 0) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(splits, 1, 1);
     cfg.blockDim = dim3(kNarrowW * 32);
-    cfg.dynamicSmemBytes = smem_bytes(kNarrowStages, kNarrowW);
+    cfg.dynamicSmemBytes = smem_bytes(kNarrowStages, kNarrowW) + (tma ? 1024 : 0);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = splits;
@@ -742,7 +851,9 @@ int cluster_capacity(int device, int splits) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    c = cudaOccupancyMaxActiveClusters(&n, attn_bf16_d128<kNarrowStages, kNarrowW>, &cfg) == cudaSuccess ? std::max(n, 0) : 0;
+    const cudaError_t e = tma ? cudaOccupancyMaxActiveClusters(&n, attn_bf16_d128<kNarrowStages, kNarrowW, true>, &cfg)
+                              : cudaOccupancyMaxActiveClusters(&n, attn_bf16_d128<kNarrowStages, kNarrowW, false>, &cfg);
+    c = e == cudaSuccess ? std::max(n, 0) : 0;
     if (c == 0) {
       cudaGetLastError();
       c = -1;  // cached "does not fit"
@@ -766,7 +877,7 @@ struct Plan {
 // clusters do not co-reside 8 at a time on B200's GPCs and run in two
 // waves, which the occupancy check catches). Explicit split counts and
 // merge modes are honoured (tests, sweeps).
-Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge, int device) {
+Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge, int device, bool tma) {
   const int sms = sm_count(device);
   const long groups = std::max(1L, static_cast<long>(batch) * heads);
   const int pages = std::max(1, (max_ctx + kT - 1) / kT);
@@ -779,7 +890,7 @@ Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge,
     const int lowest = requested > 0 ? target : std::max(2, (3 * target + 3) / 4);
     for (int s = std::min(target, kMaxClusterSplits); s >= lowest; --s) {
       const bool ok = s >= 2 && s >= min_splits && groups * s <= sms &&
-                      cluster_capacity(device, s) >= (requested > 0 ? 1 : groups);
+                      cluster_capacity(device, s, tma) >= (requested > 0 ? 1 : groups);
       if (ok) {
         p = Plan{s, true, true};
         break;
@@ -832,11 +943,20 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     if (int rc = kvx::configure(dev)) return rc;
     if (params->split_merge < KVX_MERGE_AUTO || params->split_merge > KVX_MERGE_CLUSTER)
       return kvx::fail_arg("kvx_decode_attention: unknown split_merge");
-    const kvx::Plan plan = kvx::plan_attention(batch, H, max_ctx, params->num_splits, params->split_merge, dev);
+    // TMA feed (default) unless disabled by KVX_ATTN_TMA=0 (measurement knob)
+    // or the pool cannot be described as a tensor.
+    static const char* tma_env = std::getenv("KVX_ATTN_TMA");
+    const CUtensorMap* tmap = (tma_env && tma_env[0] == '0')
+                                  ? nullptr
+                                  : kvx::attn_tensor_map(const_cast<kvx_pool*>(pool), H);
+    const bool tma = tmap != nullptr;
+    const kvx::Plan plan =
+        kvx::plan_attention(batch, H, max_ctx, params->num_splits, params->split_merge, dev, tma);
     if (params->split_merge == KVX_MERGE_CLUSTER && !plan.cluster && plan.splits > 1)
       return kvx::fail_arg("kvx_decode_attention: split_merge=CLUSTER but the splits do not fit one cluster");
     const int splits = plan.splits;
     kvx::AttnArgs a{};
+    if (tma) a.tmap = *tmap;
     a.pool = pool->base;
     a.page_bytes = pool->page_bytes;
     a.pool_pages = pool->num_pages;
@@ -880,7 +1000,8 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(narrow ? kvx::kNarrowW * 32 : 4 * 32);
-    cfg.dynamicSmemBytes = narrow ? kvx::smem_bytes(kvx::kNarrowStages, kvx::kNarrowW) : kvx::smem_bytes(kvx::kStagesWide, 4);
+    cfg.dynamicSmemBytes = (narrow ? kvx::smem_bytes(kvx::kNarrowStages, kvx::kNarrowW) : kvx::smem_bytes(kvx::kStagesWide, 4)) +
+                           (tma ? 1024 : 0);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
@@ -901,11 +1022,18 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     if (plan.cluster && !cluster_pdl) attr[0].val.programmaticStreamSerializationAllowed = 0;
     cfg.attrs = attr;
     cfg.numAttrs = plan.cluster ? 2 : 1;
-    if (narrow)
-      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kNarrowStages, kvx::kNarrowW>, a), "kvx_decode_attention");
+    if (narrow && tma)
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kNarrowStages, kvx::kNarrowW, true>, a),
+                   "kvx_decode_attention");
+    else if (narrow)
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kNarrowStages, kvx::kNarrowW, false>, a),
+                   "kvx_decode_attention");
+    else if (tma)
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 4, true>, a), "kvx_decode_attention");
     else
-      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 4>, a), "kvx_decode_attention");
+      KVX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kvx::attn_bf16_d128<kvx::kStagesWide, 4, false>, a), "kvx_decode_attention");
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention");
+    kvx::note_launch();
     return KVX_OK;
   }
 
@@ -920,6 +1048,7 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
                                                   static_cast<const uint8_t*>(d_new_v), H, layout->block_tokens,
                                                   row_bytes, params->max_blocks);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention_append(append)");
+    kvx::note_launch();
   }
   dim3 grid(Hq, batch);
   if (layout->dtype == KVX_DTYPE_F32)
@@ -932,6 +1061,7 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
                                                      layout->head_dim, layout->block_tokens, params->max_blocks,
                                                      scale);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_decode_attention(generic)");
+  kvx::note_launch();
   return KVX_OK;
 }
 

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 
 #include <string>
 #include <vector>
@@ -23,6 +24,11 @@ struct kvx_pool {
   int fd = -1;           // file pool (DISK tier): pages at offset page * page_bytes
   bool direct = false;   // fd opened with O_DIRECT
   std::atomic<int> io_errno{0};  // first failed read/write (sticky)
+  // K4's TMA view of a DEVICE pool (kvx_attn.cu): built on first use for a
+  // kv-head count, then reused by every launch over this pool.
+  std::mutex tmap_mu;
+  int tmap_heads = -1;  // -1: not built; -2: cannot be built for this pool
+  alignas(64) CUtensorMap tmap;
 };
 
 namespace kvx {
@@ -31,6 +37,10 @@ void set_error(const std::string& msg);
 int fail_cuda(cudaError_t e, const char* what);
 int fail_arg(const char* what);
 int sm_count(int device);
+// Counts launches of this library's own kernels (kvx_launch_count): the
+// bench reports how many ran inside its timed region from this counter.
+void note_launch(uint64_t n = 1);
+void note_library_launch(uint64_t n = 1);  // cuBLAS calls (kvx_model projections)
 // File pools (DISK tier): sticky I/O error check, and stream-ordered page I/O
 // between a file pool and host memory (kvx_pool.cu).
 int check_io(const kvx_pool* pool, const char* who);

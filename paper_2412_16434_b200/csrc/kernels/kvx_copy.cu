@@ -183,6 +183,7 @@ void launch_pdl(Kernel kernel, unsigned grid, unsigned block, uint32_t smem, cud
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, a);
+  note_launch();
 }
 
 // AUTO picks the TMA bulk mover when both sides are in this GPU's HBM (measured
@@ -445,6 +446,7 @@ int kvx_verify_pages(const kvx_pool* pool, const uint32_t* d_page_ids, const kvx
   kvx::verify_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(pool->base, pool->page_bytes, pool->num_pages,
                                                                        d_page_ids, d_tags, n, nullptr, nullptr, 0, 1,
                                                                        1, seed, fill_mode, dtype, d_mismatches);
+  kvx::note_launch();
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_verify_pages");
   return KVX_OK;
 }
@@ -464,6 +466,7 @@ int kvx_verify_block_tables(const kvx_pool* pool, const kvx_page_layout* layout,
   kvx::verify_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(
       pool->base, pool->page_bytes, pool->num_pages, d_tables, nullptr, n, d_sessions, d_ctx_lens, batch, max_blocks,
       layout->block_tokens, seed, fill_mode, layout->dtype, d_mismatches);
+  kvx::note_launch();
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_verify_block_tables");
   return KVX_OK;
 }
@@ -481,6 +484,7 @@ int kvx_fill_pages(kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_t
   kvx::DeviceGuard guard(pool->device);
   kvx::fill_pages_kernel<<<grid, 256, 0, kvx::as_stream(stream)>>>(pool->base, pool->page_bytes, d_page_ids, d_tags,
                                                                      n, seed, fill_mode, dtype);
+  kvx::note_launch();
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_fill_pages");
   return KVX_OK;
 }
@@ -509,6 +513,7 @@ int kvx_append_kv(kvx_pool* pool, const kvx_page_layout* layout, const uint32_t*
     cudaLaunchKernelEx(&cfg, kvx::append_kv_kernel, pool->base, pool->page_bytes, d_page_ids, d_slots,
                        static_cast<const uint8_t*>(d_k), static_cast<const uint8_t*>(d_v), layout->num_kv_heads,
                        layout->block_tokens, row_bytes);
+    kvx::note_launch();
   }
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_append_kv");
   return KVX_OK;

@@ -221,6 +221,7 @@ int linear(kvx_model* m, const uint16_t* X, const uint16_t* W, uint16_t* Y, int 
   KVX_BLAS_TRY(cublasGemmEx(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, out, rows, in, &one, W, CUDA_R_16BF, in, X, CUDA_R_16BF,
                             in, &beta, Y, CUDA_R_16BF, out, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
                "kvx_model: cublasGemmEx");
+  note_library_launch();
   return KVX_OK;
 }
 
@@ -271,6 +272,7 @@ int layer_pre(kvx_model* m, int l, int rows) {
   cudaStream_t st = as_stream(m->stream);
   rms_norm<<<rows, 256, 0, st>>>(m->x, m->norm1[l], m->h, c.hidden, c.rms_eps);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rms_norm");
+  note_launch();
   return linear(m, m->h, m->wqkv[l], m->qkv, rows, c.hidden, (c.num_q_heads + 2 * c.num_kv_heads) * c.head_dim, false);
 }
 
@@ -280,10 +282,12 @@ int layer_post(kvx_model* m, int l, int rows) {
   if (int rc = linear(m, m->attn, m->wo[l], m->x, rows, c.num_q_heads * c.head_dim, c.hidden, true)) return rc;
   rms_norm<<<rows, 256, 0, st>>>(m->x, m->norm2[l], m->h, c.hidden, c.rms_eps);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rms_norm");
+  note_launch();
   if (int rc = linear(m, m->h, m->wgu[l], m->gu, rows, c.hidden, 2 * c.intermediate, false)) return rc;
   const uint64_t n = static_cast<uint64_t>(rows) * c.intermediate;
   silu_mul<<<grid_for(n, 256), 256, 0, st>>>(m->gu, m->act, c.intermediate, rows);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: silu_mul");
+  note_launch();
   return linear(m, m->act, m->wd[l], m->x, rows, c.intermediate, c.hidden, true);
 }
 
@@ -295,9 +299,11 @@ int sample(kvx_model* m, int first, int rows, int32_t* d_tokens_out) {
   rms_norm<<<rows, 256, 0, st>>>(m->x + static_cast<uint64_t>(first) * c.hidden, m->final_norm, m->h, c.hidden,
                                  c.rms_eps);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: final norm");
+  note_launch();
   if (int rc = linear(m, m->h, m->lm_head, m->logits, rows, c.hidden, c.vocab, false)) return rc;
   argmax_rows<<<rows, 512, 0, st>>>(m->logits, c.vocab, d_tokens_out);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: argmax");
+  note_launch();
   return KVX_OK;
 }
 
@@ -420,6 +426,7 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
   }
   kvx::embed_rows<<<batch, 128, 0, st>>>(m->embed, d_tokens_in, m->x, c.hidden, c.vocab);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: embed");
+  kvx::note_launch();
   const int Hq = c.num_q_heads, H = c.num_kv_heads, D = c.head_dim;
   for (int l = 0; l < c.num_layers; ++l) {
     if (int rc = kvx::layer_pre(m, l, batch)) return rc;
@@ -437,6 +444,7 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
     kvx::rope_and_token<<<batch, 256, 0, st>>>(m->qkv, d_sessions, d_ctx_lens, l, Hq, H, D, layout->block_tokens,
                                                c.rope_theta, fill_seed, fill_mode, m->q, new_k, new_v);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rope");
+    kvx::note_launch();
     const uint32_t* tab = d_tables + static_cast<uint64_t>(l) * batch * max_blocks;
     if (int rc = kvx_decode_attention_append(pool, layout, &ap, tab, d_ctx_lens, m->q, new_k, new_v, m->attn_f32,
                                              batch, max_ctx, m->attn_ws, m->attn_ws_bytes, stream))
@@ -444,6 +452,7 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
     const uint64_t n = static_cast<uint64_t>(batch) * Hq * D;
     kvx::f32_to_bf16_rows<<<kvx::grid_for(n, 256), 256, 0, st>>>(m->attn_f32, m->attn, n);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: attn to bf16");
+    kvx::note_launch();
     if (int rc = kvx::layer_post(m, l, batch)) return rc;
   }
   return kvx::sample(m, 0, batch, d_tokens_out);
@@ -464,6 +473,8 @@ int kvx_model_prefill(kvx_model* m, int32_t tokens, void* stream) {
     KVX_CUDA_TRY(cudaMemsetAsync(m->tokens, 0, static_cast<size_t>(rows) * 4, st), "kvx_model: prefill tokens");
     kvx::embed_rows<<<rows, 128, 0, st>>>(m->embed, m->tokens, m->x, c.hidden, c.vocab);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: embed");
+    kvx::note_launch();
+  kvx::note_launch();
     for (int l = 0; l < c.num_layers; ++l) {
       if (int rc = kvx::layer_pre(m, l, rows)) return rc;
       // Prefill attention is not modelled here (its K/V land in the pages as

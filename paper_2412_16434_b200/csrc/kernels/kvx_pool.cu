@@ -30,6 +30,12 @@ thread_local std::string g_error;
 
 void set_error(const std::string& msg) { g_error = msg; }
 
+namespace {
+std::atomic<uint64_t> g_launches{0}, g_library_launches{0};
+}
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void note_library_launch(uint64_t n) { g_library_launches.fetch_add(n, std::memory_order_relaxed); }
+
 int fail_cuda(cudaError_t e, const char* what) {
   g_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
   return KVX_ERR_CUDA;
@@ -136,6 +142,9 @@ extern "C" {
 const char* kvx_last_error(void) { return kvx::g_error.c_str(); }
 
 int kvx_version(void) { return 1; }
+
+uint64_t kvx_launch_count(void) { return kvx::g_launches.load(std::memory_order_relaxed); }
+uint64_t kvx_library_launch_count(void) { return kvx::g_library_launches.load(std::memory_order_relaxed); }
 
 uint64_t kvx_page_bytes(const kvx_page_layout* l) {
   if (!l) return 0;

@@ -56,6 +56,14 @@ def lib() -> C.CDLL:
     sigs = {
         "kvx_last_error": ([], C.c_char_p),
         "kvx_version": ([], C.c_int),
+        "kvx_launch_count": ([], C.c_uint64),
+        "kvx_migrate_nccl_staging_bytes": ([C.c_uint64, C.c_uint64], C.c_uint64),
+        "kvx_migrate_nccl": ([C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                              C.c_int, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p], C.c_int),
+        "kvx_nccl_get_unique_id": ([C.c_void_p], C.c_int),
+        "kvx_nccl_comm_init_rank": ([C.POINTER(C.c_void_p), C.c_int, C.c_void_p, C.c_int, C.c_int], C.c_int),
+        "kvx_nccl_comm_destroy": ([C.c_void_p], C.c_int),
+        "kvx_library_launch_count": ([], C.c_uint64),
         "kvx_page_bytes": ([P(PageLayout)], U64),
         "kvx_pool_create": ([C.c_int, U64, U64, P(V)], C.c_int),
         "kvx_pool_create_host": ([U64, U64, P(V)], C.c_int),
@@ -91,6 +99,11 @@ def lib() -> C.CDLL:
         fn.restype = res
     _LIB = h
     return h
+
+
+def launch_count() -> int:
+    """Launches of libkvx's own kernels so far (kvx_launch_count)."""
+    return lib().kvx_launch_count()
 
 
 def check(rc: int) -> None:
@@ -308,3 +321,35 @@ class Attention:
         check(lib().kvx_decode_attention(pool.handle, C.byref(self.layout), C.byref(p), _ptr(block_tables),
                                          _ptr(ctx_lens), _ptr(q), _ptr(out), batch, max_ctx, ws, ws_bytes,
                                          _stream(stream)))
+
+
+# ---- K3 over NCCL (kvx_migrate_nccl) -----------------------------------------
+
+def migrate_nccl_staging_bytes(page_bytes: int, pages_per_chunk: int) -> int:
+    return lib().kvx_migrate_nccl_staging_bytes(page_bytes, pages_per_chunk)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().kvx_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+def nccl_comm_init_rank(nranks: int, uid: bytes, rank: int, device: int) -> int:
+    comm = C.c_void_p()
+    buf = C.create_string_buffer(bytes(uid), 128)
+    check(lib().kvx_nccl_comm_init_rank(C.byref(comm), nranks, buf, rank, device))
+    return comm.value
+
+
+def nccl_comm_destroy(comm: int) -> None:
+    check(lib().kvx_nccl_comm_destroy(comm))
+
+
+def migrate_nccl(send_pool, send_ids, n_send: int, send_peer: int, recv_pool, recv_ids, n_recv: int,
+                 recv_peer: int, pages_per_chunk: int, comm: int, staging, stream=None) -> None:
+    """K1 pack -> ncclSend/ncclRecv -> K2 unpack per chunk (kvx_migrate_nccl)."""
+    check(lib().kvx_migrate_nccl(send_pool.handle if send_pool is not None else None, _ptr(send_ids), n_send,
+                                 send_peer, recv_pool.handle if recv_pool is not None else None, _ptr(recv_ids),
+                                 n_recv, recv_peer, pages_per_chunk, comm, _ptr(staging), staging.numel(),
+                                 _stream(stream)))

@@ -117,9 +117,11 @@ struct Calibration {
   std::vector<std::pair<int, double>> decode_curve;  // (batch, ms)
   double network_gbs = 12.5;
   double pcie_gbs = 25.0;
+  double disk_gbs = 3.0;          // reference LinkProfile default (costmodel.hpp:31)
   double prefill_tps = 8192.0;
   double think_s = 0.0;           // 0: config default
   std::vector<int> users;         // sweep loads; empty: default list
+  std::vector<std::string> policies;  // sweep policies; empty: all four
   std::int64_t kv_bytes_per_token = 131'072;  // Llama-3.1-8B, bf16
   std::int64_t hbm_capacity = 160'000'000'000;
 };
@@ -135,6 +137,7 @@ RunConfig make_cfg(const Calibration& c, Policy p) {
   cfg.gpu.decode_curve_ms = c.decode_curve;
   cfg.links.network_bandwidth = c.network_gbs * 1e9;
   cfg.links.pcie_bandwidth = c.pcie_gbs * 1e9;
+  cfg.links.disk_bandwidth = c.disk_gbs * 1e9;
   cfg.sample_period = ns_from_sec(5);
   cfg.invariant_stride = 1024;
   return cfg;
@@ -185,6 +188,8 @@ Calibration parse_calibration(int argc, char** argv, int from) {
       c.network_gbs = std::atof(argv[++i]);
     } else if (!std::strcmp(argv[i], "--pcie-gbs") && i + 1 < argc) {
       c.pcie_gbs = std::atof(argv[++i]);
+    } else if (!std::strcmp(argv[i], "--disk-gbs") && i + 1 < argc) {
+      c.disk_gbs = std::atof(argv[++i]);
     } else if (!std::strcmp(argv[i], "--prefill-tps") && i + 1 < argc) {
       c.prefill_tps = std::atof(argv[++i]);
     } else if (!std::strcmp(argv[i], "--typing-wpm") && i + 1 < argc) {
@@ -193,6 +198,14 @@ Calibration parse_calibration(int argc, char** argv, int from) {
       g_sessions = std::atoi(argv[++i]);
     } else if (!std::strcmp(argv[i], "--think-s") && i + 1 < argc) {
       c.think_s = std::atof(argv[++i]);
+    } else if (!std::strcmp(argv[i], "--policies") && i + 1 < argc) {
+      std::string u = argv[++i];
+      for (std::size_t pos = 0; pos < u.size();) {
+        const std::size_t comma = u.find(',', pos);
+        c.policies.push_back(u.substr(pos, comma - pos));
+        if (comma == std::string::npos) break;
+        pos = comma + 1;
+      }
     } else if (!std::strcmp(argv[i], "--users") && i + 1 < argc) {
       std::string u = argv[++i];
       for (std::size_t pos = 0; pos < u.size();) {
@@ -260,7 +273,11 @@ int main(int argc, char** argv) {
     const Calibration cal = parse_calibration(argc, argv, 3);
     think_override = cal.think_s;
     const std::vector<int> loads = cal.users.empty() ? std::vector<int>{32, 64, 128, 256, 384, 512} : cal.users;
-    const Policy policies[] = {Policy::Symphony, Policy::Retain, Policy::Swap, Policy::Recompute};
+    std::vector<Policy> policies = {Policy::Symphony, Policy::Retain, Policy::Swap, Policy::Recompute};
+    if (!cal.policies.empty()) {
+      policies.clear();
+      for (const auto& p : cal.policies) policies.push_back(policy_from(p));
+    }
     std::printf("{\"config\": %d, \"cells\": [", config);
     bool first = true;
     for (Policy p : policies)

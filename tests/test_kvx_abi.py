@@ -108,3 +108,23 @@ def test_abi_rejects_bad_arguments_without_touching_a_device(product_libs):
     out = V()
     assert lib.kvx_pool_create_host(4, 1000, ctypes.byref(out)) == KVX_ERR_ARG  # not a multiple of 16
     assert lib.kvx_signal_write(V(2), 1, None) == KVX_ERR_ARG  # misaligned flag
+
+
+def test_migrate_nccl_validates_arguments_before_touching_a_device(product_libs):
+    """kvx_migrate_nccl (K3 over NCCL, include/kvx.h): argument errors are
+    reported as KVX_ERR_ARG before NCCL or CUDA is touched; an empty call is
+    a no-op; the staging size is 2 slots of one chunk."""
+    import ctypes as C
+    lib = C.CDLL(str(product_libs.KVX_LIB))
+    lib.kvx_migrate_nccl.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_uint64, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
+    lib.kvx_migrate_nccl_staging_bytes.restype = C.c_uint64
+    lib.kvx_migrate_nccl_staging_bytes.argtypes = [C.c_uint64, C.c_uint64]
+    assert lib.kvx_migrate_nccl_staging_bytes(65536, 512) == 2 * 65536 * 512
+    assert lib.kvx_migrate_nccl(None, None, 0, -1, None, None, 0, -1, 16, None, None, 0, None) == 0
+    fake = C.c_void_p(0x1000)
+    # pages to send but no pool / ids / comm
+    assert lib.kvx_migrate_nccl(None, None, 4, 1, None, None, 0, -1, 16, fake, fake, 1 << 30, None) == 2
+    assert lib.kvx_migrate_nccl(fake, fake, 4, 1, None, None, 0, -1, 16, None, fake, 1 << 30, None) == 2
+    assert lib.kvx_migrate_nccl(fake, fake, 4, -1, None, None, 0, -1, 16, fake, fake, 1 << 30, None) == 2
+    assert lib.kvx_migrate_nccl(fake, fake, 4, 1, None, None, 0, -1, 0, fake, fake, 1 << 30, None) == 2
