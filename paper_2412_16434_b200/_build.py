@@ -47,7 +47,7 @@ def build_oracle(ref: bool = True) -> None:
     ref_src = Path(os.environ.get("REF", "/root/reference/proj")) / "src" / "kvstore.cpp"
     if ref and ref_src.exists():
         _make(ORACLE_DIR, "ref")
-        for name in ("build_payload_sim.sh", "build_serve_sim.sh"):
+        for name in ("build_payload_sim.sh", "build_serve_sim.sh", "build_serve_gpu.sh"):
             script = ROOT / "tests" / "cpp" / name
             proc = subprocess.run(["bash", str(script)], capture_output=True, text=True)
             if proc.returncode != 0:

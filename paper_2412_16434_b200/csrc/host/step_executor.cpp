@@ -122,6 +122,16 @@ Ns GpuStepExecutor::decode_step(const std::vector<Row>& rows) {
     max_ctx = std::max(max_ctx, rows[i].ctx_tokens);
     stats_.attended_tokens += rows[i].ctx_tokens;
   }
+  // Table width and planning context in buckets (2^k and 1.5 x 2^k blocks):
+  // steps of the same batch size then share one launch shape, which the
+  // model replays as a CUDA graph. Padding entries are never read (each
+  // request attends over its own ctx_lens[b] tokens).
+  {
+    std::uint32_t bucket = 16;
+    while (bucket < max_blocks) bucket = (bucket & (bucket - 1)) == 0 ? bucket + bucket / 2 : (bucket / 3) * 4;
+    max_blocks = bucket;
+    max_ctx = static_cast<std::int64_t>(max_blocks) * T;
+  }
   // Host staging: [tables L*B*max_blocks u32][ctx B][sessions B][tokens B].
   const std::size_t tab_bytes = up16(static_cast<std::size_t>(L) * B * max_blocks * 4);
   const std::size_t vec_bytes = up16(static_cast<std::size_t>(B) * 4);

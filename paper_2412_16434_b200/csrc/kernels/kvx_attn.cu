@@ -294,9 +294,6 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
         const int row_v = row_k + a.heads * kT;
         const uint32_t st = ring_s + (i % kStages) * kStageBytes;
         const uint32_t bar = smem_u32(&s_full[warp * kStages + (i % kStages)]);
-        // The stage was last read by this warp's ldmatrix (generic proxy):
-        // order those reads before the async-proxy writes.
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(&s_full[warp * kStages + (i % kStages)], kStageBytes);
         tma_load_2d(st, &a.tmap, 0, row_k, bar);
         tma_load_2d(st + 2048, &a.tmap, 64, row_k, bar);
@@ -452,6 +449,9 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
       mma_bf16(o[n], pa, b0, b1);
       mma_bf16(o[n + 1], pa, b2, b3);
     }
+    // The stage is refilled next by the TMA unit (async proxy): every lane
+    // orders its ldmatrix reads of it before that write (WAR across proxies).
+    if (kTma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
   }
   if (!kTma) cp_async_wait<0>();

@@ -29,8 +29,11 @@
 #include <cublas_v2.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "kvx_common.cuh"
@@ -55,6 +58,18 @@ struct kvx_model {
   int32_t* tokens = nullptr;
   void* attn_ws = nullptr;
   uint64_t attn_ws_bytes = 0;
+  void* blas_ws = nullptr;  // cuBLAS workspace: no allocation inside graph capture
+  // Decode steps replayed as CUDA graphs, per launch shape (pointers and
+  // sizes): the ~330 launches of a Llama-8B step cost more host time than
+  // the GPU takes for the small-batch kernels.
+  using StepKey = std::tuple<const void*, const void*, const void*, const void*, const void*, void*, int, int, int,
+                             uint64_t, int, void*>;
+  struct StepGraph {
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;  // this library's kernels inside the graph
+  };
+  std::map<StepKey, StepGraph> step_graphs;
 };
 
 namespace kvx {
@@ -335,6 +350,16 @@ int kvx_model_create(int device, const kvx_model_config* cfg, uint64_t seed, kvx
     kvx::set_error("kvx_model_create: cublasCreate failed");
     return KVX_ERR_CUDA;
   }
+  constexpr size_t kBlasWs = 64u << 20;
+  if (cudaMalloc(&m->blas_ws, kBlasWs) != cudaSuccess ||
+      cublasSetWorkspace(m->blas, m->blas_ws, kBlasWs) != CUBLAS_STATUS_SUCCESS) {
+    cudaGetLastError();
+    cublasDestroy(m->blas);
+    cudaFree(m->blas_ws);
+    delete m;
+    kvx::set_error("kvx_model_create: cuBLAS workspace");
+    return KVX_ERR_CUDA;
+  }
   m->slab_bytes = kvx_model_weight_bytes(cfg);
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&m->slab), m->slab_bytes);
   if (e != cudaSuccess) {
@@ -385,12 +410,28 @@ int kvx_model_destroy(kvx_model* m) {
                   static_cast<void*>(m->q), static_cast<void*>(m->kv_new), static_cast<void*>(m->attn),
                   static_cast<void*>(m->gu), static_cast<void*>(m->act), static_cast<void*>(m->logits),
                   static_cast<void*>(m->attn_f32), static_cast<void*>(m->tokens), m->attn_ws,
-                  static_cast<void*>(m->slab)})
+                  static_cast<void*>(m->slab), m->blas_ws})
     cudaFree(p);
+  for (auto& g : m->step_graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
   if (m->blas) cublasDestroy(m->blas);
   delete m;
   return KVX_OK;
 }
+
+}  // extern "C"
+
+namespace kvx {
+namespace {
+int enqueue_decode(kvx_model* m, kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* ap,
+                   const uint32_t* d_tables, const int32_t* d_ctx_lens, const int32_t* d_sessions,
+                   const int32_t* d_tokens_in, int32_t batch, int32_t max_blocks, int32_t max_ctx, uint64_t fill_seed,
+                   int32_t fill_mode, void* const* layer_waits, const int32_t* layer_wait_offsets,
+                   int32_t* d_tokens_out);
+}  // namespace
+}  // namespace kvx
+
+extern "C" {
 
 int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* layout, const uint32_t* d_tables,
                           const int32_t* d_ctx_lens, const int32_t* d_sessions, const int32_t* d_tokens_in,
@@ -424,6 +465,59 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
     KVX_CUDA_TRY(cudaMemsetAsync(m->attn_ws, 0, cap, st), "kvx_model: attention workspace");
     m->attn_ws_bytes = cap;
   }
+  const bool waits = layer_waits && layer_wait_offsets && layer_wait_offsets[c.num_layers] > 0;
+  static const char* graphs_env = std::getenv("KVX_MODEL_GRAPHS");
+  const bool graphs = !(graphs_env && graphs_env[0] == '0');
+  if (!waits && graphs) {
+    // Same shape seen before: replay (captured on the second sighting, so
+    // every one-time allocation / attribute / plan happened eagerly first).
+    const kvx_model::StepKey key{pool, d_tables, d_ctx_lens, d_sessions, d_tokens_in, d_tokens_out, batch, max_blocks,
+                                 max_ctx, fill_seed, fill_mode, stream};
+    kvx_model::StepGraph& g = m->step_graphs[key];
+    if (g.exec) {
+      KVX_CUDA_TRY(cudaGraphLaunch(g.exec, st), "kvx_model: graph launch");
+      kvx::note_launch(g.launches);
+      return KVX_OK;
+    }
+    if (g.seen++ > 0) {
+      const uint64_t n0 = kvx_launch_count();
+      KVX_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "kvx_model: begin capture");
+      const int rc = kvx::enqueue_decode(m, pool, layout, &ap, d_tables, d_ctx_lens, d_sessions, d_tokens_in, batch,
+                                         max_blocks, max_ctx, fill_seed, fill_mode, nullptr, nullptr, d_tokens_out);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(st, &graph);
+      if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      KVX_CUDA_TRY(e, "kvx_model: end capture");
+      const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      KVX_CUDA_TRY(ei, "kvx_model: graph instantiate");
+      g.launches = kvx_launch_count() - n0;
+      KVX_CUDA_TRY(cudaGraphLaunch(g.exec, st), "kvx_model: graph launch");
+      return KVX_OK;
+    }
+  }
+  return kvx::enqueue_decode(m, pool, layout, &ap, d_tables, d_ctx_lens, d_sessions, d_tokens_in, batch, max_blocks,
+                             max_ctx, fill_seed, fill_mode, layer_waits, layer_wait_offsets, d_tokens_out);
+}
+
+}  // extern "C"
+
+namespace kvx {
+namespace {
+
+// The launch sequence of one decode step (eager, or recorded into a graph).
+int enqueue_decode(kvx_model* m, kvx_pool* pool, const kvx_page_layout* layout, const kvx_attn_params* ap_in,
+                   const uint32_t* d_tables, const int32_t* d_ctx_lens, const int32_t* d_sessions,
+                   const int32_t* d_tokens_in, int32_t batch, int32_t max_blocks, int32_t max_ctx, uint64_t fill_seed,
+                   int32_t fill_mode, void* const* layer_waits, const int32_t* layer_wait_offsets,
+                   int32_t* d_tokens_out) {
+  const kvx_model_config& c = m->cfg;
+  void* stream = m->stream;
+  cudaStream_t st = as_stream(stream);
+  kvx_attn_params ap = *ap_in;
   kvx::embed_rows<<<batch, 128, 0, st>>>(m->embed, d_tokens_in, m->x, c.hidden, c.vocab);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: embed");
   kvx::note_launch();
@@ -457,6 +551,11 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
   }
   return kvx::sample(m, 0, batch, d_tokens_out);
 }
+
+}  // namespace
+}  // namespace kvx
+
+extern "C" {
 
 int kvx_model_prefill(kvx_model* m, int32_t tokens, void* stream) {
   if (!m) return kvx::fail_arg("kvx_model_prefill: null model");

@@ -60,6 +60,9 @@ struct Args {
   int verify_every = 0;
   std::uint64_t seed = 0;
   bool calibrate_only = false;
+  int profile_batch = 0;   // --profile-batch B: only time decode steps at batch B (ncu / nsys target)
+  int profile_steps = 20;
+  int profile_ctx = 1024;
   int max_batch = 64;
 };
 
@@ -143,10 +146,11 @@ struct Calibration {
   double prefill_tps = 0;
 };
 
-Calibration calibrate(ModelRuntime& rt, int ctx) {
+Calibration calibrate(ModelRuntime& rt, int ctx, int only_batch = 0, int reps = 5) {
   Calibration cal;
-  const int batches[] = {1, 2, 4, 8, 16, 32, 64};
-  const int sessions = 64;
+  std::vector<int> batches = {1, 2, 4, 8, 16, 32, 64};
+  if (only_batch > 0) batches = {only_batch};
+  const int sessions = std::max(64, only_batch);
   GpuProfile gpu;
   gpu.kv_bytes_per_token = kBytesPerToken;
   gpu.num_layers = kLayers;
@@ -171,9 +175,10 @@ Calibration calibrate(ModelRuntime& rt, int ctx) {
     std::vector<StepExecutor::Row> rows;
     for (int i = 0; i < b; ++i) rows.push_back({static_cast<std::uint32_t>(i), ctx});
     std::vector<double> ms;
-    for (int rep = 0; rep < 5; ++rep) ms.push_back(to_ms(exec.decode_step(rows)));
+    for (int rep = 0; rep < reps; ++rep) ms.push_back(to_ms(exec.decode_step(rows)));
     cal.curve.emplace_back(b, traffic::percentile(ms, 0.5));
   }
+  if (only_batch > 0) return cal;
   double tps = 0;
   for (int tokens : {512, 2048}) {
     std::vector<double> ns;
@@ -214,9 +219,18 @@ int main(int argc, char** argv) {
     else if (k == "--seed") a.seed = std::strtoull(next().c_str(), nullptr, 10);
     else if (k == "--max-batch") a.max_batch = std::atoi(next().c_str());
     else if (k == "--calibrate-only") a.calibrate_only = true;
+    else if (k == "--profile-batch") a.profile_batch = std::atoi(next().c_str());
+    else if (k == "--profile-steps") a.profile_steps = std::atoi(next().c_str());
+    else if (k == "--profile-ctx") a.profile_ctx = std::atoi(next().c_str());
   }
   const auto t_start = std::chrono::steady_clock::now();
   ModelRuntime rt(0, llama31_8b_config(), 0x8B8B8Bull);
+  if (a.profile_batch > 0) {  // profiling target: decode steps only
+    const Calibration p = calibrate(rt, a.profile_ctx, a.profile_batch, a.profile_steps);
+    std::printf("{\"profile\": {\"batch\": %d, \"ctx\": %d, \"steps\": %d, \"decode_ms_p50\": %.4f}}\n",
+                a.profile_batch, a.profile_ctx, a.profile_steps, p.curve[0].second);
+    return 0;
+  }
   const Calibration cal = calibrate(rt, 1024);
   std::printf("{\"calibration\": {\"model\": \"llama-3.1-8b shape, random bf16 weights\", \"ctx\": 1024, "
               "\"decode_curve_ms\": [");
