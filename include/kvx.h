@@ -62,7 +62,7 @@ extern "C" {
 #define KVX_COPY_AUTO 0   /* TMA for local HBM<->HBM, SM for peer/host pools */
 #define KVX_COPY_SM 1     /* SM kernel, 16-B vector loads/stores             */
 #define KVX_COPY_TMA 2    /* SM kernel, cp.async.bulk (TMA) through smem     */
-#define KVX_COPY_CE 3     /* copy engines (cudaMemcpyBatchAsync); host ids   */
+#define KVX_COPY_CE 3     /* copy engines (one memcpy per id run); host ids  */
 
 typedef struct kvx_pool kvx_pool;
 

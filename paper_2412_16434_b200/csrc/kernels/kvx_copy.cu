@@ -400,34 +400,21 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
     const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
     return kvx::launch_move(a, mode, dev, st, "kvx_copy_pages", local, max_ctas);
   }
-  // Copy engines: coalesce runs of consecutive ids, one batched submission.
-  std::vector<void*> dsts, srcs;
-  std::vector<size_t> sizes;
+  // Copy engines: coalesce runs of consecutive ids, one cudaMemcpyAsync per
+  // run (the payload deals new pages in ascending order, so a layer's pages
+  // are usually one or a few runs). Graph capture records one memcpy node per
+  // run.
   for (uint64_t i = 0; i < n;) {
     if (src_ids[i] >= src->num_pages || dst_ids[i] >= dst->num_pages)
       return kvx::fail_arg("kvx_copy_pages: page id out of range");
     uint64_t j = i + 1;
     while (j < n && src_ids[j] == src_ids[j - 1] + 1 && dst_ids[j] == dst_ids[j - 1] + 1) ++j;
-    srcs.push_back(src->base + static_cast<uint64_t>(src_ids[i]) * src->page_bytes);
-    dsts.push_back(dst->base + static_cast<uint64_t>(dst_ids[i]) * dst->page_bytes);
-    sizes.push_back((j - i) * src->page_bytes);
+    KVX_CUDA_TRY(cudaMemcpyAsync(dst->base + static_cast<uint64_t>(dst_ids[i]) * dst->page_bytes,
+                                 src->base + static_cast<uint64_t>(src_ids[i]) * src->page_bytes,
+                                 (j - i) * src->page_bytes, cudaMemcpyDefault, st),
+                 "kvx_copy_pages(CE)");
     i = j;
   }
-  cudaStreamCaptureStatus capturing = cudaStreamCaptureStatusNone;
-  if (st != nullptr) KVX_CUDA_TRY(cudaStreamIsCapturing(st, &capturing), "kvx_copy_pages(CE)");
-  // The batch API needs an explicit stream and cannot be graph-captured; one
-  // memcpy node per run of consecutive pages can.
-  if (st == nullptr || capturing != cudaStreamCaptureStatusNone) {
-    for (size_t r = 0; r < srcs.size(); ++r)
-      KVX_CUDA_TRY(cudaMemcpyAsync(dsts[r], srcs[r], sizes[r], cudaMemcpyDefault, st), "kvx_copy_pages(CE)");
-    return KVX_OK;
-  }
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  size_t attr_idx = 0, fail_idx = 0;
-  KVX_CUDA_TRY(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1,
-                                    &fail_idx, st),
-               "kvx_copy_pages(CE): cudaMemcpyBatchAsync");
   return KVX_OK;
 }
 
