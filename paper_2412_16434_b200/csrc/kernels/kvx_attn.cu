@@ -176,7 +176,7 @@ struct AttnArgs {
   uint32_t* arrivals; // [B][H] split counters; zero between launches
   int cluster_merge;  // 1: the splits of a (request, kv head) form one cluster; merge over DSMEM
   int early_prefetch; // KVX_ATTN_EARLY_PREFETCH: table + first pages before griddepcontrol.wait
-  int signal_early;   // cluster launches: launch_dependents after the page loop (else after the merge)
+  int signal_at;      // launch_dependents: 0 after the split merge, 1 after the page loop, 2 at kernel start
   int heads;          // kv heads
   int group;          // q heads per kv head
   int max_blocks;
@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
   // table and each warp's first pages are fetched before the wait.
   const bool early = a.early_prefetch != 0;
   KVX_TRACE(0);
+  if (a.signal_at == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
   KVX_TRACE(1);
   const int ctx = a.ctx_lens[b];
@@ -461,8 +462,9 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
   // start launching into SMs as ours drain. Cluster launches with many CTAs
   // each streaming a long slice signal only at the very end (below): there,
   // dependents resident this early cost more than their early start gains
-  // (host-side choice, signal_early; profiles/attn_trace/r01_cluster_signal.log).
-  if (!a.cluster_merge || a.signal_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // (host-side choice, signal_at; profiles/attn_trace/r01_cluster_signal.log).
+  if (a.signal_at == 1 || (!a.cluster_merge && a.signal_at == 0))
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // Full row sums across the 4 lanes sharing a row.
   l_r += __shfl_xor_sync(0xffffffffu, l_r, 1);
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
       a.out[(static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
     }
     KVX_TRACE(6);
-    if (!a.signal_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (a.signal_at == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
   for (int e = threadIdx.x; e < rows * kD; e += blockDim.x) {
@@ -983,7 +985,10 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
       const int pages = std::max(1, (max_ctx + kvx::kT - 1) / kvx::kT);
       const int per_cta = (pages + splits - 1) / splits;
       const long ctas = static_cast<long>(splits) * H * batch;
-      a.signal_early = (a.early_prefetch && (ctas <= 80 || per_cta <= 256)) ? 1 : 0;
+      a.signal_at = (a.early_prefetch && (ctas <= 80 || per_cta <= 256)) ? 1 : 0;
+      // KVX_ATTN_SIGNAL=0|1|2 (after merge / after loop / at start): measurement knob.
+      static const char* sig_env = std::getenv("KVX_ATTN_SIGNAL");
+      if (sig_env && sig_env[0] >= '0' && sig_env[0] <= '2') a.signal_at = sig_env[0] - '0';
     }
     if (splits > 1 && !plan.cluster) {
       const uint64_t rows = static_cast<uint64_t>(batch) * Hq;

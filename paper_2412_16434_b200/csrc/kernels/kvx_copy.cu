@@ -18,6 +18,7 @@
 #include <atomic>
 #include <mutex>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "kvx_common.cuh"
@@ -236,6 +237,46 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
   return KVX_OK;
 }
 
+// Host-listed page moves (KVX_COPY_CE with fragmented id runs): the id
+// pairs travel in the launch's parameter block (no upload, no device id
+// array), and a few CTAs of the LDG/STG.128 mover stream the pages. Used for
+// PCIe moves between HBM and a pinned, mapped HOST pool when the pages do not
+// form long runs: per run a copy-engine submission costs microseconds of
+// launch overhead, a 64 KiB page only ~1.2 us of PCIe time. Measured on B200
+// (profiles/r01_pcie_movers.json.txt): SM zero-copy moves 51-53 GB/s per
+// direction, fragmented or not, against 55-57 for copy engines on long runs.
+constexpr int kListedPairs = 3840;  // 30 KiB of ids + header < the 32,764-B parameter limit
+struct ListedMove {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t page_bytes;
+  uint32_t n;
+  uint32_t chunks_per_page;
+  uint32_t src_ids[kListedPairs];
+  uint32_t dst_ids[kListedPairs];
+};
+
+__global__ void __launch_bounds__(kVecThreads) page_move_listed(const __grid_constant__ ListedMove a) {
+  const uint64_t items = static_cast<uint64_t>(a.n) * a.chunks_per_page;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint32_t i = static_cast<uint32_t>(item / a.chunks_per_page);
+    const uint64_t off = (item - static_cast<uint64_t>(i) * a.chunks_per_page) * kVecChunk;
+    const int4* s = reinterpret_cast<const int4*>(a.src + static_cast<uint64_t>(a.src_ids[i]) * a.page_bytes + off);
+    int4* d = reinterpret_cast<int4*>(a.dst + static_cast<uint64_t>(a.dst_ids[i]) * a.page_bytes + off);
+    const uint64_t left = a.page_bytes - off;
+    const uint32_t vecs = static_cast<uint32_t>((left < kVecChunk ? left : kVecChunk) / 16);
+    if (vecs == kVecThreads * kVecUnroll) {
+      int4 r[kVecUnroll];
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) r[u] = ld_stream(s + threadIdx.x + u * kVecThreads);
+#pragma unroll
+      for (int u = 0; u < kVecUnroll; ++u) st_stream(d + threadIdx.x + u * kVecThreads, r[u]);
+    } else {
+      for (uint32_t v = threadIdx.x; v < vecs; v += kVecThreads) st_stream(d + v, ld_stream(s + v));
+    }
+  }
+}
+
 // ---- K5: contents -----------------------------------------------------------
 
 // 16-byte vector v of a page whose tag hashes to h (K5 content).
@@ -400,13 +441,49 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
     const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
     return kvx::launch_move(a, mode, dev, st, "kvx_copy_pages", local, max_ctas);
   }
-  // Copy engines: coalesce runs of consecutive ids, one cudaMemcpyAsync per
-  // run (the payload deals new pages in ascending order, so a layer's pages
-  // are usually one or a few runs). Graph capture records one memcpy node per
-  // run.
-  for (uint64_t i = 0; i < n;) {
+  // Host id lists: copy engines, one cudaMemcpyAsync per run of consecutive
+  // ids, when the pages form long runs (the payload deals new pages in
+  // ascending order); otherwise the listed-id SM mover, ids in the launch
+  // parameters. Graph capture records one memcpy node per run / one kernel
+  // node per chunk of kListedPairs pages.
+  uint64_t runs = 0;
+  for (uint64_t i = 0; i < n; ++i) {
     if (src_ids[i] >= src->num_pages || dst_ids[i] >= dst->num_pages)
       return kvx::fail_arg("kvx_copy_pages: page id out of range");
+    runs += i == 0 || src_ids[i] != src_ids[i - 1] + 1 || dst_ids[i] != dst_ids[i - 1] + 1;
+  }
+  const uint64_t run_bytes = n * src->page_bytes / runs;
+  static const uint64_t min_run = [] {
+    const char* e = std::getenv("KVX_CE_MIN_RUN_BYTES");
+    return e ? std::strtoull(e, nullptr, 10) : (uint64_t{1} << 20);
+  }();
+  // Every pool is device-addressable here: HBM, IPC-opened peer HBM, or
+  // pinned host memory allocated mapped (UVA: host pointer == device pointer).
+  if (run_bytes < min_run && src->page_bytes % 16 == 0 && (src->device >= 0 || dst->device >= 0)) {
+    const int dev = src->device >= 0 ? src->device : dst->device;
+    kvx::DeviceGuard guard(dev);
+    static thread_local kvx::ListedMove m;
+    m.src = src->base;
+    m.dst = dst->base;
+    m.page_bytes = src->page_bytes;
+    m.chunks_per_page = static_cast<uint32_t>((src->page_bytes + kvx::kVecChunk - 1) / kvx::kVecChunk);
+    static const unsigned ctas = [] {
+      const char* e = std::getenv("KVX_LISTED_CTAS");
+      return e ? static_cast<unsigned>(std::atoi(e)) : 64u;
+    }();
+    for (uint64_t at = 0; at < n; at += kvx::kListedPairs) {
+      m.n = static_cast<uint32_t>(std::min<uint64_t>(kvx::kListedPairs, n - at));
+      std::memcpy(m.src_ids, src_ids + at, m.n * sizeof(uint32_t));
+      std::memcpy(m.dst_ids, dst_ids + at, m.n * sizeof(uint32_t));
+      const uint64_t items = static_cast<uint64_t>(m.n) * m.chunks_per_page;
+      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, std::max(1u, ctas)));
+      kvx::page_move_listed<<<grid, kvx::kVecThreads, 0, st>>>(m);
+      kvx::note_launch();
+      KVX_CUDA_TRY(cudaGetLastError(), "kvx_copy_pages(listed)");
+    }
+    return KVX_OK;
+  }
+  for (uint64_t i = 0; i < n;) {
     uint64_t j = i + 1;
     while (j < n && src_ids[j] == src_ids[j - 1] + 1 && dst_ids[j] == dst_ids[j - 1] + 1) ++j;
     KVX_CUDA_TRY(cudaMemcpyAsync(dst->base + static_cast<uint64_t>(dst_ids[i]) * dst->page_bytes,

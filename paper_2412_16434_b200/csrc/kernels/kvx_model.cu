@@ -62,8 +62,12 @@ struct kvx_model {
   // Decode steps replayed as CUDA graphs, per launch shape (pointers and
   // sizes): the ~330 launches of a Llama-8B step cost more host time than
   // the GPU takes for the small-batch kernels.
+  // Every buffer a graph captured is either in the key (caller pointers, the
+  // pool's memory) or owned here; reallocating an owned buffer (activations
+  // grown by a bigger batch or a prefill, the attention workspace) drops
+  // every graph (drop_step_graphs).
   using StepKey = std::tuple<const void*, const void*, const void*, const void*, const void*, void*, int, int, int,
-                             uint64_t, int, void*>;
+                             uint64_t, int, void*, const void*, uint64_t>;
   struct StepGraph {
     int seen = 0;
     cudaGraphExec_t exec = nullptr;
@@ -240,11 +244,20 @@ int linear(kvx_model* m, const uint16_t* X, const uint16_t* W, uint16_t* Y, int 
   return KVX_OK;
 }
 
+// Captured decode-step graphs hold the addresses of the activations and the
+// workspace: called (after a stream sync) before either is reallocated.
+void drop_step_graphs(kvx_model* m) {
+  for (auto& g : m->step_graphs)
+    if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
+  m->step_graphs.clear();
+}
+
 int ensure_rows(kvx_model* m, int rows) {
   if (rows <= m->rows_cap) return KVX_OK;
   const kvx_model_config& c = m->cfg;
   cudaStream_t st = as_stream(m->stream);
   if (m->x) KVX_CUDA_TRY(cudaStreamSynchronize(st), "kvx_model: sync");
+  drop_step_graphs(m);
   for (void* p : {static_cast<void*>(m->x), static_cast<void*>(m->h), static_cast<void*>(m->qkv),
                   static_cast<void*>(m->q), static_cast<void*>(m->kv_new), static_cast<void*>(m->attn),
                   static_cast<void*>(m->gu), static_cast<void*>(m->act), static_cast<void*>(m->logits),
@@ -457,6 +470,7 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
   if (ws > m->attn_ws_bytes) {
     if (m->attn_ws) {
       KVX_CUDA_TRY(cudaStreamSynchronize(st), "kvx_model: sync");
+      kvx::drop_step_graphs(m);
       cudaFree(m->attn_ws);
       m->attn_ws = nullptr;
     }
@@ -471,8 +485,9 @@ int kvx_model_decode_step(kvx_model* m, kvx_pool* pool, const kvx_page_layout* l
   if (!waits && graphs) {
     // Same shape seen before: replay (captured on the second sighting, so
     // every one-time allocation / attribute / plan happened eagerly first).
-    const kvx_model::StepKey key{pool, d_tables, d_ctx_lens, d_sessions, d_tokens_in, d_tokens_out, batch, max_blocks,
-                                 max_ctx, fill_seed, fill_mode, stream};
+    const kvx_model::StepKey key{pool,     d_tables,  d_ctx_lens, d_sessions,    d_tokens_in,
+                                 d_tokens_out, batch,   max_blocks, max_ctx,     fill_seed,
+                                 fill_mode, stream,  kvx_pool_base(pool), kvx_pool_num_pages(pool)};
     kvx_model::StepGraph& g = m->step_graphs[key];
     if (g.exec) {
       KVX_CUDA_TRY(cudaGraphLaunch(g.exec, st), "kvx_model: graph launch");

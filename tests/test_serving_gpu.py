@@ -25,7 +25,7 @@ def test_gpu_executed_serving_consumes_bit_exact_caches(tmp_path):
     if not BIN.exists():
         pytest.skip("serve_gpu not built (tests/cpp/build_serve_gpu.sh needs /root/reference)")
     cmd = [str(BIN), "--config", "5", "--policies", "symphony,swap,recompute", "--users", "12", "--sessions", "16",
-           "--nodes", "2", "--device-gb", "2", "--host-gb", "1", "--verify-every", "1", "--disk-dir", str(tmp_path)]
+           "--nodes", "2", "--device-gb", "8", "--host-gb", "8", "--verify-every", "1", "--disk-dir", str(tmp_path)]
     proc = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     assert proc.returncode == 0, proc.stdout[-3000:] + proc.stderr[-3000:]
     lines = [json.loads(ln) for ln in proc.stdout.splitlines() if ln.startswith("{")]
