@@ -326,6 +326,14 @@ int kvx_model_decode_step(kvx_model* model, kvx_pool* pool, const kvx_page_layou
  * MLPs, 4,096-row passes, LM head of the last token). The prompt's K/V pages
  * are the store's Created fill; prefill attention is not executed. */
 int kvx_model_prefill(kvx_model* model, int32_t tokens, void* stream);
+/* One projection of the model's kind, Y[rows][out] (+= when accumulate)
+ * X[rows][in] . W[out][in]^T (bf16 in/out, fp32 accumulation), on the model's
+ * workspace: K7 (skinny_linear, tensor-core mma over streamed weights) for
+ * rows <= 16 with in % 128 == 0 and out % 16 == 0, cuBLAS otherwise — the
+ * decode step's projection path, exposed for tests and measurement. The
+ * shape must be one of the model's (its split-K workspace is sized for them). */
+int kvx_model_linear(kvx_model* model, const void* d_x, const void* d_w, void* d_y, int32_t rows, int32_t in,
+                     int32_t out, int32_t accumulate, void* stream);
 /* Timing helpers for hosts without CUDA headers: events with timing. */
 int kvx_timer_create(void** out);
 int kvx_timer_elapsed_ms(void* start, void* stop, float* ms);

@@ -45,6 +45,7 @@
 // receiver-GPU memory while the ledger still says Host (kvstore.cpp:914-923),
 // which keeps ledger parity exact (SURVEY.md §7 hard part 2, option 1).
 
+#include <algorithm>
 #include <cstdint>
 #include <deque>
 #include <initializer_list>
@@ -209,6 +210,12 @@ class NodePayload final : public TierBackend {
   static Copies& at(Row& r, std::uint32_t b) {
     if (b >= r.b.size()) r.b.resize(static_cast<std::size_t>(b) + 1);
     return r.b[b];
+  }
+  // Grows the row once to hold every block of `blocks` (not one at() at a time).
+  static void presize(Row& r, const std::vector<std::uint32_t>& blocks) {
+    if (blocks.empty()) return;
+    const std::uint32_t hi = *std::max_element(blocks.begin(), blocks.end());
+    if (hi >= r.b.size()) r.b.resize(static_cast<std::size_t>(hi) + 1);
   }
   void drop_row_if_empty(std::uint32_t s, std::uint16_t l);
 

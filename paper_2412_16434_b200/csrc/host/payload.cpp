@@ -262,7 +262,7 @@ void NodePayload::seal_released() {
       --held_[r.pool];
     }
   } else {
-    h.pages.swap(released_);
+    h.pages.assign(released_.begin(), released_.end());  // released_ keeps its capacity
     quarantine_.push_back(std::move(h));
   }
   released_.clear();
@@ -630,6 +630,7 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
 
   if (why == BlockEvent::Created) {
     Row& r = row(session, layer);
+    presize(r, blocks);
     for (std::uint32_t b : blocks) {
       Copies& c = at(r, b);
       release(c.tier(t));
@@ -682,6 +683,7 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
   std::vector<bool> used(f.blocks.size(), false);
   std::vector<std::uint32_t> missing;
   Row& r = row(session, layer);
+  presize(r, blocks);
   std::size_t cursor = 0;  // both lists usually ascend: a merge walk, bisection otherwise
   for (std::uint32_t b : blocks) {
     std::size_t i = cursor;
@@ -727,6 +729,7 @@ void NodePayload::move_now(std::uint32_t session, std::uint16_t layer, Tier tier
   }
   std::vector<Ref> src, dst;
   Row& r = row(session, layer);
+  presize(r, blocks);
   for (std::uint32_t b : blocks) {
     const Ref from = src_node->best_source(session, layer, b, src_node == this ? t : -1);
     if (from.pool < 0)

@@ -180,6 +180,7 @@ struct AttnArgs {
   int heads;          // kv heads
   int group;          // q heads per kv head
   int max_blocks;
+  int spec_pages;     // pages of the host's max_ctx: the slice the table is staged for before ctx_lens[b] arrives
   int splits;
   float scale_log2;
 };
@@ -240,7 +241,20 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
   if (a.signal_at == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
   KVX_TRACE(1);
+  const uint32_t* table = a.tables + static_cast<uint64_t>(b) * a.max_blocks;
+  // Stage this CTA's slice of the block table once (one coalesced read
+  // instead of a dependent global load in front of every page fetch). The
+  // slice depends on ctx_lens[b]; it is staged speculatively for a request
+  // of the host's max_ctx (spec_pages <= max_blocks: inside the row), so the
+  // table read does not wait for the ctx read — at batch 1, and whenever the
+  // request is a longest one, the guess is the slice. Otherwise it is staged
+  // again. Entries are checked against the pool when a page is issued.
+  const int s_per = (a.spec_pages + a.splits - 1) / a.splits;
+  const int s_begin = split * s_per;
+  const int s_end = min(a.spec_pages, s_begin + s_per);
   const int ctx = a.ctx_lens[b];
+  for (int i = threadIdx.x; i < s_end - s_begin && i < kMaxPagesPerCta; i += blockDim.x)
+    s_pages[i] = __ldg(table + s_begin + i);
   // Precondition (kvx.h): 0 <= ctx_lens[b] <= max_ctx <= max_blocks * 16. A
   // longer request would read past its table row and overflow the staged
   // slice below: fail loudly instead of corrupting memory.
@@ -250,7 +264,6 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
   const int p_begin = split * per_split;
   const int p_end = min(n_pages, p_begin + per_split);
   if (p_end - p_begin > kMaxPagesPerCta) __trap();
-  const uint32_t* table = a.tables + static_cast<uint64_t>(b) * a.max_blocks;
   const int hq0 = h * a.group;
   // Q as mma A fragments. Rows = the group's query heads, zero-padded to 16.
   uint32_t qa[kD / 16][4];
@@ -269,12 +282,9 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
   };
   if (!early) load_q();  // issued first: its latency overlaps the table read
 
-  // Stage this CTA's slice of the block table once (one coalesced read
-  // instead of a dependent global load in front of every page fetch).
-  for (int i = threadIdx.x; i < p_end - p_begin; i += blockDim.x) {
-    const uint32_t page = __ldg(table + p_begin + i);
-    if (page >= a.pool_pages) __trap();  // corrupt block table: fail loudly
-    s_pages[i] = page;
+  if (p_begin != s_begin || p_end != s_end) {  // a shorter request: its own slice
+    __syncthreads();
+    for (int i = threadIdx.x; i < p_end - p_begin; i += blockDim.x) s_pages[i] = __ldg(table + p_begin + i);
   }
   __syncthreads();
 
@@ -291,6 +301,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
     if (kTma) {
       if (i < my_count && lane == 0) {
         const int p = my_first + i * W;
+        if (s_pages[p - p_begin] >= a.pool_pages) __trap();  // corrupt block table: fail loudly
         const int row_k = static_cast<int>(s_pages[p - p_begin]) * (2 * a.heads * kT) + h * kT;
         const int row_v = row_k + a.heads * kT;
         const uint32_t st = ring_s + (i % kStages) * kStageBytes;
@@ -305,6 +316,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
     }
     if (i < my_count) {
       const int p = my_first + i * W;
+      if (s_pages[p - p_begin] >= a.pool_pages) __trap();  // corrupt block table: fail loudly
       const uint8_t* page = a.pool + static_cast<uint64_t>(s_pages[p - p_begin]) * a.page_bytes;
       const uint8_t* k_src = page + static_cast<uint64_t>(h) * kTileBytes;
       const uint8_t* v_src = page + static_cast<uint64_t>(a.heads + h) * kTileBytes;
@@ -341,7 +353,9 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
     // visible to this CTA's page loads.
     if (threadIdx.x < 32) {
       const int t = ctx - 1, slot = t - (n_pages - 1) * kT;
-      uint8_t* page = const_cast<uint8_t*>(a.pool) + static_cast<uint64_t>(s_pages[n_pages - 1 - p_begin]) * a.page_bytes;
+      const uint32_t last_page = s_pages[n_pages - 1 - p_begin];
+      if (last_page >= a.pool_pages) __trap();  // corrupt block table: fail loudly
+      uint8_t* page = const_cast<uint8_t*>(a.pool) + static_cast<uint64_t>(last_page) * a.page_bytes;
       const int kv = threadIdx.x >> 4, c = threadIdx.x & 15;  // lanes 0-15: K row, 16-31: V row (16 x 16 B)
       const uint16_t* src = (kv ? a.new_v : a.new_k) + (static_cast<uint64_t>(b) * a.heads + h) * kD;
       uint8_t* dst = page + static_cast<uint64_t>((kv * a.heads + h) * kT + slot) * (kD * 2);
@@ -900,6 +914,10 @@ Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge,
     }
   }
   if (!p.cluster) p.narrow = static_cast<long>(p.splits) * groups <= sms;
+  // KVX_ATTN_NARROW=0|1 forces the 4-warp (2 CTAs/SM) / 8-warp variant of a
+  // workspace-merged launch (measurement knob).
+  static const char* narrow_env = std::getenv("KVX_ATTN_NARROW");
+  if (!p.cluster && narrow_env && (narrow_env[0] == '0' || narrow_env[0] == '1')) p.narrow = narrow_env[0] == '1';
   return p;
 }
 
@@ -971,6 +989,7 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     a.heads = H;
     a.group = group;
     a.max_blocks = params->max_blocks;
+    a.spec_pages = std::min(params->max_blocks, (max_ctx + kvx::kT - 1) / kvx::kT);
     a.splits = splits;
     a.scale_log2 = scale * kvx::kLog2e;
     a.cluster_merge = plan.cluster ? 1 : 0;

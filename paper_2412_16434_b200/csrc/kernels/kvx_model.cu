@@ -28,6 +28,7 @@
 
 #include <cublas_v2.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -59,6 +60,12 @@ struct kvx_model {
   void* attn_ws = nullptr;
   uint64_t attn_ws_bytes = 0;
   void* blas_ws = nullptr;  // cuBLAS workspace: no allocation inside graph capture
+  // K7 (skinny_linear): split-K partials and per-tile arrival counters
+  // (zero between launches), sized at creation for every projection shape.
+  float* skinny_part = nullptr;
+  uint32_t* skinny_counters = nullptr;
+  uint64_t skinny_part_floats = 0;
+  uint32_t skinny_tiles = 0;
   // Decode steps replayed as CUDA graphs, per launch shape (pointers and
   // sizes): the ~330 launches of a Llama-8B step cost more host time than
   // the GPU takes for the small-batch kernels.
@@ -234,8 +241,170 @@ const char* blas_name(cublasStatus_t s) {
     }                                                                                \
   } while (0)
 
+// ---- K7: decode projections at small batch ---------------------------------
+// At decode batch sizes a projection streams its weight matrix once and does
+// ~rows multiply-adds per weight: HBM-bound. cuBLAS reaches ~half the copy
+// roofline on these skinny shapes (a Llama-3.1-8B step took 4.5 ms for
+// ~15 GB of weights), so rows <= 16 go to this kernel:
+//   * a warp owns 16 output features x a K chunk; per 128 k each lane loads
+//     4 x 16 B of each of its two weight rows (streaming, L1 no-allocate) and
+//     the matching 16 B of X (cached: every warp of the CTA reads the same X
+//     chunk), then issues bf16 mma.sync m16n8k16 (features on M, batch rows
+//     on N). The k order inside a 32-k group is permuted identically for W
+//     and X (lane c holds physical k 8c..8c+7), so each lane's loads are
+//     whole 16-B vectors and no shuffles or shared memory are needed;
+//   * split-K sized so ~2 waves of warps stream at once; the last warp of a
+//     tile (arrival counter) sums the partials in split order (deterministic)
+//     and writes bf16 Y, adding the residual when accumulating.
+constexpr int kSkinnyMaxRows = 16;
+constexpr int kSkinnyWarps = 8;
+
+struct SkinnyArgs {
+  const uint16_t* X;  // [rows][in]
+  const uint16_t* W;  // [out][in]
+  uint16_t* Y;        // [rows][out]
+  float* part;        // [tiles][splits][NT * 128]
+  uint32_t* counters; // [tiles]
+  int rows, in, out, splits, k_chunk, accumulate;
+};
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// Cached read-only vector load, issued in program order with the streaming
+// weight loads (volatile) so a step's X loads are all in flight before its mmas.
+__device__ __forceinline__ int4 ld_nc_v4(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t v) { return __uint_as_float(static_cast<uint32_t>(v) << 16); }
+
+template <int NT>  // n-tiles of 8 batch rows: 1 (rows <= 8) or 2 (rows <= 16)
+__global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_linear(const SkinnyArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kSkinnyWarps + warp;
+  if (tile * 16 >= a.out) return;  // no block-wide barriers below
+  const int split = blockIdx.y;
+  const int k0 = split * a.k_chunk;
+  const int k1 = min(a.in, k0 + a.k_chunk);
+  const int g = lane >> 2, c = lane & 3;
+  const uint16_t* w0 = a.W + static_cast<uint64_t>(tile * 16 + g) * a.in + 8 * c;
+  const uint16_t* w8 = w0 + static_cast<uint64_t>(8) * a.in;
+  const uint16_t* xr[NT];
+  bool xv[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    xv[nt] = g + 8 * nt < a.rows;
+    xr[nt] = a.X + static_cast<uint64_t>(xv[nt] ? g + 8 * nt : 0) * a.in + 8 * c;
+  }
+  float d[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+  for (int k = k0; k < k1; k += 128) {  // in and k_chunk are multiples of 128
+    int4 wa[4], wb[4], xs[NT][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      wa[j] = ld_stream(reinterpret_cast<const int4*>(w0 + k + 32 * j));
+      wb[j] = ld_stream(reinterpret_cast<const int4*>(w8 + k + 32 * j));
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        xs[nt][j] = xv[nt] ? ld_nc_v4(xr[nt] + k + 32 * j) : make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        // virtual k {2c,2c+1 | 2c+8,2c+9} <- physical 8c+{0,1 | 2,3}, then 8c+{4,5 | 6,7}
+        mma_bf16_16816(d[nt], wa[j].x, wb[j].x, wa[j].y, wb[j].y, xs[nt][j].x, xs[nt][j].y);
+        mma_bf16_16816(d[nt], wa[j].z, wb[j].z, wa[j].w, wb[j].w, xs[nt][j].z, xs[nt][j].w);
+      }
+  }
+  if (a.splits > 1) {
+    float4* mine = reinterpret_cast<float4*>(a.part + (static_cast<uint64_t>(tile) * a.splits + split) * (NT * 128));
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) mine[nt * 32 + lane] = make_float4(d[nt][0], d[nt][1], d[nt][2], d[nt][3]);
+    __threadfence();
+    uint32_t prev = 0;
+    if (lane == 0) prev = atomicAdd(a.counters + tile, 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != static_cast<uint32_t>(a.splits - 1)) return;
+    __threadfence();
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+    const float4* all = reinterpret_cast<const float4*>(a.part + static_cast<uint64_t>(tile) * a.splits * (NT * 128));
+    for (int s2 = 0; s2 < a.splits; ++s2)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float4 v = __ldcg(all + (static_cast<uint64_t>(s2) * NT + nt) * 32 + lane);
+        d[nt][0] += v.x;
+        d[nt][1] += v.y;
+        d[nt][2] += v.z;
+        d[nt][3] += v.w;
+      }
+    if (lane == 0) a.counters[tile] = 0;  // ready for the next launch
+  }
+  // d[nt][0/1]: feature g, batch rows 8nt + 2c + {0,1}; d[nt][2/3]: feature g + 8.
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int n = 8 * nt + 2 * c + (e & 1);
+      if (n >= a.rows) continue;
+      uint16_t* y = a.Y + static_cast<uint64_t>(n) * a.out + tile * 16 + g + (e >> 1) * 8;
+      const float v = d[nt][e] + (a.accumulate ? bf16_to_f32(*y) : 0.f);
+      *y = f32_to_bf16_rne(v);
+    }
+}
+
+// Split-K factor of a skinny projection: ~2 resident waves of warps.
+void skinny_plan(int in, int out, int sms, int& splits, int& k_chunk) {
+  const int tiles = out / 16;
+  const int groups = in / 128;
+  const long target = 2L * sms * 16;  // 16 resident warps per SM (2 CTAs of 8)
+  int s = static_cast<int>(std::max(1L, (target + tiles - 1) / tiles));
+  s = std::min(s, groups);
+  k_chunk = ((groups + s - 1) / s) * 128;
+  splits = (in + k_chunk - 1) / k_chunk;
+}
+
+bool skinny_ok(int rows, int in, int out) {
+  static const char* env = std::getenv("KVX_MODEL_SKINNY");
+  if (env && env[0] == '0') return false;  // measurement knob: cuBLAS for every projection
+  return rows > 0 && rows <= kSkinnyMaxRows && in % 128 == 0 && out % 16 == 0;
+}
+
+int skinny_linear_launch(kvx_model* m, const uint16_t* X, const uint16_t* W, uint16_t* Y, int rows, int in, int out,
+                         bool accumulate, cudaStream_t st) {
+  SkinnyArgs a{X, W, Y, m->skinny_part, m->skinny_counters, rows, in, out, 1, in, accumulate ? 1 : 0};
+  skinny_plan(in, out, sm_count(m->device), a.splits, a.k_chunk);
+  const uint32_t tiles = static_cast<uint32_t>(out / 16);
+  const int nt = rows <= 8 ? 1 : 2;
+  if (a.splits > 1 && (tiles > m->skinny_tiles ||
+                       static_cast<uint64_t>(tiles) * a.splits * nt * 128 > m->skinny_part_floats))
+    return fail_arg("kvx_model: skinny projection workspace too small");
+  dim3 grid((tiles + kSkinnyWarps - 1) / kSkinnyWarps, a.splits);
+  if (nt == 1)
+    skinny_linear<1><<<grid, kSkinnyWarps * 32, 0, st>>>(a);
+  else
+    skinny_linear<2><<<grid, kSkinnyWarps * 32, 0, st>>>(a);
+  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: skinny_linear");
+  note_launch();
+  return KVX_OK;
+}
+
 // Y[rows][out] (+)= X[rows][in] . W[out][in]^T, bf16 in/out, fp32 compute.
 int linear(kvx_model* m, const uint16_t* X, const uint16_t* W, uint16_t* Y, int rows, int in, int out, bool accumulate) {
+  if (skinny_ok(rows, in, out)) return skinny_linear_launch(m, X, W, Y, rows, in, out, accumulate, as_stream(m->stream));
   const float one = 1.f, beta = accumulate ? 1.f : 0.f;
   KVX_BLAS_TRY(cublasGemmEx(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, out, rows, in, &one, W, CUDA_R_16BF, in, X, CUDA_R_16BF,
                             in, &beta, Y, CUDA_R_16BF, out, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
@@ -373,6 +542,36 @@ int kvx_model_create(int device, const kvx_model_config* cfg, uint64_t seed, kvx
     kvx::set_error("kvx_model_create: cuBLAS workspace");
     return KVX_ERR_CUDA;
   }
+  {
+    // K7 workspace for the largest split-K plan among the step's projections.
+    const int sms = kvx::sm_count(device);
+    const int shapes[5][2] = {{c.hidden, (c.num_q_heads + 2 * c.num_kv_heads) * c.head_dim},
+                              {c.num_q_heads * c.head_dim, c.hidden},
+                              {c.hidden, 2 * c.intermediate},
+                              {c.intermediate, c.hidden},
+                              {c.hidden, c.vocab}};
+    for (const auto& sh : shapes) {
+      if (sh[0] % 128 || sh[1] % 16) continue;
+      int splits = 1, chunk = 0;
+      kvx::skinny_plan(sh[0], sh[1], sms, splits, chunk);
+      m->skinny_tiles = std::max<uint32_t>(m->skinny_tiles, static_cast<uint32_t>(sh[1] / 16));
+      if (splits > 1) m->skinny_part_floats = std::max<uint64_t>(m->skinny_part_floats, uint64_t(sh[1] / 16) * splits * 256);
+    }
+    if (cudaMalloc(reinterpret_cast<void**>(&m->skinny_part), std::max<uint64_t>(m->skinny_part_floats, 1) * 4) !=
+            cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&m->skinny_counters), std::max<uint32_t>(m->skinny_tiles, 1) * 4) !=
+            cudaSuccess ||
+        cudaMemset(m->skinny_counters, 0, std::max<uint32_t>(m->skinny_tiles, 1) * 4) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(m->skinny_part);
+      cudaFree(m->skinny_counters);
+      cublasDestroy(m->blas);
+      cudaFree(m->blas_ws);
+      delete m;
+      kvx::set_error("kvx_model_create: projection workspace");
+      return KVX_ERR_CUDA;
+    }
+  }
   m->slab_bytes = kvx_model_weight_bytes(cfg);
   cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&m->slab), m->slab_bytes);
   if (e != cudaSuccess) {
@@ -423,7 +622,8 @@ int kvx_model_destroy(kvx_model* m) {
                   static_cast<void*>(m->q), static_cast<void*>(m->kv_new), static_cast<void*>(m->attn),
                   static_cast<void*>(m->gu), static_cast<void*>(m->act), static_cast<void*>(m->logits),
                   static_cast<void*>(m->attn_f32), static_cast<void*>(m->tokens), m->attn_ws,
-                  static_cast<void*>(m->slab), m->blas_ws})
+                  static_cast<void*>(m->slab), m->blas_ws, static_cast<void*>(m->skinny_part),
+                  static_cast<void*>(m->skinny_counters)})
     cudaFree(p);
   for (auto& g : m->step_graphs)
     if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
@@ -571,6 +771,16 @@ int enqueue_decode(kvx_model* m, kvx_pool* pool, const kvx_page_layout* layout, 
 }  // namespace kvx
 
 extern "C" {
+
+int kvx_model_linear(kvx_model* m, const void* d_x, const void* d_w, void* d_y, int32_t rows, int32_t in,
+                     int32_t out, int32_t accumulate, void* stream) {
+  if (!m || !d_x || !d_w || !d_y) return kvx::fail_arg("kvx_model_linear: null argument");
+  if (rows <= 0 || in <= 0 || out <= 0) return kvx::fail_arg("kvx_model_linear: empty shape");
+  kvx::DeviceGuard guard(m->device);
+  if (int rc = kvx::bind(m, stream)) return rc;
+  return kvx::linear(m, static_cast<const uint16_t*>(d_x), static_cast<const uint16_t*>(d_w),
+                     static_cast<uint16_t*>(d_y), rows, in, out, accumulate != 0);
+}
 
 int kvx_model_prefill(kvx_model* m, int32_t tokens, void* stream) {
   if (!m) return kvx::fail_arg("kvx_model_prefill: null model");
