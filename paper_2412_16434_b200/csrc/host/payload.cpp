@@ -468,6 +468,14 @@ bool NodePayload::decode_rows(const std::vector<std::pair<std::uint32_t, std::ui
                               std::uint32_t stride, std::uint32_t* out, std::vector<void*>& waits) {
   std::uint64_t fill = 0;  // newest fill among the rows (the FILL lane completes in order)
   const std::size_t first_wait = waits.size();
+  // A batch already complete on the GPU needs no wait (and an empty wait
+  // list lets the step replay as a CUDA graph): queried once per event.
+  void* last_checked = nullptr;
+  auto add_wait = [&](void* ev) {
+    if (std::find(waits.begin() + static_cast<std::ptrdiff_t>(first_wait), waits.end(), ev) != waits.end()) return;
+    if (kvx_event_query(ev) == KVX_OK) return;
+    waits.push_back(ev);
+  };
   for (std::size_t i = 0; i < reqs.size(); ++i) {
     const std::uint32_t n = reqs[i].second;
     if (n == 0) continue;
@@ -484,15 +492,15 @@ bool NodePayload::decode_rows(const std::vector<std::pair<std::uint32_t, std::ui
       if (!c.coming[0]) return false;
       const InFlight& f = flight(c.coming[0]);  // a load still landing: wait for exactly that move
       dst[b] = flight_page(f, b).page;
-      if (std::find(waits.begin() + static_cast<std::ptrdiff_t>(first_wait), waits.end(), f.event) == waits.end())
-        waits.push_back(f.event);
+      if (f.event != last_checked) {
+        last_checked = f.event;
+        add_wait(f.event);
+      }
     }
   }
   // No retiring here: the executor collects all layers' waits before issuing
   // them, so handles found for earlier layers must stay alive.
-  if (void* ev = fill ? lanes_[kLaneFill].find_pending(fill) : nullptr)
-    if (std::find(waits.begin() + static_cast<std::ptrdiff_t>(first_wait), waits.end(), ev) == waits.end())
-      waits.push_back(ev);
+  if (void* ev = fill ? lanes_[kLaneFill].find_pending(fill) : nullptr) add_wait(ev);
   return true;
 }
 
