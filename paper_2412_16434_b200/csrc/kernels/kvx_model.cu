@@ -66,6 +66,9 @@ struct kvx_model {
   uint32_t* skinny_counters = nullptr;
   uint64_t skinny_part_floats = 0;
   uint32_t skinny_tiles = 0;
+  // argmax_rows: per-row candidates of its CTAs and arrival counters
+  unsigned long long* argmax_cand = nullptr;
+  uint32_t* argmax_counters = nullptr;
   // Decode steps replayed as CUDA graphs, per launch shape (pointers and
   // sizes): the ~330 launches of a Llama-8B step cost more host time than
   // the GPU takes for the small-batch kernels.
@@ -103,6 +106,7 @@ __device__ __forceinline__ float bf(uint16_t v) { return __uint_as_float(static_
 
 // x[r] = E[token[r]]
 __global__ void embed_rows(const uint16_t* E, const int32_t* tok, uint16_t* x, int hidden, int vocab) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a PDL-launched K7 may prefetch its weights
   const int r = blockIdx.x;
   int t = tok[r] % vocab;
   if (t < 0) t += vocab;
@@ -111,15 +115,31 @@ __global__ void embed_rows(const uint16_t* E, const int32_t* tok, uint16_t* x, i
   for (int i = threadIdx.x; i < hidden / 8; i += blockDim.x) dst[i] = src[i];
 }
 
-// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w, one CTA per row.
-__global__ void __launch_bounds__(256) rms_norm(const uint16_t* x, const uint16_t* w, uint16_t* y, int hidden,
-                                                 float eps) {
-  const int r = blockIdx.x;
-  const uint16_t* xr = x + static_cast<uint64_t>(r) * hidden;
+// y[r] = x[r] * rsqrt(mean(x[r]^2) + eps) * w, one CTA per row. The row is
+// read once into registers (16-B vectors, all loads in flight together) and
+// reused for the scaling pass: one memory latency per launch, not one per
+// strided element.
+constexpr int kNormThreads = 256, kNormMaxVec = 8;  // hidden <= 8 x 8 x 256 = 16384
+__global__ void __launch_bounds__(kNormThreads) rms_norm(const uint16_t* x, const uint16_t* w, uint16_t* y, int hidden,
+                                                          float eps) {
+  const int r = blockIdx.x, nv = hidden / 8;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a PDL-launched K7 may prefetch its weights
+  const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<uint64_t>(r) * hidden);
+  uint4 v[kNormMaxVec];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
-    const float v = bf(xr[i]);
-    ss += v * v;
+#pragma unroll
+  for (int u = 0; u < kNormMaxVec; ++u) {
+    const int i = threadIdx.x + u * kNormThreads;
+    v[u] = i < nv ? xr[i] : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int u = 0; u < kNormMaxVec; ++u) {
+    const uint32_t q[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float lo = __uint_as_float(q[e] << 16), hi = __uint_as_float(q[e] & 0xFFFF0000u);
+      ss += lo * lo + hi * hi;
+    }
   }
   __shared__ float red[32];
   for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -132,8 +152,23 @@ __global__ void __launch_bounds__(256) rms_norm(const uint16_t* x, const uint16_
   }
   __syncthreads();
   const float inv = rsqrtf(red[0] / hidden + eps);
-  uint16_t* yr = y + static_cast<uint64_t>(r) * hidden;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) yr[i] = f32_to_bf16_rne(bf(xr[i]) * inv * bf(w[i]));
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* yr = reinterpret_cast<uint4*>(y + static_cast<uint64_t>(r) * hidden);
+#pragma unroll
+  for (int u = 0; u < kNormMaxVec; ++u) {
+    const int i = threadIdx.x + u * kNormThreads;
+    if (i >= nv) continue;
+    const uint4 wv = wr[i];
+    const uint32_t q[4] = {v[u].x, v[u].y, v[u].z, v[u].w}, qw[4] = {wv.x, wv.y, wv.z, wv.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float lo = __uint_as_float(q[e] << 16) * inv * __uint_as_float(qw[e] << 16);
+      const float hi = __uint_as_float(q[e] & 0xFFFF0000u) * inv * __uint_as_float(qw[e] & 0xFFFF0000u);
+      o[e] = static_cast<uint32_t>(f32_to_bf16_rne(lo)) | (static_cast<uint32_t>(f32_to_bf16_rne(hi)) << 16);
+    }
+    yr[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
 }
 
 // From one request's QKV row: q with RoPE at position ctx-1 (Llama rotate-half
@@ -143,6 +178,7 @@ __global__ void __launch_bounds__(256) rms_norm(const uint16_t* x, const uint16_
 __global__ void rope_and_token(const uint16_t* qkv, const int32_t* sessions, const int32_t* ctx_lens, int layer,
                                int hq, int hkv, int d, int block_tokens, float theta, uint64_t seed, int fill_mode,
                                uint16_t* q_out, uint16_t* k_out, uint16_t* v_out) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a PDL-launched K7 may prefetch its weights
   const int b = blockIdx.x;
   const int pos = max(ctx_lens[b] - 1, 0);
   const uint16_t* row = qkv + static_cast<uint64_t>(b) * (hq + 2 * hkv) * d;
@@ -174,6 +210,7 @@ __global__ void rope_and_token(const uint16_t* qkv, const int32_t* sessions, con
 }
 
 __global__ void f32_to_bf16_rows(const float* in, uint16_t* out, uint64_t n) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a PDL-launched K7 may prefetch its weights
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     out[i] = f32_to_bf16_rne(in[i]);
@@ -181,6 +218,7 @@ __global__ void f32_to_bf16_rows(const float* in, uint16_t* out, uint64_t n) {
 
 // act = silu(gate) * up over [rows][2 * inter] -> [rows][inter]
 __global__ void silu_mul(const uint16_t* gu, uint16_t* act, int inter, uint64_t rows) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // a PDL-launched K7 may prefetch its weights
   const uint64_t n = rows * inter;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -190,29 +228,66 @@ __global__ void silu_mul(const uint16_t* gu, uint16_t* act, int inter, uint64_t 
   }
 }
 
-// Greedy sampling: argmax over one row of logits per CTA.
-__global__ void __launch_bounds__(512) argmax_rows(const uint16_t* logits, int vocab, int32_t* out) {
-  const int r = blockIdx.x;
-  const uint16_t* row = logits + static_cast<uint64_t>(r) * vocab;
-  float best = -INFINITY;
-  int arg = 0;
-  for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-    const float v = bf(row[i]);
-    if (v > best) best = v, arg = i;
-  }
+// Greedy sampling: argmax over one row of logits, kArgmaxCtas CTAs per row.
+// Candidates are 64-bit keys (order-preserving float bits, then the
+// complemented index), so the max key is the max logit at its smallest index
+// — the first occurrence, as a serial scan would pick. The last CTA of a row
+// (arrival counter) reduces the row's candidates and resets the counter.
+constexpr int kArgmaxCtas = 32, kArgmaxThreads = 512;
+__device__ __forceinline__ unsigned long long argmax_key(float v, uint32_t idx) {
+  uint32_t b = __float_as_uint(v);
+  b ^= (b >> 31) ? 0xFFFFFFFFu : 0x80000000u;
+  return (static_cast<unsigned long long>(b) << 32) | (0xFFFFFFFFu - idx);
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long k) {
   for (int o = 16; o; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-    if (ov > best || (ov == best && oa < arg)) best = ov, arg = oa;
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, k, o);
+    k = other > k ? other : k;
   }
-  __shared__ float sv[16];
-  __shared__ int sa[16];
-  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = best, sa[threadIdx.x >> 5] = arg;
+  return k;
+}
+__global__ void __launch_bounds__(kArgmaxThreads) argmax_rows(const uint16_t* logits, int vocab,
+                                                             unsigned long long* cand, uint32_t* counters,
+                                                             int32_t* out) {
+  const int r = blockIdx.y, part = blockIdx.x;
+  const int chunk = ((vocab + kArgmaxCtas - 1) / kArgmaxCtas + 7) & ~7;
+  const int lo = part * chunk, hi = min(vocab, lo + chunk);
+  const uint16_t* row = logits + static_cast<uint64_t>(r) * vocab;
+  unsigned long long best = 0;
+  // vocab % 8 == 0 (checked at creation): whole 16-B vectors.
+  for (int i = lo + 8 * threadIdx.x; i < hi; i += 8 * kArgmaxThreads) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + i);
+    const uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const unsigned long long k0 = argmax_key(__uint_as_float(q[e] << 16), i + 2 * e);
+      const unsigned long long k1 = argmax_key(__uint_as_float(q[e] & 0xFFFF0000u), i + 2 * e + 1);
+      best = k0 > best ? k0 : best;
+      best = k1 > best ? k1 : best;
+    }
+  }
+  __shared__ unsigned long long sk[kArgmaxThreads / 32];
+  __shared__ bool last;
+  best = warp_max_u64(best);
+  if ((threadIdx.x & 31) == 0) sk[threadIdx.x >> 5] = best;
   __syncthreads();
+  if (threadIdx.x < 32) {
+    best = warp_max_u64(threadIdx.x < kArgmaxThreads / 32 ? sk[threadIdx.x] : 0ull);
+    if (threadIdx.x == 0) {
+      cand[static_cast<uint64_t>(r) * kArgmaxCtas + part] = best;
+      __threadfence();
+      last = atomicAdd(counters + r, 1u) == kArgmaxCtas - 1;
+    }
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  unsigned long long k = threadIdx.x < kArgmaxCtas ? __ldcg(cand + static_cast<uint64_t>(r) * kArgmaxCtas + threadIdx.x)
+                                                   : 0ull;
+  k = warp_max_u64(k);
   if (threadIdx.x == 0) {
-    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w)
-      if (sv[w] > best || (sv[w] == best && sa[w] < arg)) best = sv[w], arg = sa[w];
-    out[r] = arg;
+    out[r] = static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFu));
+    counters[r] = 0;
   }
 }
 
@@ -245,7 +320,7 @@ const char* blas_name(cublasStatus_t s) {
 // At decode batch sizes a projection streams its weight matrix once and does
 // ~rows multiply-adds per weight: HBM-bound. cuBLAS reaches ~half the copy
 // roofline on these skinny shapes (a Llama-3.1-8B step took 4.5 ms for
-// ~15 GB of weights), so rows <= 16 go to this kernel:
+// ~15 GB of weights), so rows <= 8 go to this kernel:
 //   * a warp owns 16 output features x a K chunk; per 128 k each lane loads
 //     4 x 16 B of each of its two weight rows (streaming, L1 no-allocate) and
 //     the matching 16 B of X (cached: every warp of the CTA reads the same X
@@ -256,7 +331,7 @@ const char* blas_name(cublasStatus_t s) {
 //   * split-K sized so ~2 waves of warps stream at once; the last warp of a
 //     tile (arrival counter) sums the partials in split order (deterministic)
 //     and writes bf16 Y, adding the residual when accumulating.
-constexpr int kSkinnyMaxRows = 16;
+constexpr int kSkinnyMaxRows = 8;  // measured: cuBLAS is faster from 16 rows (profiles/r02_model_step.txt)
 constexpr int kSkinnyWarps = 8;
 
 struct SkinnyArgs {
@@ -287,8 +362,25 @@ __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
 
 __device__ __forceinline__ float bf16_to_f32(uint16_t v) { return __uint_as_float(static_cast<uint32_t>(v) << 16); }
 
+__device__ __forceinline__ int4 ld_w(const uint16_t* p) {  // streamed once: no L1 allocation
+  int4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_x(const uint16_t* p) {  // X: shared by the CTA's warps, cached
+  int4 r;
+  asm("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void mma_acc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 template <int NT>  // n-tiles of 8 batch rows: 1 (rows <= 8) or 2 (rows <= 16)
-__global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_linear(const SkinnyArgs a) {
+__global__ void __launch_bounds__(kSkinnyWarps * 32, 2) skinny_linear(const SkinnyArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kSkinnyWarps + warp;
   if (tile * 16 >= a.out) return;  // no block-wide barriers below
@@ -308,27 +400,46 @@ __global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_linear(const SkinnyA
   float d[NT][4];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
-  for (int k = k0; k < k1; k += 128) {  // in and k_chunk are multiples of 128
-    int4 wa[4], wb[4], xs[NT][4];
+  // Two 128-k groups of weights in flight per lane (software pipelined: the
+  // next group's loads are issued before this group's mmas).
+  int4 wa[4], wb[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      wa[j] = ld_stream(reinterpret_cast<const int4*>(w0 + k + 32 * j));
-      wb[j] = ld_stream(reinterpret_cast<const int4*>(w8 + k + 32 * j));
-    }
+  for (int j = 0; j < 4; ++j) {
+    wa[j] = ld_w(w0 + k0 + 32 * j);
+    wb[j] = ld_w(w8 + k0 + 32 * j);
+  }
+  // Programmatic dependent launch: the weights do not depend on the kernel
+  // before us, so the first group is in flight before we wait for it (X, the
+  // residual Y and the split-K workspace are touched only after the wait).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int k = k0; k < k1; k += 128) {  // in and k_chunk are multiples of 128
+    int4 xs[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        xs[nt][j] = xv[nt] ? ld_nc_v4(xr[nt] + k + 32 * j) : make_int4(0, 0, 0, 0);
+      for (int j = 0; j < 4; ++j) xs[nt][j] = xv[nt] ? ld_x(xr[nt] + k + 32 * j) : make_int4(0, 0, 0, 0);
+    int4 na[4], nb[4];
+    const bool more = k + 128 < k1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      na[j] = more ? ld_w(w0 + k + 128 + 32 * j) : make_int4(0, 0, 0, 0);
+      nb[j] = more ? ld_w(w8 + k + 128 + 32 * j) : make_int4(0, 0, 0, 0);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         // virtual k {2c,2c+1 | 2c+8,2c+9} <- physical 8c+{0,1 | 2,3}, then 8c+{4,5 | 6,7}
-        mma_bf16_16816(d[nt], wa[j].x, wb[j].x, wa[j].y, wb[j].y, xs[nt][j].x, xs[nt][j].y);
-        mma_bf16_16816(d[nt], wa[j].z, wb[j].z, wa[j].w, wb[j].w, xs[nt][j].z, xs[nt][j].w);
+        mma_acc(d[nt], wa[j].x, wb[j].x, wa[j].y, wb[j].y, xs[nt][j].x, xs[nt][j].y);
+        mma_acc(d[nt], wa[j].z, wb[j].z, wa[j].w, wb[j].w, xs[nt][j].z, xs[nt][j].w);
       }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      wa[j] = na[j];
+      wb[j] = nb[j];
+    }
   }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // our weight stream is done
   if (a.splits > 1) {
     float4* mine = reinterpret_cast<float4*>(a.part + (static_cast<uint64_t>(tile) * a.splits + split) * (NT * 128));
 #pragma unroll
@@ -342,15 +453,25 @@ __global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_linear(const SkinnyA
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
     const float4* all = reinterpret_cast<const float4*>(a.part + static_cast<uint64_t>(tile) * a.splits * (NT * 128));
-    for (int s2 = 0; s2 < a.splits; ++s2)
+    // Eight partials in flight per lane, summed in split order (deterministic).
+    for (int s0 = 0; s0 < a.splits; s0 += 8) {
+      float4 v[8][NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const float4 v = __ldcg(all + (static_cast<uint64_t>(s2) * NT + nt) * 32 + lane);
-        d[nt][0] += v.x;
-        d[nt][1] += v.y;
-        d[nt][2] += v.z;
-        d[nt][3] += v.w;
-      }
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          v[u][nt] = s0 + u < a.splits ? __ldcg(all + (static_cast<uint64_t>(s0 + u) * NT + nt) * 32 + lane)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          d[nt][0] += v[u][nt].x;
+          d[nt][1] += v[u][nt].y;
+          d[nt][2] += v[u][nt].z;
+          d[nt][3] += v[u][nt].w;
+        }
+    }
     if (lane == 0) a.counters[tile] = 0;  // ready for the next launch
   }
   // d[nt][0/1]: feature g, batch rows 8nt + 2c + {0,1}; d[nt][2/3]: feature g + 8.
@@ -366,12 +487,14 @@ __global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_linear(const SkinnyA
     }
 }
 
-// Split-K factor of a skinny projection: ~2 resident waves of warps.
+// Split-K factor of a skinny projection: one wave of CTAs (two 8-warp CTAs
+// per SM at 128 registers), so no partial second wave trails the launch.
 void skinny_plan(int in, int out, int sms, int& splits, int& k_chunk) {
   const int tiles = out / 16;
   const int groups = in / 128;
-  const long target = 2L * sms * 16;  // 16 resident warps per SM (2 CTAs of 8)
-  int s = static_cast<int>(std::max(1L, (target + tiles - 1) / tiles));
+  const int ctas_per_split = (tiles + kSkinnyWarps - 1) / kSkinnyWarps;
+  const int wave = 2 * sms;
+  int s = std::max(1, wave / std::max(1, ctas_per_split));
   s = std::min(s, groups);
   k_chunk = ((groups + s - 1) / s) * 128;
   splits = (in + k_chunk - 1) / k_chunk;
@@ -392,12 +515,17 @@ int skinny_linear_launch(kvx_model* m, const uint16_t* X, const uint16_t* W, uin
   if (a.splits > 1 && (tiles > m->skinny_tiles ||
                        static_cast<uint64_t>(tiles) * a.splits * nt * 128 > m->skinny_part_floats))
     return fail_arg("kvx_model: skinny projection workspace too small");
-  dim3 grid((tiles + kSkinnyWarps - 1) / kSkinnyWarps, a.splits);
-  if (nt == 1)
-    skinny_linear<1><<<grid, kSkinnyWarps * 32, 0, st>>>(a);
-  else
-    skinny_linear<2><<<grid, kSkinnyWarps * 32, 0, st>>>(a);
-  KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: skinny_linear");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((tiles + kSkinnyWarps - 1) / kSkinnyWarps, a.splits);
+  cfg.blockDim = dim3(kSkinnyWarps * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // weights prefetched under the previous kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KVX_CUDA_TRY(nt == 1 ? cudaLaunchKernelEx(&cfg, skinny_linear<1>, a) : cudaLaunchKernelEx(&cfg, skinny_linear<2>, a),
+               "kvx_model: skinny_linear");
   note_launch();
   return KVX_OK;
 }
@@ -498,7 +626,8 @@ int sample(kvx_model* m, int first, int rows, int32_t* d_tokens_out) {
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: final norm");
   note_launch();
   if (int rc = linear(m, m->h, m->lm_head, m->logits, rows, c.hidden, c.vocab, false)) return rc;
-  argmax_rows<<<rows, 512, 0, st>>>(m->logits, c.vocab, d_tokens_out);
+  argmax_rows<<<dim3(kArgmaxCtas, rows), kArgmaxThreads, 0, st>>>(m->logits, c.vocab, m->argmax_cand,
+                                                                  m->argmax_counters, d_tokens_out);
   KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: argmax");
   note_launch();
   return KVX_OK;
@@ -521,8 +650,10 @@ int kvx_model_create(int device, const kvx_model_config* cfg, uint64_t seed, kvx
   if (!cfg || !out) return kvx::fail_arg("kvx_model_create: null argument");
   const kvx_model_config& c = *cfg;
   if (c.num_layers <= 0 || c.hidden <= 0 || c.hidden % 8 || c.num_kv_heads <= 0 || c.num_q_heads % c.num_kv_heads ||
-      c.head_dim != 128 || c.intermediate <= 0 || c.vocab <= 0 || c.num_q_heads * c.head_dim % 8)
-    return kvx::fail_arg("kvx_model_create: unsupported shape (head_dim 128, hidden % 8 == 0, GQA)");
+      c.head_dim != 128 || c.intermediate <= 0 || c.vocab <= 0 || c.vocab % 8 || c.num_q_heads * c.head_dim % 8 ||
+      c.hidden > 16384)
+    return kvx::fail_arg("kvx_model_create: unsupported shape (head_dim 128, hidden % 8 == 0 and <= 16384, vocab % 8 "
+                         "== 0, GQA)");
   kvx::DeviceGuard guard(device);
   auto* m = new kvx_model;
   m->cfg = c;
@@ -561,7 +692,10 @@ int kvx_model_create(int device, const kvx_model_config* cfg, uint64_t seed, kvx
             cudaSuccess ||
         cudaMalloc(reinterpret_cast<void**>(&m->skinny_counters), std::max<uint32_t>(m->skinny_tiles, 1) * 4) !=
             cudaSuccess ||
-        cudaMemset(m->skinny_counters, 0, std::max<uint32_t>(m->skinny_tiles, 1) * 4) != cudaSuccess) {
+        cudaMemset(m->skinny_counters, 0, std::max<uint32_t>(m->skinny_tiles, 1) * 4) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&m->argmax_cand), 256 * kvx::kArgmaxCtas * 8) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&m->argmax_counters), 256 * 4) != cudaSuccess ||
+        cudaMemset(m->argmax_counters, 0, 256 * 4) != cudaSuccess) {
       cudaGetLastError();
       cudaFree(m->skinny_part);
       cudaFree(m->skinny_counters);
@@ -623,7 +757,8 @@ int kvx_model_destroy(kvx_model* m) {
                   static_cast<void*>(m->gu), static_cast<void*>(m->act), static_cast<void*>(m->logits),
                   static_cast<void*>(m->attn_f32), static_cast<void*>(m->tokens), m->attn_ws,
                   static_cast<void*>(m->slab), m->blas_ws, static_cast<void*>(m->skinny_part),
-                  static_cast<void*>(m->skinny_counters)})
+                  static_cast<void*>(m->skinny_counters), static_cast<void*>(m->argmax_cand),
+                  static_cast<void*>(m->argmax_counters)})
     cudaFree(p);
   for (auto& g : m->step_graphs)
     if (g.second.exec) cudaGraphExecDestroy(g.second.exec);
@@ -750,7 +885,7 @@ int enqueue_decode(kvx_model* m, kvx_pool* pool, const kvx_page_layout* layout, 
     if (layer_waits && layer_wait_offsets)
       for (int i = layer_wait_offsets[l]; i < layer_wait_offsets[l + 1]; ++i)
         KVX_CUDA_TRY(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(layer_waits[i]), 0), "kvx_model: layer wait");
-    kvx::rope_and_token<<<batch, 256, 0, st>>>(m->qkv, d_sessions, d_ctx_lens, l, Hq, H, D, layout->block_tokens,
+    kvx::rope_and_token<<<batch, 1024, 0, st>>>(m->qkv, d_sessions, d_ctx_lens, l, Hq, H, D, layout->block_tokens,
                                                c.rope_theta, fill_seed, fill_mode, m->q, new_k, new_v);
     KVX_CUDA_TRY(cudaGetLastError(), "kvx_model: rope");
     kvx::note_launch();

@@ -3,7 +3,7 @@ plain PyTorch fp32 reference of the same op (Y (+)= X . W^T, bf16 in/out).
 
 The serving engine's quanta (kvx_model_decode_step) run every projection of
 a Llama-3.1-8B-shaped layer through kvx_model_linear's path: K7 for batch
-rows <= 16, cuBLAS above. Checked here on every projection shape of the
+rows <= 8, cuBLAS above. Checked here on every projection shape of the
 model (QKV, O, gate/up, down, LM head) at rows 1..16 and past the K7 limit,
 with and without the residual accumulate, within bf16 output rounding."""
 import ctypes as C
@@ -58,12 +58,13 @@ def test_projection_matches_fp32_reference(model, rows, accumulate):
                                   C.c_void_p(st.cuda_stream))
         assert rc == 0, lib.kvx_last_error()
         torch.cuda.synchronize()
-        ref = x.float() @ w.float().t()
-        if accumulate:
-            ref = ref + y0.float()
+        xw = x.float() @ w.float().t()
+        ref = xw + y0.float() if accumulate else xw
         err = (y.float() - ref).abs()
-        # bf16 output rounding (2^-8 relative) + fp32 summation-order noise
-        tol = 2 ** -8 * ref.abs() + 1e-3 * ref.abs().max()
+        # bf16 output rounding (2^-8 relative) + fp32 summation-order noise;
+        # accumulating, cuBLAS (rows > 16) may round X.W^T to bf16 before
+        # adding Y: a second rounding of |X.W^T|.
+        tol = 2 ** -8 * (ref.abs() + (xw.abs() if accumulate else 0)) + 1e-3 * ref.abs().max()
         assert bool((err <= tol).all()), (k, n, rows, accumulate, float(err.max()), float((err - tol).max()))
 
 
