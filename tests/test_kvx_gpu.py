@@ -122,6 +122,36 @@ def test_copy_pages_between_pools_bit_exact(dev, mode):
     assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
 
 
+@pytest.mark.parametrize("pattern", ["fragmented", "runs"])
+def test_copy_engine_lane_host_pools_bit_exact(dev, pattern):
+    """KVX_COPY_CE with host id lists between HBM and a pinned mapped HOST pool
+    (the payload's PCIe lanes), both directions: fragmented ids take the
+    listed-id SM mover (ids in the launch parameters; 5,000 pages = two
+    launches of <= 3,840), long runs one cudaMemcpyAsync per run."""
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(17)
+    n, pages = 5000, 5200
+    if pattern == "fragmented":
+        src_ids = rng.permutation(pages)[:n].astype(np.uint32)
+        host_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    else:
+        src_ids = np.arange(100, 100 + n, dtype=np.uint32)
+        host_ids = np.arange(7, 7 + n, dtype=np.uint32)
+    tags = O.tags_array(4, 2, np.arange(n))
+    src, ref = filled_pool(layout, pages, src_ids, tags, 21, kvx.FILL_VALUES, dev)
+    host = kvx.Pool(pages, pb, host=True)
+    back = kvx.Pool(pages, pb, device=0)
+    back.as_tensor().zero_()
+    torch.cuda.synchronize()  # the fill ran on the legacy stream
+    s = torch.cuda.Stream()
+    kvx.copy_pages(src, src_ids, host, host_ids, n, kvx.COPY_CE, stream=s)   # D2H
+    kvx.copy_pages(host, host_ids, back, src_ids, n, kvx.COPY_CE, stream=s)  # H2D
+    s.synchronize()
+    got = back.as_tensor().cpu().numpy()
+    assert np.array_equal(got[src_ids], ref[src_ids])
+
+
 @pytest.mark.parametrize("mode", [kvx.COPY_SM, kvx.COPY_TMA])
 @pytest.mark.parametrize("cap", [1, 3, 17])
 def test_capped_copy_bit_exact(dev, mode, cap):
