@@ -211,6 +211,16 @@ int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, 
  * Ignored for KVX_COPY_CE. */
 int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
                           uint64_t n, int mode, uint32_t max_ctas, void* stream);
+/* K3 with HOST id arrays (src_ids / dst_ids in host memory, range-checked
+ * here): the ids travel in the launch parameters (3,840 pages per launch), so
+ * a move costs no id upload — the payload's per-layer path (NodePayload).
+ * mode: KVX_COPY_AUTO (TMA bulk mover for HBM<->HBM on one device, else the
+ * SM vector mover), KVX_COPY_SM or KVX_COPY_TMA; max_ctas > 0 caps the grid.
+ * At least one endpoint must be a device pool; not for file pools. Replaces
+ * the same reference transfers as kvx_copy_pages. */
+int kvx_copy_pages_listed(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
+                          uint64_t n, int mode, uint32_t max_ctas, void* stream);
+
 
 /* K3 over NCCL (the collective-library migration variant):
  * per chunk of pages_per_chunk pages — one migration layer — K1 packs the

@@ -121,13 +121,39 @@ __global__ void __launch_bounds__(kVecThreads) page_move_vec(MoveArgs a) {
   }
 }
 
+// Host-listed moves: the id pairs travel in the kernel's parameter block
+// (no upload, no device id array): used where the ids come from the host
+// per move (the payload's lanes), so a move costs one launch call.
+constexpr int kListedPairs = 3840;  // 30 KiB of ids + header < the 32,764-B parameter limit
+struct ListedBulkArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t n_pages;
+  uint64_t page_bytes;
+  uint32_t chunk_bytes;
+  uint32_t chunks_per_page;
+  int stages;
+  uint32_t src_ids[kListedPairs];
+  uint32_t dst_ids[kListedPairs];
+};
+__device__ __forceinline__ void item_addr(const ListedBulkArgs& a, uint64_t item, const uint8_t*& s, uint8_t*& d,
+                                          uint32_t& bytes) {
+  const uint64_t page = item / a.chunks_per_page;
+  const uint32_t c = static_cast<uint32_t>(item - page * a.chunks_per_page);
+  const uint64_t off = static_cast<uint64_t>(c) * a.chunk_bytes;
+  s = a.src + static_cast<uint64_t>(a.src_ids[page]) * a.page_bytes + off;  // ids range-checked on the host
+  d = a.dst + static_cast<uint64_t>(a.dst_ids[page]) * a.page_bytes + off;
+  const uint64_t left = a.page_bytes - off;
+  bytes = static_cast<uint32_t>(left < a.chunk_bytes ? left : a.chunk_bytes);
+}
+
 // TMA bulk variant: lane 0 of a single warp per SM streams chunks through a
 // a.stages-deep shared-memory ring. Load k+S-1 is issued as soon as the
 // bulk store of chunk k-1 has finished READING its stage.
-__global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
+template <typename Args>
+__device__ __forceinline__ void bulk_body(const Args& a) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kBulkMaxStages];
-  pdl_enter();
   const int S = a.stages;
   const uint32_t slot = a.chunk_bytes;
   if (threadIdx.x != 0) return;
@@ -163,6 +189,15 @@ __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
     }
   }
   bulk_wait<0>();
+}
+
+__global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
+  pdl_enter();
+  bulk_body(a);
+}
+
+__global__ void __launch_bounds__(32, 1) page_move_bulk_listed(const __grid_constant__ ListedBulkArgs a) {
+  bulk_body(a);
 }
 
 // Launch with programmatic stream serialization (PDL).
@@ -245,7 +280,6 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
 // launch overhead, a 64 KiB page only ~1.2 us of PCIe time. Measured on B200
 // (profiles/r01_pcie_movers.json.txt): SM zero-copy moves 51-53 GB/s per
 // direction, fragmented or not, against 55-57 for copy engines on long runs.
-constexpr int kListedPairs = 3840;  // 30 KiB of ids + header < the 32,764-B parameter limit
 struct ListedMove {
   const uint8_t* src;
   uint8_t* dst;
@@ -382,6 +416,81 @@ __global__ void __launch_bounds__(128) append_kv_kernel(uint8_t* base, uint64_t 
 
 using kvx::MoveArgs;
 
+namespace kvx {
+namespace {
+// Host-listed move (ids already range-checked by the caller): chunks of
+// kListedPairs pages, ids copied into each launch's parameter block. TMA
+// bulk mover for HBM<->HBM on one device, the LDG/STG.128 mover otherwise
+// (peer, mapped host) or when asked (mode KVX_COPY_SM); `max_ctas` bounds
+// the grid (0: the mover's default).
+int launch_listed(const kvx_pool* src, const uint32_t* src_ids, const kvx_pool* dst, const uint32_t* dst_ids,
+                  uint64_t n, int mode, uint32_t max_ctas, cudaStream_t st, const char* who) {
+  const int dev = src->device >= 0 ? src->device : dst->device;
+  DeviceGuard guard(dev);
+  if (src->page_bytes % 16 || reinterpret_cast<uintptr_t>(src->base) % 16 || reinterpret_cast<uintptr_t>(dst->base) % 16)
+    return fail_arg("page movers need 16-byte aligned pages");
+  const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
+  const int sms = sm_count(dev);
+  if (mode == KVX_COPY_AUTO) mode = local ? KVX_COPY_TMA : KVX_COPY_SM;
+  if (mode == KVX_COPY_TMA) {
+    static thread_local ListedBulkArgs b;
+    const BulkGeometry geo = bulk_geometry(true, true);
+    b.src = src->base;
+    b.dst = dst->base;
+    b.page_bytes = src->page_bytes;
+    b.chunk_bytes = static_cast<uint32_t>(std::min<uint64_t>(src->page_bytes, geo.chunk));
+    b.chunks_per_page = static_cast<uint32_t>((src->page_bytes + b.chunk_bytes - 1) / b.chunk_bytes);
+    b.stages = geo.stages;
+    const uint32_t smem = static_cast<uint32_t>(geo.stages) * b.chunk_bytes;
+    static std::atomic<uint32_t> configured[64] = {};
+    std::atomic<uint32_t>& have = configured[(dev < 0 ? 0 : dev) % 64];
+    if (have.load(std::memory_order_acquire) < smem) {
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lock(mu);
+      if (have.load(std::memory_order_relaxed) < smem) {
+        KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk_listed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+                     who);
+        have.store(smem, std::memory_order_release);
+      }
+    }
+    for (uint64_t at = 0; at < n; at += kListedPairs) {
+      b.n_pages = std::min<uint64_t>(kListedPairs, n - at);
+      std::memcpy(b.src_ids, src_ids + at, b.n_pages * sizeof(uint32_t));
+      std::memcpy(b.dst_ids, dst_ids + at, b.n_pages * sizeof(uint32_t));
+      const uint64_t items = b.n_pages * b.chunks_per_page;
+      unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * geo.ctas_per_sm));
+      if (max_ctas && grid > max_ctas) grid = max_ctas;
+      page_move_bulk_listed<<<grid, 32, smem, st>>>(b);
+      note_launch();
+      KVX_CUDA_TRY(cudaGetLastError(), who);
+    }
+    return KVX_OK;
+  }
+  if (mode != KVX_COPY_SM) {
+    set_error(std::string(who) + ": unsupported copy mode");
+    return KVX_ERR_UNSUPPORTED;
+  }
+  static thread_local ListedMove m;
+  m.src = src->base;
+  m.dst = dst->base;
+  m.page_bytes = src->page_bytes;
+  m.chunks_per_page = static_cast<uint32_t>((src->page_bytes + kVecChunk - 1) / kVecChunk);
+  for (uint64_t at = 0; at < n; at += kListedPairs) {
+    m.n = static_cast<uint32_t>(std::min<uint64_t>(kListedPairs, n - at));
+    std::memcpy(m.src_ids, src_ids + at, m.n * sizeof(uint32_t));
+    std::memcpy(m.dst_ids, dst_ids + at, m.n * sizeof(uint32_t));
+    const uint64_t items = static_cast<uint64_t>(m.n) * m.chunks_per_page;
+    unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * 8));
+    if (max_ctas && grid > max_ctas) grid = max_ctas;
+    page_move_listed<<<grid, kVecThreads, 0, st>>>(m);
+    note_launch();
+    KVX_CUDA_TRY(cudaGetLastError(), who);
+  }
+  return KVX_OK;
+}
+}  // namespace
+}  // namespace kvx
+
 extern "C" {
 
 int kvx_pack(const kvx_pool* src, const uint32_t* d_page_ids, uint64_t n, void* d_dst, int mode, void* stream) {
@@ -460,28 +569,11 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
   // Every pool is device-addressable here: HBM, IPC-opened peer HBM, or
   // pinned host memory allocated mapped (UVA: host pointer == device pointer).
   if (run_bytes < min_run && src->page_bytes % 16 == 0 && (src->device >= 0 || dst->device >= 0)) {
-    const int dev = src->device >= 0 ? src->device : dst->device;
-    kvx::DeviceGuard guard(dev);
-    static thread_local kvx::ListedMove m;
-    m.src = src->base;
-    m.dst = dst->base;
-    m.page_bytes = src->page_bytes;
-    m.chunks_per_page = static_cast<uint32_t>((src->page_bytes + kvx::kVecChunk - 1) / kvx::kVecChunk);
     static const unsigned ctas = [] {
       const char* e = std::getenv("KVX_LISTED_CTAS");
       return e ? static_cast<unsigned>(std::atoi(e)) : 64u;
     }();
-    for (uint64_t at = 0; at < n; at += kvx::kListedPairs) {
-      m.n = static_cast<uint32_t>(std::min<uint64_t>(kvx::kListedPairs, n - at));
-      std::memcpy(m.src_ids, src_ids + at, m.n * sizeof(uint32_t));
-      std::memcpy(m.dst_ids, dst_ids + at, m.n * sizeof(uint32_t));
-      const uint64_t items = static_cast<uint64_t>(m.n) * m.chunks_per_page;
-      const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, std::max(1u, ctas)));
-      kvx::page_move_listed<<<grid, kvx::kVecThreads, 0, st>>>(m);
-      kvx::note_launch();
-      KVX_CUDA_TRY(cudaGetLastError(), "kvx_copy_pages(listed)");
-    }
-    return KVX_OK;
+    return kvx::launch_listed(src, src_ids, dst, dst_ids, n, KVX_COPY_SM, ctas, st, "kvx_copy_pages(listed)");
   }
   for (uint64_t i = 0; i < n;) {
     uint64_t j = i + 1;
@@ -493,6 +585,22 @@ int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool
     i = j;
   }
   return KVX_OK;
+}
+
+int kvx_copy_pages_listed(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
+                          uint64_t n, int mode, uint32_t max_ctas, void* stream) {
+  if (!src || !dst || (n && (!src_ids || !dst_ids))) return kvx::fail_arg("kvx_copy_pages_listed: null argument");
+  if (src->page_bytes != dst->page_bytes) return kvx::fail_arg("kvx_copy_pages_listed: page size mismatch");
+  if (src->fd >= 0 || dst->fd >= 0) return kvx::fail_arg("kvx_copy_pages_listed: not on a file pool");
+  if (src->device < 0 && dst->device < 0) return kvx::fail_arg("kvx_copy_pages_listed: needs a device endpoint");
+  if (mode != KVX_COPY_AUTO && mode != KVX_COPY_SM && mode != KVX_COPY_TMA)
+    return kvx::fail_arg("kvx_copy_pages_listed: mode must be AUTO, SM or TMA");
+  for (uint64_t i = 0; i < n; ++i)
+    if (src_ids[i] >= src->num_pages || dst_ids[i] >= dst->num_pages)
+      return kvx::fail_arg("kvx_copy_pages_listed: page id out of range");
+  if (n == 0) return KVX_OK;
+  return kvx::launch_listed(src, src_ids, dst, dst_ids, n, mode, max_ctas, kvx::as_stream(stream),
+                            "kvx_copy_pages_listed");
 }
 
 int kvx_verify_pages(const kvx_pool* pool, const uint32_t* d_page_ids, const kvx_block_tag* d_tags, uint64_t n,

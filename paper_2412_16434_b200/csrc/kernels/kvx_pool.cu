@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include <unordered_map>
 #include "kvx_common.cuh"
 
 namespace kvx {
@@ -398,10 +399,38 @@ int kvx_read_page(const kvx_pool* pool, uint64_t page, void* host_out) {
 
 extern "C" {
 
+// Ordering events are recycled: the payload records two per moved layer
+// (batch + transfer), and cudaEventCreate/Destroy cost microseconds each on
+// the host path a migration runs on. A destroyed event goes back to its
+// device's free list; re-recording it later is safe (a stream wait binds the
+// record current when the wait is enqueued). Timing events are not pooled.
+namespace kvx {
+namespace {
+std::mutex g_event_mu;
+std::unordered_map<cudaEvent_t, int> g_event_device;  // pooled-kind events alive or free -> device
+std::vector<cudaEvent_t> g_event_free[64];
+}  // namespace
+}  // namespace kvx
+
 int kvx_event_create(void** out) {
   if (!out) return kvx::fail_arg("kvx_event_create: null out");
+  int dev = 0;
+  KVX_CUDA_TRY(cudaGetDevice(&dev), "kvx_event_create");
+  {
+    std::lock_guard<std::mutex> lock(kvx::g_event_mu);
+    auto& fl = kvx::g_event_free[dev % 64];
+    if (!fl.empty()) {
+      *out = fl.back();
+      fl.pop_back();
+      return KVX_OK;
+    }
+  }
   cudaEvent_t e = nullptr;
   KVX_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "kvx_event_create");
+  {
+    std::lock_guard<std::mutex> lock(kvx::g_event_mu);
+    kvx::g_event_device[e] = dev;
+  }
   *out = e;
   return KVX_OK;
 }
@@ -422,7 +451,17 @@ int kvx_timer_elapsed_ms(void* start, void* stop, float* ms) {
 }
 
 int kvx_event_destroy(void* event) {
-  if (event) KVX_CUDA_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(event)), "kvx_event_destroy");
+  if (!event) return KVX_OK;
+  const auto e = static_cast<cudaEvent_t>(event);
+  {
+    std::lock_guard<std::mutex> lock(kvx::g_event_mu);
+    const auto it = kvx::g_event_device.find(e);
+    if (it != kvx::g_event_device.end()) {  // an ordering event: back to its device's free list
+      kvx::g_event_free[it->second % 64].push_back(e);
+      return KVX_OK;
+    }
+  }
+  KVX_CUDA_TRY(cudaEventDestroy(e), "kvx_event_destroy");
   return KVX_OK;
 }
 

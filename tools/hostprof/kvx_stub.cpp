@@ -77,3 +77,7 @@ int kvx_fill_pages(kvx_pool*, const uint32_t*, const kvx_block_tag*, uint64_t, u
   return KVX_OK;
 }
 }
+extern "C" int kvx_copy_pages_listed(const kvx_pool*, const uint32_t*, kvx_pool*, const uint32_t*, uint64_t, int,
+                                     uint32_t, void*) {
+  return KVX_OK;
+}
