@@ -108,6 +108,9 @@ def test_abi_rejects_bad_arguments_without_touching_a_device(product_libs):
     out = V()
     assert lib.kvx_pool_create_host(4, 1000, ctypes.byref(out)) == KVX_ERR_ARG  # not a multiple of 16
     assert lib.kvx_signal_write(V(2), 1, None) == KVX_ERR_ARG  # misaligned flag
+    lib.kvx_copy_pages_listed.argtypes = [V, V, V, V, U64, ctypes.c_int, ctypes.c_uint32, V]
+    assert lib.kvx_copy_pages_listed(None, None, None, None, 4, 0, 0, None) == KVX_ERR_ARG
+    assert b"null" in lib.kvx_last_error()
 
 
 def test_migrate_nccl_validates_arguments_before_touching_a_device(product_libs):

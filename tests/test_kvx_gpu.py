@@ -122,6 +122,39 @@ def test_copy_pages_between_pools_bit_exact(dev, mode):
     assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
 
 
+@pytest.mark.parametrize("mode", [kvx.COPY_AUTO, kvx.COPY_SM, kvx.COPY_TMA])
+def test_copy_pages_listed_bit_exact(dev, mode):
+    """kvx_copy_pages_listed (the payload's per-layer HBM moves): host id
+    lists in the launch parameters, 5,000 scattered pages = two launches of
+    <= 3,840, every mover; out-of-range ids rejected before any launch."""
+    layout = LLAMA8B
+    pb = layout.page_bytes()
+    rng = np.random.default_rng(23 + mode)
+    n, pages = 5000, 5300
+    src_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    dst_ids = rng.permutation(pages)[:n].astype(np.uint32)
+    tags = O.tags_array(6, 1, np.arange(n))
+    src, ref = filled_pool(layout, pages, src_ids, tags, 31, kvx.FILL_VALUES, dev)
+    dst = kvx.Pool(pages, pb, device=0)
+    dst.as_tensor().zero_()
+    torch.cuda.synchronize()
+    lib = kvx.lib()
+    V, U64 = ctypes.c_void_p, ctypes.c_uint64
+    lib.kvx_copy_pages_listed.argtypes = [V, V, V, V, U64, ctypes.c_int, ctypes.c_uint32, V]
+    s = torch.cuda.Stream()
+    rc = lib.kvx_copy_pages_listed(src.handle, src_ids.ctypes.data, dst.handle, dst_ids.ctypes.data, n, mode, 0,
+                                   ctypes.c_void_p(s.cuda_stream))
+    assert rc == 0, lib.kvx_last_error()
+    s.synchronize()
+    ref_dst = np.zeros((pages, pb), np.uint8)
+    O.copy_pages(ref, src_ids, ref_dst, dst_ids, pb)
+    assert np.array_equal(dst.as_tensor().cpu().numpy(), ref_dst)
+    bad = dst_ids.copy()
+    bad[-1] = pages  # out of range
+    assert lib.kvx_copy_pages_listed(src.handle, src_ids.ctypes.data, dst.handle, bad.ctypes.data, n, mode, 0,
+                                     ctypes.c_void_p(s.cuda_stream)) == 2
+
+
 @pytest.mark.parametrize("pattern", ["fragmented", "runs"])
 def test_copy_engine_lane_host_pools_bit_exact(dev, pattern):
     """KVX_COPY_CE with host id lists between HBM and a pinned mapped HOST pool
