@@ -749,8 +749,7 @@ def bench_store_migration(args, torch, np, kvx, dev):
     nodes share this GPU (on a multi-GPU box the push crosses NVLink). Inside
     the host-timed region per step: the store bookkeeping of both nodes, the
     block-table uploads from host memory (the page-id lists of every layer,
-    H2D in the movers' launch parameters, kvx_copy_pages_listed), the GPU
-    moves, and a probe page read back to host memory (D2H);
+    H2D), the GPU moves, and a probe page read back to host memory (D2H);
     the probe is verified against the block's content."""
     from paper_2412_16434_b200 import kvstore as K
     cfg = CFG_8B
@@ -808,7 +807,7 @@ def bench_store_migration(args, torch, np, kvx, dev):
         dst.release_session(i, now + 3)  # untimed: frees the landing pages for the next step
         now += 10_000_000_000
     t = statistics.mean(times)
-    ids_bytes = 2 * n * 4  # source + destination page ids of every layer (launch parameters), per step
+    ids_bytes = 2 * n * 4  # source + destination page ids of every layer, uploaded per step
     host = nodes[1].host_ns()
     return {"value": n * pb / t / GB, "unit": UNIT, "h2d_bytes_per_step": ids_bytes, "d2h_bytes_per_step": pb,
             "ms_per_step": 1e3 * t, "steps": len(times), "verified_probe_pages": verified,

@@ -212,8 +212,11 @@ int kvx_copy_pages(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, 
 int kvx_copy_pages_capped(const kvx_pool* src, const uint32_t* src_ids, kvx_pool* dst, const uint32_t* dst_ids,
                           uint64_t n, int mode, uint32_t max_ctas, void* stream);
 /* K3 with HOST id arrays (src_ids / dst_ids in host memory, range-checked
- * here): the ids travel in the launch parameters (3,840 pages per launch), so
- * a move costs no id upload — the payload's per-layer path (NodePayload).
+ * here): the ids travel in the launch parameters (up to 3,840 pages per
+ * launch), so a move needs no device id array or upload — the CE lane's mover
+ * for fragmented PCIe moves. (A launch copies its parameter block: per-layer
+ * HBM moves in NodePayload keep the staged upload + kvx_copy_pages_capped,
+ * measured cheaper on the host.)
  * mode: KVX_COPY_AUTO (TMA bulk mover for HBM<->HBM on one device, else the
  * SM vector mover), KVX_COPY_SM or KVX_COPY_TMA; max_ctas > 0 caps the grid.
  * At least one endpoint must be a device pool; not for file pools. Replaces

@@ -329,7 +329,6 @@ class NodePayload final : public TierBackend {
   std::vector<Ref> scratch_src_, scratch_dst_;  // transfer_posted scratch (reused)
   std::vector<void*> scratch_waits_;
   std::vector<std::uint32_t> scratch_pages_;
-  std::vector<std::uint32_t> scratch_ids_;  // issue(): host id lists handed to kvx_copy_pages_listed
 };
 
 }  // namespace symsim

@@ -548,28 +548,44 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
   for (std::size_t i = 1; i < src.size() && uniform; ++i)
     uniform = src[i].pool == src[0].pool && dst[i].pool == dst[0].pool;
   if (uniform && hbm(src[0].pool) && hbm(dst[0].pool)) {
-    // The ids travel in the mover's launch parameters (kvx_copy_pages_listed):
-    // no staging, no upload call.
     const std::size_t n = src.size();
-    std::vector<std::uint32_t>& ids = scratch_ids_;
-    ids.resize(2 * n);
-    for (std::size_t i = 0; i < n; ++i) ids[i] = src[i].page;
-    for (std::size_t i = 0; i < n; ++i) ids[n + i] = dst[i].page;
+    std::uint32_t* d_ids = nullptr;
+    {
+      const HostTimer up(host_ns_[kHostUpload]);
+      auto* h = static_cast<std::uint32_t*>(runner.stage(L, 2 * n * sizeof(std::uint32_t)));
+      for (std::size_t i = 0; i < n; ++i) h[i] = src[i].page;
+      for (std::size_t i = 0; i < n; ++i) h[n + i] = dst[i].page;
+      d_ids = runner.upload_ids(L, h, 2 * n);
+    }
     {
       const HostTimer launch_timer(host_ns_[kHostLaunch]);
-      kvx_check(kvx_copy_pages_listed(src_node.pools_[src[0].pool], ids.data(), pools_[dst[0].pool], ids.data() + n, n,
+      kvx_check(kvx_copy_pages_capped(src_node.pools_[src[0].pool], d_ids, pools_[dst[0].pool], d_ids + n, n,
                                       KVX_COPY_AUTO, push ? src_node.opts_.migrate_max_ctas : 0u, L.stream),
                 "page copy");
     }
     runner.close_batch(lane);
     return L.stream;
   }
-  // General case: bucket by pool pair.
+  // General case: bucket by pool pair; the id lists of every HBM<->HBM
+  // bucket go up in ONE staged upload.
   std::vector<std::uint32_t> bucket_ids[16][2];
   for (std::size_t i = 0; i < src.size(); ++i) {
     const int k = src[i].pool * 4 + dst[i].pool;
     bucket_ids[k][0].push_back(src[i].page);
     bucket_ids[k][1].push_back(dst[i].page);
+  }
+  std::size_t offsets[16][2] = {};
+  std::vector<std::uint32_t> staged;
+  for (int k = 0; k < 16; ++k)
+    if (!bucket_ids[k][0].empty() && hbm(k / 4) && hbm(k % 4))
+      for (int side = 0; side < 2; ++side) {
+        offsets[k][side] = staged.size();
+        staged.insert(staged.end(), bucket_ids[k][side].begin(), bucket_ids[k][side].end());
+      }
+  const std::uint32_t* d_staged = nullptr;
+  if (!staged.empty()) {
+    const HostTimer up(host_ns_[kHostUpload]);
+    d_staged = runner.device_ids(L, staged);
   }
   const HostTimer launch_timer(host_ns_[kHostLaunch]);
   for (int sp = 0; sp < 4; ++sp)
@@ -584,7 +600,9 @@ void* NodePayload::issue(const std::vector<Ref>& src, const std::vector<Ref>& ds
       const bool file_side = kvx_pool_file_direct(from) >= 0 || kvx_pool_file_direct(to) >= 0;
       const bool file_hop = file_side && (hbm(sp) || hbm(dp));
       if (hbm(sp) && hbm(dp)) {
-        kvx_check(kvx_copy_pages_listed(from, s_ids.data(), to, d_ids.data(), s_ids.size(), KVX_COPY_AUTO,
+        const std::uint32_t* ds = d_staged + offsets[sp * 4 + dp][0];
+        const std::uint32_t* dd = d_staged + offsets[sp * 4 + dp][1];
+        kvx_check(kvx_copy_pages_capped(from, ds, to, dd, s_ids.size(), KVX_COPY_AUTO,
                                         push ? src_node.opts_.migrate_max_ctas : 0u, L.stream),
                   "page copy");
       } else if (file_hop) {

@@ -124,7 +124,11 @@ __global__ void __launch_bounds__(kVecThreads) page_move_vec(MoveArgs a) {
 // Host-listed moves: the id pairs travel in the kernel's parameter block
 // (no upload, no device id array): used where the ids come from the host
 // per move (the payload's lanes), so a move costs one launch call.
-constexpr int kListedPairs = 3840;  // 30 KiB of ids + header < the 32,764-B parameter limit
+// A launch copies its whole parameter block, so the id arrays come in three
+// capacities (2 KiB / 8 KiB / 30 KiB of ids) and a move uses the smallest
+// that holds it; 3,840 pairs + header stay under the 32,764-B limit.
+constexpr int kListedPairs = 3840;
+template <int CAP>
 struct ListedBulkArgs {
   const uint8_t* src;
   uint8_t* dst;
@@ -133,10 +137,11 @@ struct ListedBulkArgs {
   uint32_t chunk_bytes;
   uint32_t chunks_per_page;
   int stages;
-  uint32_t src_ids[kListedPairs];
-  uint32_t dst_ids[kListedPairs];
+  uint32_t src_ids[CAP];
+  uint32_t dst_ids[CAP];
 };
-__device__ __forceinline__ void item_addr(const ListedBulkArgs& a, uint64_t item, const uint8_t*& s, uint8_t*& d,
+template <int CAP>
+__device__ __forceinline__ void item_addr(const ListedBulkArgs<CAP>& a, uint64_t item, const uint8_t*& s, uint8_t*& d,
                                           uint32_t& bytes) {
   const uint64_t page = item / a.chunks_per_page;
   const uint32_t c = static_cast<uint32_t>(item - page * a.chunks_per_page);
@@ -196,7 +201,8 @@ __global__ void __launch_bounds__(32, 1) page_move_bulk(MoveArgs a) {
   bulk_body(a);
 }
 
-__global__ void __launch_bounds__(32, 1) page_move_bulk_listed(const __grid_constant__ ListedBulkArgs a) {
+template <int CAP>
+__global__ void __launch_bounds__(32, 1) page_move_bulk_listed(const __grid_constant__ ListedBulkArgs<CAP> a) {
   bulk_body(a);
 }
 
@@ -280,17 +286,19 @@ int launch_move(MoveArgs a, int mode, int device, cudaStream_t stream, const cha
 // launch overhead, a 64 KiB page only ~1.2 us of PCIe time. Measured on B200
 // (profiles/r01_pcie_movers.json.txt): SM zero-copy moves 51-53 GB/s per
 // direction, fragmented or not, against 55-57 for copy engines on long runs.
+template <int CAP>
 struct ListedMove {
   const uint8_t* src;
   uint8_t* dst;
   uint64_t page_bytes;
   uint32_t n;
   uint32_t chunks_per_page;
-  uint32_t src_ids[kListedPairs];
-  uint32_t dst_ids[kListedPairs];
+  uint32_t src_ids[CAP];
+  uint32_t dst_ids[CAP];
 };
 
-__global__ void __launch_bounds__(kVecThreads) page_move_listed(const __grid_constant__ ListedMove a) {
+template <int CAP>
+__global__ void __launch_bounds__(kVecThreads) page_move_listed(const __grid_constant__ ListedMove<CAP> a) {
   const uint64_t items = static_cast<uint64_t>(a.n) * a.chunks_per_page;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint32_t i = static_cast<uint32_t>(item / a.chunks_per_page);
@@ -423,17 +431,11 @@ namespace {
 // bulk mover for HBM<->HBM on one device, the LDG/STG.128 mover otherwise
 // (peer, mapped host) or when asked (mode KVX_COPY_SM); `max_ctas` bounds
 // the grid (0: the mover's default).
-int launch_listed(const kvx_pool* src, const uint32_t* src_ids, const kvx_pool* dst, const uint32_t* dst_ids,
-                  uint64_t n, int mode, uint32_t max_ctas, cudaStream_t st, const char* who) {
-  const int dev = src->device >= 0 ? src->device : dst->device;
-  DeviceGuard guard(dev);
-  if (src->page_bytes % 16 || reinterpret_cast<uintptr_t>(src->base) % 16 || reinterpret_cast<uintptr_t>(dst->base) % 16)
-    return fail_arg("page movers need 16-byte aligned pages");
-  const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
-  const int sms = sm_count(dev);
-  if (mode == KVX_COPY_AUTO) mode = local ? KVX_COPY_TMA : KVX_COPY_SM;
-  if (mode == KVX_COPY_TMA) {
-    static thread_local ListedBulkArgs b;
+template <int CAP>
+int launch_listed_chunk(const kvx_pool* src, const uint32_t* src_ids, const kvx_pool* dst, const uint32_t* dst_ids,
+                        uint32_t n, bool tma, int dev, int sms, uint32_t max_ctas, cudaStream_t st, const char* who) {
+  if (tma) {
+    static thread_local ListedBulkArgs<CAP> b;
     const BulkGeometry geo = bulk_geometry(true, true);
     b.src = src->base;
     b.dst = dst->base;
@@ -448,43 +450,60 @@ int launch_listed(const kvx_pool* src, const uint32_t* src_ids, const kvx_pool* 
       static std::mutex mu;
       std::lock_guard<std::mutex> lock(mu);
       if (have.load(std::memory_order_relaxed) < smem) {
-        KVX_CUDA_TRY(cudaFuncSetAttribute(page_move_bulk_listed, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-                     who);
+        KVX_CUDA_TRY(
+            cudaFuncSetAttribute(page_move_bulk_listed<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), who);
         have.store(smem, std::memory_order_release);
       }
     }
-    for (uint64_t at = 0; at < n; at += kListedPairs) {
-      b.n_pages = std::min<uint64_t>(kListedPairs, n - at);
-      std::memcpy(b.src_ids, src_ids + at, b.n_pages * sizeof(uint32_t));
-      std::memcpy(b.dst_ids, dst_ids + at, b.n_pages * sizeof(uint32_t));
-      const uint64_t items = b.n_pages * b.chunks_per_page;
-      unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * geo.ctas_per_sm));
-      if (max_ctas && grid > max_ctas) grid = max_ctas;
-      page_move_bulk_listed<<<grid, 32, smem, st>>>(b);
-      note_launch();
-      KVX_CUDA_TRY(cudaGetLastError(), who);
-    }
-    return KVX_OK;
-  }
-  if (mode != KVX_COPY_SM) {
-    set_error(std::string(who) + ": unsupported copy mode");
-    return KVX_ERR_UNSUPPORTED;
-  }
-  static thread_local ListedMove m;
-  m.src = src->base;
-  m.dst = dst->base;
-  m.page_bytes = src->page_bytes;
-  m.chunks_per_page = static_cast<uint32_t>((src->page_bytes + kVecChunk - 1) / kVecChunk);
-  for (uint64_t at = 0; at < n; at += kListedPairs) {
-    m.n = static_cast<uint32_t>(std::min<uint64_t>(kListedPairs, n - at));
-    std::memcpy(m.src_ids, src_ids + at, m.n * sizeof(uint32_t));
-    std::memcpy(m.dst_ids, dst_ids + at, m.n * sizeof(uint32_t));
+    b.n_pages = n;
+    std::memcpy(b.src_ids, src_ids, n * sizeof(uint32_t));
+    std::memcpy(b.dst_ids, dst_ids, n * sizeof(uint32_t));
+    const uint64_t items = b.n_pages * b.chunks_per_page;
+    unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * geo.ctas_per_sm));
+    if (max_ctas && grid > max_ctas) grid = max_ctas;
+    page_move_bulk_listed<CAP><<<grid, 32, smem, st>>>(b);
+  } else {
+    static thread_local ListedMove<CAP> m;
+    m.src = src->base;
+    m.dst = dst->base;
+    m.page_bytes = src->page_bytes;
+    m.chunks_per_page = static_cast<uint32_t>((src->page_bytes + kVecChunk - 1) / kVecChunk);
+    m.n = n;
+    std::memcpy(m.src_ids, src_ids, n * sizeof(uint32_t));
+    std::memcpy(m.dst_ids, dst_ids, n * sizeof(uint32_t));
     const uint64_t items = static_cast<uint64_t>(m.n) * m.chunks_per_page;
     unsigned grid = static_cast<unsigned>(std::min<uint64_t>(items, static_cast<uint64_t>(sms) * 8));
     if (max_ctas && grid > max_ctas) grid = max_ctas;
-    page_move_listed<<<grid, kVecThreads, 0, st>>>(m);
-    note_launch();
-    KVX_CUDA_TRY(cudaGetLastError(), who);
+    page_move_listed<CAP><<<grid, kVecThreads, 0, st>>>(m);
+  }
+  note_launch();
+  KVX_CUDA_TRY(cudaGetLastError(), who);
+  return KVX_OK;
+}
+
+int launch_listed(const kvx_pool* src, const uint32_t* src_ids, const kvx_pool* dst, const uint32_t* dst_ids,
+                  uint64_t n, int mode, uint32_t max_ctas, cudaStream_t st, const char* who) {
+  const int dev = src->device >= 0 ? src->device : dst->device;
+  DeviceGuard guard(dev);
+  if (src->page_bytes % 16 || reinterpret_cast<uintptr_t>(src->base) % 16 || reinterpret_cast<uintptr_t>(dst->base) % 16)
+    return fail_arg("page movers need 16-byte aligned pages");
+  const bool local = !src->host && !dst->host && !src->ipc && !dst->ipc && src->device == dst->device;
+  const int sms = sm_count(dev);
+  if (mode == KVX_COPY_AUTO) mode = local ? KVX_COPY_TMA : KVX_COPY_SM;
+  if (mode != KVX_COPY_TMA && mode != KVX_COPY_SM) {
+    set_error(std::string(who) + ": unsupported copy mode");
+    return KVX_ERR_UNSUPPORTED;
+  }
+  const bool tma = mode == KVX_COPY_TMA;
+  for (uint64_t at = 0; at < n; at += kListedPairs) {
+    const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(kListedPairs, n - at));
+    const int rc = k <= 256    ? launch_listed_chunk<256>(src, src_ids + at, dst, dst_ids + at, k, tma, dev, sms,
+                                                          max_ctas, st, who)
+                   : k <= 1024 ? launch_listed_chunk<1024>(src, src_ids + at, dst, dst_ids + at, k, tma, dev, sms,
+                                                           max_ctas, st, who)
+                               : launch_listed_chunk<kListedPairs>(src, src_ids + at, dst, dst_ids + at, k, tma, dev,
+                                                                   sms, max_ctas, st, who);
+    if (rc) return rc;
   }
   return KVX_OK;
 }
