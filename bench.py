@@ -1039,14 +1039,22 @@ def bench_store_ring(args, torch, np, kvx, rank, world):
                 e0.record(peer_streams[src])
                 evs.append([src, e0])
         scheds = []
+        own = []  # per session: an event right before its own pushes are posted
         for s_ in range(world):
             src, dst = holder[s_], (holder[s_] + 1) % world
             stores[src].mark_migrating_out(s_)
+            if timed:
+                e_own = torch.cuda.Event(enable_timing=True)
+                e_own.record(peer_streams[src])
+                own.append(e_own)
             scheds.append((dst, stores[dst].import_migration(s_, cfg["ctx"], now)))  # posts the 80 pushes
         for ev in evs:
             e1 = torch.cuda.Event(enable_timing=True)
             e1.record(peer_streams[ev[0]])
             ev.append(e1)
+        if timed:
+            for ev, e_own in zip(evs, own):
+                ev.append(e_own)
         for dst, sched in scheds:
             pump(stores[dst], sched)
         for s_ in range(world):
@@ -1054,14 +1062,19 @@ def bench_store_ring(args, torch, np, kvx, rank, world):
             holder[s_] = (holder[s_] + 1) % world
         for nd in nodes:
             nd.synchronize()
-        return [e[1].elapsed_time(e[2]) for e in evs] if timed else None
+        if not timed:
+            return None
+        # (step start -> last push, own posting start -> last push) per device
+        return [(e[1].elapsed_time(e[2]), e[3].elapsed_time(e[2])) for e in evs]
 
     for _ in range(max(1, args.warmup)):
         step(False)
     steps = max(1, min(args.steps, 10))
     n0 = kvx.launch_count()
     t0 = time.perf_counter()
-    per_step = [max(step(True)) for _ in range(steps)]
+    timings = [step(True) for _ in range(steps)]
+    per_step = [max(t[0] for t in tt) for tt in timings]
+    per_device_own = [max(t[1] for t in tt) for tt in timings]
     wall = (time.perf_counter() - t0) / steps
     launches = kvx.launch_count() - n0
     # What each node holds now is the session's creation content, bit for bit.
@@ -1095,7 +1108,12 @@ def bench_store_ring(args, torch, np, kvx, rank, world):
                      "path": "per session: kvs_mark_migrating_out -> kvs_import_migration -> apply x L -> "
                              "kvs_release_session, host wall clock per ring step (all sessions)"},
                 store_path={"devices": ndev, "nodes": world, "probe_pages_checked": checked,
-                            "host_us_per_layer": host, "per_step_max_device_ms": per_step},
+                            "host_us_per_layer": host, "per_step_max_device_ms": per_step,
+                            "per_session_from_own_posting_ms": per_device_own,
+                            "device_side_gbs": session_bytes / (statistics.mean(per_device_own) * 1e-3) / GB,
+                            "note": "one host thread posts every node's import in turn (the reference simulator "
+                                    "is single-threaded): value counts from the step's start, "
+                                    "device_side_gbs from each session's own posting"},
                 roofline={"bound": "nvlink" if ndev > 1 else "hbm", "achieved": achieved,
                           "peak": NVLINK_PEAK_GBS if ndev > 1 else None, "unit": "GB/s",
                           "frac": achieved / NVLINK_PEAK_GBS if ndev > 1 else None, "traffic": None,
