@@ -511,6 +511,20 @@ def test_fused_append_decode_step(dev, layout, hq, splits):
     torch.cuda.synchronize()
     assert torch.equal(pool_a.as_tensor(), pool_b.as_tensor())
     assert torch.equal(out_a, out_b)
+    # and against the fp64 oracle over the pool the fused step left behind
+    _check_against_oracle(pool_a, layout, hq, tables, ctx_lens, q, out_a)
+
+
+def _check_against_oracle(pool, layout, hq, tables, ctx_lens, q, out):
+    qn = q.cpu().view(torch.int16).numpy().view(np.uint16) if q.dtype == torch.bfloat16 else q.cpu().numpy()
+    scale = float(np.float32(1.0 / np.sqrt(np.float32(layout.head_dim))))
+    ref = O.decode_attention(pool.as_tensor().cpu().numpy(), olayout(layout), hq, tables, ctx_lens, qn, scale)
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
+    if layout.dtype == kvx.BF16:
+        assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (err.max(), err.mean())
+        assert err.mean() < 5e-4
+    else:
+        assert np.all(err <= 1e-5 * np.maximum(1.0, np.abs(ref))), err.max()
 
 
 def test_fused_decode_step_full_size(dev):
@@ -546,6 +560,7 @@ def test_fused_decode_step_full_size(dev):
     torch.cuda.synchronize()
     assert torch.equal(pool_a.as_tensor(), pool_b.as_tensor())
     assert torch.equal(out_a, out_b)
+    _check_against_oracle(pool_a, layout, 32, tables, lens, q, out_a)
     page = pool_a.as_tensor()[int(tables[1, t[1] // 16])].view(torch.bfloat16).view(2, 8, 16, 128)
     assert torch.equal(page[0, :, t[1] % 16], nk[1]) and torch.equal(page[1, :, t[1] % 16], nv[1])
 
