@@ -49,5 +49,50 @@ for layout in (kvx.PageLayout(8, 128, 16, kvx.BF16), kvx.PageLayout(4, 64, 16, k
         early = kvx.Attention(layout, hq, blocks, num_splits=splits, split_merge=merge, flags=kvx.ATTN_EARLY_PREFETCH)
         early(pool, tables, lens, q, out, batch, ctx, ws)
         early(pool, tables, lens, q, out, batch, ctx, ws, new_k=nk, new_v=nk)
+    # round 2: the CE lane with host ids (listed-id SM mover for fragmented
+    # ids, per-run copies for runs) and kvx_copy_pages_listed (TMA / SM)
+    hids = rng.permutation(n).astype(np.uint32)
+    kvx.copy_pages(pool, ids.cpu().numpy().astype(np.uint32), host, hids, n, kvx.COPY_CE)
+    kvx.copy_pages(host, hids, pool, dst.cpu().numpy().astype(np.uint32), n, kvx.COPY_CE)
+    runs = np.arange(n, dtype=np.uint32)
+    kvx.copy_pages(pool, runs, host, runs, n, kvx.COPY_CE)
+    import ctypes
+    lib = kvx.lib()
+    V, U64 = ctypes.c_void_p, ctypes.c_uint64
+    lib.kvx_copy_pages_listed.argtypes = [V, V, V, V, U64, ctypes.c_int, ctypes.c_uint32, V]
+    s_ids = ids.cpu().numpy().astype(np.uint32)
+    d_ids = dst.cpu().numpy().astype(np.uint32)
+    for mode in (kvx.COPY_AUTO, kvx.COPY_SM, kvx.COPY_TMA):
+        assert lib.kvx_copy_pages_listed(pool.handle, s_ids.ctypes.data, pool.handle, d_ids.ctypes.data, n, mode, 0,
+                                         None) == 0, lib.kvx_last_error()
+
+# round 2: K7 projections (one small model's shapes) and the model's kernels
+import ctypes  # noqa: E402
+
+
+class ModelConfig(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("hidden", ctypes.c_int32), ("num_q_heads", ctypes.c_int32),
+                ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32), ("intermediate", ctypes.c_int32),
+                ("vocab", ctypes.c_int32), ("rms_eps", ctypes.c_float), ("rope_theta", ctypes.c_float)]
+
+
+lib = kvx.lib()
+lib.kvx_model_create.argtypes = [ctypes.c_int, ctypes.POINTER(ModelConfig), ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]
+lib.kvx_model_linear.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int32] * 4 + [ctypes.c_void_p]
+lib.kvx_model_prefill.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]
+lib.kvx_model_destroy.argtypes = [ctypes.c_void_p]
+cfg = ModelConfig(1, 512, 8, 2, 128, 1024, 1024, 1e-5, 500000.0)
+m = ctypes.c_void_p()
+assert lib.kvx_model_create(0, ctypes.byref(cfg), 3, ctypes.byref(m)) == 0, lib.kvx_last_error()
+for rows in (1, 5, 8, 12):
+    for k_, n_ in ((512, 1536), (1024, 512), (512, 1024)):
+        x = torch.randn(rows, k_, device=dev).to(torch.bfloat16)
+        w = torch.randn(n_, k_, device=dev).to(torch.bfloat16)
+        y = torch.zeros(rows, n_, device=dev, dtype=torch.bfloat16)
+        for acc in (0, 1):
+            assert lib.kvx_model_linear(m, x.data_ptr(), w.data_ptr(), y.data_ptr(), rows, k_, n_, acc, None) == 0
+assert lib.kvx_model_prefill(m, 40, None) == 0  # norms, SiLU, argmax of the last row
+torch.cuda.synchronize()
+lib.kvx_model_destroy(m)
 torch.cuda.synchronize()
 print("sanitize driver done")
