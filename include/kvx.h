@@ -95,6 +95,10 @@ typedef struct {
  * pages are then fetched before waiting on that kernel (programmatic
  * dependent launch), overlapping its tail. */
 #define KVX_ATTN_EARLY_PREFETCH 1
+/* Bits 8..11: clusters per (request, kv head) for an explicit split count
+ * (num_splits = G x C): C-CTA clusters merge over DSMEM, then the G cluster
+ * results merge in the workspace (needed). 0 / 1: one cluster (or the auto plan). */
+#define KVX_ATTN_CLUSTERS(g) (((g) & 0xF) << 8)
 
 /* Split-K merge strategies (both in-kernel, one launch). AUTO picks CLUSTER
  * when the splits of each (request, kv head) fit one thread-block cluster

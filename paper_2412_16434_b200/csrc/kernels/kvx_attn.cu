@@ -174,7 +174,9 @@ struct AttnArgs {
   float* part_o;      // [B][Hq][S][128]
   float* part_ml;     // [B][Hq][S][2]
   uint32_t* arrivals; // [B][H] split counters; zero between launches
-  int cluster_merge;  // 1: the splits of a (request, kv head) form one cluster; merge over DSMEM
+  int cluster_merge;  // 1: the splits of a (request, kv head) form clusters; merge over DSMEM
+  int csize;          // cluster size (splits per cluster); splits = csize * cgroups
+  int cgroups;        // clusters per (request, kv head): > 1 adds a merge of the clusters' results in the workspace
   int early_prefetch; // KVX_ATTN_EARLY_PREFETCH: table + first pages before griddepcontrol.wait
   int signal_at;      // launch_dependents: 0 after the split merge, 1 after the page loop, 2 at kernel start
   int heads;          // kv heads
@@ -215,14 +217,16 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
   }
   // Output slice per cluster CTA, in float4 units so no vector push straddles
   // two owners.
-  const int chunk = ((a.group * kD + a.splits - 1) / a.splits + 3) & ~3;
+  const int csize = a.cluster_merge ? a.csize : a.splits;
+  const int crank = split % csize;  // rank in this CTA's cluster (clusters tile grid x)
+  const int chunk = ((a.group * kD + csize - 1) / csize + 3) & ~3;
   if (a.cluster_merge) {
     if (threadIdx.x == 0) {
       // One arrival (ours, with the byte count) + every partial's bytes.
-      const int len = max(0, min(chunk, a.group * kD - split * chunk));
+      const int len = max(0, min(chunk, a.group * kD - crank * chunk));
       mbar_init(&s_merge_bar, 1);
       fence_mbar_init();
-      mbar_arrive_expect_tx(&s_merge_bar, static_cast<uint32_t>(a.splits * (len * 4 + a.group * 8)));
+      mbar_arrive_expect_tx(&s_merge_bar, static_cast<uint32_t>(csize * (len * 4 + a.group * 8)));
     }
     // Publishes the barrier (and its expected bytes) to the cluster; the
     // matching wait comes after the page loop, long after every CTA arrived.
@@ -538,11 +542,11 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
     };
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // every owner's barrier is armed
     const uint32_t bar_local = smem_u32(&s_merge_bar);
-    if (threadIdx.x < rows * a.splits) {
-      const int r = threadIdx.x / a.splits, owner = threadIdx.x - r * a.splits;
+    if (threadIdx.x < rows * csize) {
+      const int r = threadIdx.x / csize, owner = threadIdx.x - r * csize;
       float f[W], M, L;
       row_weights(r, f, M, L);
-      st_async_v2(map_rank(smem_u32(s_recv_ml + (split * 16 + r) * 2), owner), M, L, map_rank(bar_local, owner));
+      st_async_v2(map_rank(smem_u32(s_recv_ml + (crank * 16 + r) * 2), owner), M, L, map_rank(bar_local, owner));
     }
     for (int q = threadIdx.x; q < rows * kD / 4; q += blockDim.x) {
       const int e = 4 * q, r = e / kD, d = e - r * kD;
@@ -558,7 +562,7 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
         O.w += f[w] * v.w;
       }
       const int owner = e / chunk;
-      st_async_v4(map_rank(smem_u32(s_recv_o + split * chunk + (e - owner * chunk)), owner), O,
+      st_async_v4(map_rank(smem_u32(s_recv_o + crank * chunk + (e - owner * chunk)), owner), O,
                   map_rank(bar_local, owner));
     }
     KVX_TRACE(5);
@@ -567,10 +571,12 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
     // another CTA's memory, so no closing cluster barrier is needed.
     mbar_wait_cluster(&s_merge_bar, 0);
     KVX_TRACE(10);
-    const int ns = a.splits;
-    const int e_end = min(rows * kD, (split + 1) * chunk);
-    for (int e = split * chunk + threadIdx.x; e < e_end; e += blockDim.x) {
-      const int r = e / kD, d = e - r * kD, off = e - split * chunk;
+    const int ns = csize;
+    const int e_begin = crank * chunk, e_end = min(rows * kD, (crank + 1) * chunk);
+    const int G = a.cgroups, cg = split / csize;
+    const uint64_t row0 = static_cast<uint64_t>(b) * a.heads * a.group + hq0;
+    for (int e = e_begin + threadIdx.x; e < e_end; e += blockDim.x) {
+      const int r = e / kD, d = e - r * kD, off = e - e_begin;
       float M = -INFINITY;
       for (int s2 = 0; s2 < ns; ++s2) M = fmaxf(M, s_recv_ml[(s2 * 16 + r) * 2]);
       const float Mb = M == -INFINITY ? 0.f : M;
@@ -580,7 +586,43 @@ __global__ void __launch_bounds__(W * 32, W >= 8 ? 1 : 8 / W) attn_bf16_d128(con
         L += f * s_recv_ml[(s2 * 16 + r) * 2 + 1];
         O += f * s_recv_o[s2 * chunk + off];
       }
-      a.out[(static_cast<uint64_t>(b) * a.heads * a.group + hq0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
+      if (G == 1) {
+        a.out[(row0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
+      } else {  // this cluster's partial of the slice, for the merge across clusters
+        a.part_o[((row0 + r) * G + cg) * kD + d] = O;
+        if (d == 0 || e == e_begin) {  // (M, L) of the row: identical in every owner of this cluster
+          a.part_ml[((row0 + r) * G + cg) * 2] = M;
+          a.part_ml[((row0 + r) * G + cg) * 2 + 1] = L;
+        }
+      }
+    }
+    if (G > 1) {
+      // Merge across the G clusters of this (request, kv head), slice by
+      // slice: the owners of slice crank arrive on one counter; the last one
+      // combines the G partials in cluster order (deterministic) and resets it.
+      __threadfence();
+      __syncthreads();
+      uint32_t* arrive = a.arrivals + (static_cast<uint64_t>(b) * a.heads + h) * kMaxClusterSplits + crank;
+      if (threadIdx.x == 0) s_last = atomicAdd(arrive, 1u) == static_cast<uint32_t>(G - 1);
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        for (int e = e_begin + threadIdx.x; e < e_end; e += blockDim.x) {
+          const int r = e / kD, d = e - r * kD;
+          const float* ml = a.part_ml + (row0 + r) * G * 2;
+          float M = -INFINITY;
+          for (int g2 = 0; g2 < G; ++g2) M = fmaxf(M, __ldcg(ml + 2 * g2));
+          const float Mb = M == -INFINITY ? 0.f : M;
+          float L = 0.f, O = 0.f;
+          for (int g2 = 0; g2 < G; ++g2) {
+            const float f = exp2f(__ldcg(ml + 2 * g2) - Mb);
+            L += f * __ldcg(ml + 2 * g2 + 1);
+            O += f * __ldcg(a.part_o + ((row0 + r) * G + g2) * kD + d);
+          }
+          a.out[(row0 + r) * kD + d] = L > 0.f ? O / L : 0.f;
+        }
+        if (threadIdx.x == 0) *arrive = 0;  // ready for the next launch
+      }
     }
     KVX_TRACE(6);
     if (a.signal_at == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -772,9 +814,14 @@ int choose_splits(int batch, int heads, int max_ctx, int requested, int sms) {
   return std::max(min_splits, std::min(max_splits, s));
 }
 
+// Split partials ([B][Hq][S][kD + 2] floats) + arrival counters
+// ([B][H][kMaxClusterSplits]: one per (request, kv head), or per output slice
+// when the splits form several clusters). Sized for at least
+// kMaxClusterSplits splits, so any plan of this launch shape fits.
 uint64_t workspace_for(uint64_t batch, uint64_t hq, uint64_t heads, int splits) {
   if (splits <= 1) return 0;
-  return batch * hq * splits * (kD + 2) * sizeof(float) + batch * heads * sizeof(uint32_t);
+  const uint64_t s = static_cast<uint64_t>(std::max(splits, kMaxClusterSplits));
+  return batch * hq * s * (kD + 2) * sizeof(float) + batch * heads * kMaxClusterSplits * sizeof(uint32_t);
 }
 
 // One-time per-device kernel attributes (dynamic smem, cluster sizes > 8).
@@ -881,8 +928,9 @@ int cluster_capacity(int device, int splits, bool tma) {
 
 struct Plan {
   int splits;
-  bool cluster;  // merge over DSMEM (grid x = splits = cluster size)
-  bool narrow;   // 8 warps per CTA
+  bool cluster;    // merge over DSMEM (cluster size = splits / groups)
+  bool narrow;     // 8 warps per CTA
+  int groups = 1;  // clusters per (request, kv head); > 1: their results merge in the workspace
 };
 
 // Launch plan: the split count from choose_splits; the splits of each
@@ -893,7 +941,8 @@ struct Plan {
 // clusters do not co-reside 8 at a time on B200's GPCs and run in two
 // waves, which the occupancy check catches). Explicit split counts and
 // merge modes are honoured (tests, sweeps).
-Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge, int device, bool tma) {
+Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge, int device, bool tma,
+                    int req_groups = 1) {
   const int sms = sm_count(device);
   const long groups = std::max(1L, static_cast<long>(batch) * heads);
   const int pages = std::max(1, (max_ctx + kT - 1) / kT);
@@ -913,6 +962,10 @@ Plan plan_attention(int batch, int heads, int max_ctx, int requested, int merge,
       }
     }
   }
+  // Two-level merge on request (KVX_ATTN_CLUSTERS(G) in the flags with an
+  // explicit split count S): S/G-CTA clusters, G per (request, kv head).
+  if (req_groups > 1 && requested > 0 && merge != KVX_MERGE_GLOBAL)
+    return Plan{requested, true, true, req_groups};
   if (!p.cluster) p.narrow = static_cast<long>(p.splits) * groups <= sms;
   // KVX_ATTN_NARROW=0|1 forces the 4-warp (2 CTAs/SM) / 8-warp variant of a
   // workspace-merged launch (measurement knob).
@@ -970,8 +1023,15 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
                                   ? nullptr
                                   : kvx::attn_tensor_map(const_cast<kvx_pool*>(pool), H);
     const bool tma = tmap != nullptr;
+    const int req_groups = (params->flags >> 8) & 0xF;
+    if (req_groups > 1 && (params->num_splits <= 0 || params->num_splits % req_groups ||
+                           params->num_splits / req_groups < 2 ||
+                           params->num_splits / req_groups > kvx::kMaxClusterSplits ||
+                           params->split_merge == KVX_MERGE_GLOBAL))
+      return kvx::fail_arg("kvx_decode_attention: KVX_ATTN_CLUSTERS(G) needs num_splits = G x C, 2 <= C <= 16, "
+                           "and a cluster merge");
     const kvx::Plan plan =
-        kvx::plan_attention(batch, H, max_ctx, params->num_splits, params->split_merge, dev, tma);
+        kvx::plan_attention(batch, H, max_ctx, params->num_splits, params->split_merge, dev, tma, req_groups);
     if (params->split_merge == KVX_MERGE_CLUSTER && !plan.cluster && plan.splits > 1)
       return kvx::fail_arg("kvx_decode_attention: split_merge=CLUSTER but the splits do not fit one cluster");
     const int splits = plan.splits;
@@ -993,6 +1053,8 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     a.splits = splits;
     a.scale_log2 = scale * kvx::kLog2e;
     a.cluster_merge = plan.cluster ? 1 : 0;
+    a.cgroups = plan.cluster ? plan.groups : 1;
+    a.csize = plan.cluster ? splits / plan.groups : splits;
     a.early_prefetch = (params->flags & KVX_ATTN_EARLY_PREFETCH) ? 1 : 0;
     {
       // Measured with early prefetch on (32 / 64 q heads, batch 1-8,
@@ -1009,7 +1071,7 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
       static const char* sig_env = std::getenv("KVX_ATTN_SIGNAL");
       if (sig_env && sig_env[0] >= '0' && sig_env[0] <= '2') a.signal_at = sig_env[0] - '0';
     }
-    if (splits > 1 && !plan.cluster) {
+    if (splits > 1 && (!plan.cluster || plan.groups > 1)) {
       const uint64_t rows = static_cast<uint64_t>(batch) * Hq;
       if (!d_workspace || workspace_bytes < kvx::workspace_for(batch, Hq, H, splits))
         return kvx::fail_arg("kvx_decode_attention: workspace too small");
@@ -1031,7 +1093,7 @@ int decode_attention(const kvx_pool* pool, const kvx_page_layout* layout, const 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = plan.cluster ? splits : 1;
+    attr[1].val.clusterDim.x = plan.cluster ? splits / plan.groups : 1;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     // Cluster launches use PDL too, with launch_dependents at the very end of

@@ -345,7 +345,7 @@ def test_append_kv_bit_exact(dev, layout):
     assert np.array_equal(pool.as_tensor().cpu().numpy(), ref)
 
 
-def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0, merge=kvx.MERGE_AUTO):
+def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0, merge=kvx.MERGE_AUTO, flags=0):
     rng = np.random.default_rng(seed)
     pb = layout.page_bytes()
     batch = len(ctx_lens)
@@ -362,7 +362,7 @@ def _attention_case(dev, layout, hq, ctx_lens, splits=0, seed=0, merge=kvx.MERGE
     else:
         q = rng.standard_normal((batch, hq, layout.head_dim)).astype(np.float32)
     ctx = np.asarray(ctx_lens, np.int32)
-    att = kvx.Attention(layout, hq, max_blocks, num_splits=splits, split_merge=merge)
+    att = kvx.Attention(layout, hq, max_blocks, num_splits=splits, split_merge=merge, flags=flags)
     ws_bytes = att.workspace_bytes(batch, max_ctx)
     ws = torch.zeros(max(ws_bytes, 1), dtype=torch.uint8, device=dev) if ws_bytes else None
     out = torch.full((batch, hq, layout.head_dim), float("nan"), dtype=torch.float32, device=dev)
@@ -406,6 +406,25 @@ def test_attention_cluster_merge(dev, hq, ctx_lens, splits):
     err = np.abs(got - ref)
     assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (err.max(), err.mean())
     assert err.mean() < 5e-4
+
+
+@pytest.mark.parametrize("hq,ctx_lens,splits,groups", [
+    (32, [32768], 16, 4), (32, [8192], 12, 2), (32, [5000, 16, 0], 15, 3), (64, [4096], 8, 2),
+    (32, [100], 16, 2),  # slices with no pages in some clusters
+])
+def test_attention_two_level_cluster_merge(dev, hq, ctx_lens, splits, groups):
+    """KVX_ATTN_CLUSTERS(G): the splits of a (request, kv head) form G
+    clusters of splits/G CTAs; each cluster merges over DSMEM, then the last
+    owner of each output slice merges the G cluster results from the
+    workspace. Checked against the fp64 oracle, twice in a row (the arrival
+    counters reset)."""
+    flags = kvx.ATTN_EARLY_PREFETCH | (groups << 8)
+    for rep in range(2):
+        got, ref = _attention_case(dev, LLAMA8B, hq, ctx_lens, splits, seed=splits + rep, merge=kvx.MERGE_AUTO,
+                                   flags=flags)
+        err = np.abs(got - ref)
+        assert np.all(err <= 2e-3 + 1e-2 * np.abs(ref)), (rep, err.max(), err.mean())
+        assert err.mean() < 5e-4
 
 
 def test_attention_cluster_merge_refuses_what_does_not_fit(dev):

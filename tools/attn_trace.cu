@@ -112,7 +112,7 @@ int main(int argc, char** argv) {
   launch(iters + 1);
   cudaStreamSynchronize(st);
   const char* tma_env = getenv("KVX_ATTN_TMA");
-  const kvx::Plan plan = kvx::plan_attention(batch, H, ctx, splits_req, merge, 0, !(tma_env && tma_env[0] == '0'));
+  const kvx::Plan plan = kvx::plan_attention(batch, H, ctx, splits_req, merge, 0, !(tma_env && tma_env[0] == '0'), (flags >> 8) & 0xF);
   const int splits = plan.splits;
   const int ctas = splits * H * batch;
   std::vector<unsigned long long> tr(static_cast<size_t>(ctas) * 32);
