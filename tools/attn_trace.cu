@@ -53,7 +53,7 @@ int main(int argc, char** argv) {
   std::mt19937 rng(7);
   std::vector<uint32_t> ids(pages);
   std::iota(ids.begin(), ids.end(), 0u);
-  std::shuffle(ids.begin(), ids.end(), rng);
+  if (!getenv("KVX_TRACE_SEQUENTIAL")) std::shuffle(ids.begin(), ids.end(), rng);  // sequential: pages in table order
   uint32_t* d_tables;
   cudaMalloc(&d_tables, pages * 4);
   cudaMemcpy(d_tables, ids.data(), pages * 4, cudaMemcpyHostToDevice);
