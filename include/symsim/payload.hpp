@@ -95,6 +95,7 @@ class PayloadCluster {
 class NodePayload final : public TierBackend {
  public:
   enum Pool : int { kDevicePool = 0, kHostPool = 1, kLandingPool = 2, kDiskPool = 3 };
+  static constexpr int kPools = 4;
 
   NodePayload(PayloadCluster* cluster, int node_id, const PayloadOptions& opts);
   ~NodePayload() override;
@@ -279,6 +280,8 @@ class NodePayload final : public TierBackend {
   InFlight& flight(std::uint32_t coming) { return flights_[coming - 1]; }
   const InFlight& flight(std::uint32_t coming) const { return flights_[coming - 1]; }
   static Ref flight_page(const InFlight& f, std::uint32_t b);
+  static void reset_flight(InFlight& f);
+  void give_back(const Ref* pages, std::size_t n);
   std::uint32_t alloc(Pool p);
   void alloc_n(Pool p, std::size_t n, std::vector<std::uint32_t>& out);
   void release(const Ref& r);

@@ -6,6 +6,8 @@ Product: paper_2412_16434_b200/lib/libkvx.so (sm_100a kernels, include/kvx.h)
 """
 from __future__ import annotations
 
+import contextlib
+import fcntl
 import os
 import shutil
 import subprocess
@@ -25,6 +27,19 @@ def _jobs() -> str:
     return str(max(1, min(16, os.cpu_count() or 1)))
 
 
+@contextlib.contextmanager
+def _build_lock():
+    """One build at a time across processes (pytest-xdist workers share the
+    build tree and the overlay headers)."""
+    (ROOT / "build").mkdir(exist_ok=True)
+    with open(ROOT / "build" / ".lock", "w") as fh:
+        fcntl.flock(fh, fcntl.LOCK_EX)
+        try:
+            yield
+        finally:
+            fcntl.flock(fh, fcntl.LOCK_UN)
+
+
 def _make(directory: Path, *targets: str) -> None:
     if shutil.which("make") is None:
         raise RuntimeError("make is required to build the B200 libraries")
@@ -36,19 +51,22 @@ def _make(directory: Path, *targets: str) -> None:
 
 def build_product() -> None:
     """Compile every CUDA/C++ product source for sm_100a (idempotent)."""
-    _make(CSRC, "all")
+    with _build_lock():
+        _make(CSRC, "all")
 
 
 def build_oracle(ref: bool = True) -> None:
     """Compile the oracle's C restatement, and the reference oracle when the
     reference sources are present (they are not on the GPU box, which uses the
     prebuilt oracle/_ref files)."""
-    _make(ORACLE_DIR, "payload")
+    with _build_lock():
+        _make(ORACLE_DIR, "payload")
     ref_src = Path(os.environ.get("REF", "/root/reference/proj")) / "src" / "kvstore.cpp"
     if ref and ref_src.exists():
-        _make(ORACLE_DIR, "ref")
+        with _build_lock():
+            _make(ORACLE_DIR, "ref")
         for name in ("build_payload_sim.sh", "build_serve_sim.sh", "build_serve_gpu.sh"):
-            script = ROOT / "tests" / "cpp" / name
+            script = ROOT / "tests" / "cpp" / name  # takes build/.lock itself
             proc = subprocess.run(["bash", str(script)], capture_output=True, text=True)
             if proc.returncode != 0:
                 raise RuntimeError(f"build failed: {script}\n{proc.stdout}\n{proc.stderr}")

@@ -243,6 +243,23 @@ void NodePayload::release(const Ref& r) {
   ++held_[r.pool];
 }
 
+// Returns held pages to their free lists (each list grows once; per-page
+// push_back dominated reclaim on 2,048-page layers). Order within a pool is
+// the order of `pages`, as one push_back at a time would leave it.
+void NodePayload::give_back(const Ref* pages, std::size_t n) {
+  std::size_t count[kPools] = {};
+  for (std::size_t i = 0; i < n; ++i) ++count[pages[i].pool];
+  std::uint32_t* out[kPools] = {};
+  for (int p = 0; p < kPools; ++p) {
+    if (!count[p]) continue;
+    const std::size_t at = free_[p].size();
+    free_[p].resize(at + count[p]);
+    out[p] = free_[p].data() + at;
+    held_[p] -= count[p];
+  }
+  for (std::size_t i = 0; i < n; ++i) *out[pages[i].pool]++ = pages[i].page;
+}
+
 // Closes the group of pages freed so far: they may be reused once every
 // batch queued until now, on any lane of any node, has completed.
 void NodePayload::seal_released() {
@@ -257,10 +274,7 @@ void NodePayload::seal_released() {
   else
     mark(*this);
   if (h.marks.empty()) {  // nothing queued anywhere: free now
-    for (const Ref& r : released_) {
-      free_[r.pool].push_back(r.page);
-      --held_[r.pool];
-    }
+    give_back(released_.data(), released_.size());
   } else {
     h.pages.assign(released_.begin(), released_.end());  // released_ keeps its capacity
     quarantine_.push_back(std::move(h));
@@ -294,10 +308,7 @@ bool NodePayload::reclaim(bool wait_for_oldest) {
       L.retire();
     }
     if (!ready) break;
-    for (const Ref& r : h.pages) {
-      free_[r.pool].push_back(r.page);
-      --held_[r.pool];
-    }
+    give_back(h.pages.data(), h.pages.size());
     quarantine_.pop_front();
     any = true;
     wait_for_oldest = false;
@@ -435,6 +446,19 @@ NodePayload::Ref NodePayload::best_source(std::uint32_t s, std::uint16_t l, std:
 NodePayload::Ref NodePayload::flight_page(const InFlight& f, std::uint32_t b) {
   const auto pos = std::lower_bound(f.blocks.begin(), f.blocks.end(), b);  // f.blocks ascends
   return f.pages[static_cast<std::size_t>(pos - f.blocks.begin())];
+}
+
+// Empties a finished flight slot but keeps its vectors' capacity: the next
+// posting into the slot refills them without a fresh allocation (2,048-block
+// layers at 70B @32K).
+void NodePayload::reset_flight(InFlight& f) {
+  f.id = 0;
+  f.tier = 0;
+  f.session = 0;
+  f.layer = 0;
+  f.blocks.clear();
+  f.pages.clear();
+  f.event = nullptr;
 }
 
 bool NodePayload::inflight_source(std::uint32_t s, std::uint16_t l, std::uint32_t b, int exclude_tier, Ref* page,
@@ -688,10 +712,24 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
   const std::uint32_t slot = flight_of_.at(applying_);
   InFlight& f = flights_[slot];
   applying_valid_ = false;
-  std::vector<bool> used(f.blocks.size(), false);
   std::vector<std::uint32_t> missing;
   Row& r = row(session, layer);
   presize(r, blocks);
+  if (blocks.size() == f.blocks.size() &&
+      std::equal(blocks.begin(), blocks.end(), f.blocks.begin())) {  // the usual case: every posted block gained
+    Copies* const rb = r.b.data();
+    const Ref* const fp = f.pages.data();
+    for (std::size_t i = 0; i < blocks.size(); ++i) {
+      Copies& c = rb[blocks[i]];
+      if (c.slot[t] != kNoPage) release(c.tier(t));
+      c.slot[t] = pack(fp[i]);
+    }
+    kvx_event_destroy(f.event);
+    reset_flight(f);
+    flight_of_.erase(applying_);
+    free_flights_.push_back(slot);
+    return;
+  }
   std::size_t cursor = 0;  // both lists usually ascend: a merge walk, bisection otherwise
   for (std::uint32_t b : blocks) {
     std::size_t i = cursor;
@@ -707,12 +745,11 @@ void NodePayload::tier_gained(std::uint32_t session, std::uint16_t layer, Tier t
     Copies& c = at(r, b);
     release(c.tier(t));
     c.slot[t] = pack(f.pages[i]);
-    used[i] = true;
+    f.pages[i] = Ref{};  // installed; release() skips it below
   }
-  for (std::size_t i = 0; i < f.blocks.size(); ++i)
-    if (!used[i]) release(f.pages[i]);
+  for (const Ref& p : f.pages) release(p);
   kvx_event_destroy(f.event);
-  f = InFlight{};
+  reset_flight(f);
   flight_of_.erase(applying_);
   free_flights_.push_back(slot);
   if (!missing.empty()) move_now(session, layer, tier, why, missing);
@@ -783,12 +820,20 @@ void NodePayload::tier_lost(std::uint32_t session, std::uint16_t layer, Tier tie
   const int t = static_cast<int>(tier);
   const auto it = rows_.find(row_key(session, layer));
   if (it == rows_.end()) return;
-  for (std::uint32_t b : blocks) {
-    if (b >= it->second.b.size()) continue;
-    Copies& c = it->second.b[b];
-    release(c.tier(t));
-    c.slot[t] = kNoPage;
+  const std::size_t base = released_.size();
+  released_.resize(base + blocks.size());
+  Ref* const out = released_.data() + base;
+  std::size_t n = 0;
+  Copies* const rb = it->second.b.data();
+  const std::size_t rn = it->second.b.size();
+  for (const std::uint32_t b : blocks) {
+    if (b >= rn || rb[b].slot[t] == kNoPage) continue;
+    const Ref r = rb[b].tier(t);  // release(), inlined
+    out[n++] = r;
+    ++held_[r.pool];
+    rb[b].slot[t] = kNoPage;
   }
+  released_.resize(base + n);
   drop_row_if_empty(session, layer);
 }
 
@@ -839,30 +884,41 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
   const Row* srow = src_node->find_row(tr.session, tr.layer);
   const int exclude = src_node == this ? t : -1;
   const std::size_t span = static_cast<std::size_t>(tr.block_hi - tr.block_lo + 1);
-  src.reserve(span);
-  f.blocks.reserve(span);
+  // Written through raw pointers into buffers sized for the whole span, then
+  // trimmed: per-element push_back costs several times the loop body on
+  // 2,048-block layers.
+  src.resize(span);
+  f.blocks.resize(span);
+  Ref* const sp = src.data();
+  std::uint32_t* const bp = f.blocks.data();
+  std::size_t n = 0;
+  const Copies* const hv = have ? have->b.data() : nullptr;
+  const std::size_t hn = have ? have->b.size() : 0;
+  const Copies* const sv = srow ? srow->b.data() : nullptr;
+  const std::size_t sn = srow ? srow->b.size() : 0;
   for (std::uint64_t b64 = tr.block_lo; b64 <= tr.block_hi; ++b64) {
     const auto b = static_cast<std::uint32_t>(b64);
-    if (have && b < have->b.size()) {
-      const Copies& c = have->b[b];
-      if (c.slot[t] != kNoPage || c.coming[t]) continue;  // already there / already coming
-    }
-    if (!srow || b >= srow->b.size()) continue;
-    const Copies& sc = srow->b[b];
+    if (b < hn && (hv[b].slot[t] != kNoPage || hv[b].coming[t])) continue;  // already there / already coming
+    if (b >= sn) continue;
+    const Copies& sc = sv[b];
+    const int k = (exclude != 0 && sc.slot[0] != kNoPage)   ? 0
+                  : (exclude != 1 && sc.slot[1] != kNoPage) ? 1
+                  : (exclude != 2 && sc.slot[2] != kNoPage) ? 2
+                                                            : -1;
     Ref from;
-    for (int k = 0; k < 3; ++k)
-      if (k != exclude && sc.slot[k] != kNoPage) {
-        from = sc.tier(k);
-        break;
-      }
-    if (from.pool < 0) {  // chained behind a move still in flight on the source side
+    if (k >= 0) {
+      from = sc.tier(k);
+    } else {  // chained behind a move still in flight on the source side
       void* ev = nullptr;
       if (!src_node->inflight_source(tr.session, tr.layer, b, exclude, &from, &ev)) continue;
       if (waits.empty() || waits.back() != ev) waits.push_back(ev);
     }
-    src.push_back(from);
-    f.blocks.push_back(b);
+    sp[n] = from;
+    bp[n] = b;
+    ++n;
   }
+  src.resize(n);
+  f.blocks.resize(n);
   if (f.blocks.empty()) {
     free_flights_.push_back(slot);
     return;
@@ -872,8 +928,13 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
   // the HBM movers take any permutation.
   if (dest == kHostPool || dest == kDiskPool) sort_pages(pages);
   dst.resize(pages.size());
-  for (std::size_t i = 0; i < pages.size(); ++i) dst[i] = Ref{static_cast<std::int8_t>(dest), pages[i]};
-  f.pages.assign(dst.begin(), dst.end());
+  f.pages.resize(pages.size());
+  {
+    Ref* const dp = dst.data();
+    Ref* const fp = f.pages.data();
+    const std::uint32_t* const pg = pages.data();
+    for (std::size_t i = 0; i < pages.size(); ++i) dp[i] = fp[i] = Ref{static_cast<std::int8_t>(dest), pg[i]};
+  }
   std::sort(waits.begin(), waits.end());
   waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
   void* lane_stream = issue(src, dst, *src_node, push, waits, srow ? srow->fill_ticket : 0);
@@ -882,7 +943,8 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
   {
     Row& r = row(tr.session, tr.layer);
     if (r.b.size() <= f.blocks.back()) r.b.resize(static_cast<std::size_t>(f.blocks.back()) + 1);  // ascending
-    for (std::uint32_t b : f.blocks) r.b[b].coming[t] = slot + 1;
+    Copies* const rb = r.b.data();
+    for (const std::uint32_t b : f.blocks) rb[b].coming[t] = slot + 1;
   }
   moved_[7] += f.blocks.size() * page_bytes_;  // bytes issued ahead of their apply
   flight_of_.emplace(tr.id, slot);
@@ -908,15 +970,19 @@ void NodePayload::transfer_retired(std::uint64_t id, bool voided) {
   // the file pools before the store installs these pages as valid.
   if (!voided) check_file_io();
   const auto rt = rows_.find(row_key(f.session, f.layer));
-  if (rt != rows_.end())
-    for (std::uint32_t b : f.blocks)
-      if (b < rt->second.b.size() && rt->second.b[b].coming[f.tier] == slot + 1) rt->second.b[b].coming[f.tier] = 0;
+  if (rt != rows_.end()) {
+    Copies* const rb = rt->second.b.data();
+    const std::size_t rn = rt->second.b.size();
+    const int ft = f.tier;
+    for (const std::uint32_t b : f.blocks)
+      if (b < rn && rb[b].coming[ft] == slot + 1) rb[b].coming[ft] = 0;
+  }
   if (voided) {
     for (const Ref& r : f.pages) release(r);
     kvx_event_destroy(f.event);
     const std::uint32_t s = f.session;
     const std::uint16_t l = f.layer;
-    f = InFlight{};
+    reset_flight(f);
     flight_of_.erase(it);
     free_flights_.push_back(slot);
     drop_row_if_empty(s, l);

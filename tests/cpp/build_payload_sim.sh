@@ -8,6 +8,7 @@
 #   oracle/_ref/payload_sim_ref  the reference KvStore (state oracle, CPU only)
 set -euo pipefail
 ROOT="$(cd "$(dirname "$0")/../.." && pwd)"
+mkdir -p "$ROOT/build"; exec 9>"$ROOT/build/.lock"; flock 9  # one build at a time (parallel test workers)
 REF="${REF:-/root/reference/proj}"
 OUT="$ROOT/oracle/_ref"
 OBJ="$ROOT/build/payload_sim"
@@ -16,7 +17,10 @@ CXX="${CXX:-g++}"
 CC_SYS="$(command -v /usr/bin/gcc || command -v gcc)"
 [ -f "$REF/src/kvstore.cpp" ] || { echo "reference not present at $REF" >&2; exit 3; }
 mkdir -p "$OUT" "$OBJ/overlay/symsim"
-for h in kvstore costmodel time; do cp "$ROOT/include/symsim/$h.hpp" "$OBJ/overlay/symsim/$h.hpp"; done
+for h in kvstore costmodel time; do  # unchanged headers stay put; changed ones are replaced atomically (parallel test workers)
+  d="$OBJ/overlay/symsim/$h.hpp"
+  cmp -s "$ROOT/include/symsim/$h.hpp" "$d" || { cp "$ROOT/include/symsim/$h.hpp" "$d.$$" && mv -f "$d.$$" "$d"; }
+done
 make -s -C "$ROOT/paper_2412_16434_b200/csrc" all
 
 CUDA_INC="${CUDA_HOME:-/usr/local/cuda}/include"

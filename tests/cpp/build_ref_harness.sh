@@ -18,6 +18,7 @@
 # usage: [B200_ENGINE=1] tests/cpp/build_ref_harness.sh [suite ...]   (default: all suites)
 set -euo pipefail
 ROOT="$(cd "$(dirname "$0")/../.." && pwd)"
+mkdir -p "$ROOT/build"; exec 9>"$ROOT/build/.lock"; flock 9  # one build at a time (parallel test workers)
 REF="${REF:-/root/reference/proj}"
 OUT="$ROOT/build/ref_harness"
 HDRS=(kvstore costmodel time)

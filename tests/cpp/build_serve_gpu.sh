@@ -6,6 +6,7 @@
 # GPU step executor (libsymsim_b200 + libkvx). Built here, shipped prebuilt.
 set -euo pipefail
 ROOT="$(cd "$(dirname "$0")/../.." && pwd)"
+mkdir -p "$ROOT/build"; exec 9>"$ROOT/build/.lock"; flock 9  # one build at a time (parallel test workers)
 REF="${REF:-/root/reference/proj}"
 OUT="$ROOT/oracle/_ref"
 OBJ="$ROOT/build/serve_gpu"
@@ -14,7 +15,10 @@ CXX="${CXX:-g++}"
 [ -f "$REF/src/kvstore.cpp" ] || { echo "reference not present at $REF" >&2; exit 3; }
 make -s -C "$ROOT/paper_2412_16434_b200/csrc" all
 mkdir -p "$OUT" "$OBJ/overlay/symsim"
-for h in kvstore costmodel time engine; do cp "$ROOT/include/symsim/$h.hpp" "$OBJ/overlay/symsim/$h.hpp"; done
+for h in kvstore costmodel time engine; do  # unchanged headers stay put; changed ones are replaced atomically (parallel test workers)
+  d="$OBJ/overlay/symsim/$h.hpp"
+  cmp -s "$ROOT/include/symsim/$h.hpp" "$d" || { cp "$ROOT/include/symsim/$h.hpp" "$d.$$" && mv -f "$d.$$" "$d"; }
+done
 CUDA_INC="${CUDA_HOME:-/usr/local/cuda}/include"
 P=(-std=c++20 -O2 -I"$OBJ/overlay" -I"$REF/include" -I"$ROOT/include" -I"$CUDA_INC" -I"$JSON_DIR")
 pids=()

@@ -5,6 +5,7 @@
 #   oracle/_ref/serve_sim_ref  the reference KvStore + cost model
 set -euo pipefail
 ROOT="$(cd "$(dirname "$0")/../.." && pwd)"
+mkdir -p "$ROOT/build"; exec 9>"$ROOT/build/.lock"; flock 9  # one build at a time (parallel test workers)
 REF="${REF:-/root/reference/proj}"
 OUT="$ROOT/oracle/_ref"
 OBJ="$ROOT/build/serve_sim"
@@ -12,7 +13,10 @@ JSON_DIR="${JSON_DIR:-$(python3 -c 'import os,sysconfig;print(os.path.join(sysco
 CXX="${CXX:-g++}"
 [ -f "$REF/src/kvstore.cpp" ] || { echo "reference not present at $REF" >&2; exit 3; }
 mkdir -p "$OUT" "$OBJ/overlay/symsim"
-for h in kvstore costmodel time engine; do cp "$ROOT/include/symsim/$h.hpp" "$OBJ/overlay/symsim/$h.hpp"; done
+for h in kvstore costmodel time engine; do  # unchanged headers stay put; changed ones are replaced atomically (parallel test workers)
+  d="$OBJ/overlay/symsim/$h.hpp"
+  cmp -s "$ROOT/include/symsim/$h.hpp" "$d" || { cp "$ROOT/include/symsim/$h.hpp" "$d.$$" && mv -f "$d.$$" "$d"; }
+done
 P=(-std=c++20 -O2 -I"$OBJ/overlay" -I"$REF/include" -I"$JSON_DIR")
 R=(-std=c++20 -O2 -I"$REF/include" -I"$JSON_DIR")
 pids=()

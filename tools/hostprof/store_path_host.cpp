@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -66,7 +67,7 @@ int main(int argc, char** argv) {
     po.seed = 0x70B;
     po.free_running = true;
     nodes.push_back(std::make_unique<NodePayload>(&cluster, n, po));
-    stores[n]->attach_backend(nodes[n].get());
+    if (!std::getenv("NOBACKEND")) stores[n]->attach_backend(nodes[n].get());
     for (int r = 0; r < reps; ++r) stores[n]->register_session(r, "s" + std::to_string(r), PriorityClass::Normal);
     stores[n]->finalize_sessions();
   }
@@ -95,5 +96,12 @@ int main(int argc, char** argv) {
     std::printf("%-22s %8.2f us/layer\n", k, us);
   }
   std::printf("%-22s %8.2f us/layer (host, no GPU)\n", "migration total", total);
+  static const char* kPhase[] = {"posted", "retired", "issue", "reclaim", "upload", "launch", "close", "alloc"};
+  for (int n = 0; n < 2; ++n) {
+    std::printf("node%d:", n);
+    for (int k = 0; k < NodePayload::kHostPhases; ++k)
+      std::printf(" %s %.1f", kPhase[k], nodes[n]->host_ns()[k] / 1e3 / reps / kLayers);
+    std::printf(" us/layer\n");
+  }
   return 0;
 }
