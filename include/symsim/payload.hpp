@@ -329,7 +329,7 @@ class NodePayload final : public TierBackend {
   std::uint64_t apply_wait_ns_ = 0;
   std::uint64_t posted_ = 0;
   std::uint64_t host_ns_[kHostPhases] = {};
-  std::vector<Ref> scratch_src_, scratch_dst_;  // transfer_posted scratch (reused)
+  std::vector<Ref> scratch_src_;  // transfer_posted scratch (reused)
   std::vector<void*> scratch_waits_;
   std::vector<std::uint32_t> scratch_pages_;
 };

@@ -873,11 +873,9 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
   // Per-posting scratch is kept across calls: fresh 16-100 KB buffers per
   // layer cost more in allocation and first-touch faults than the work.
   std::vector<Ref>& src = scratch_src_;
-  std::vector<Ref>& dst = scratch_dst_;
   std::vector<void*>& waits = scratch_waits_;
   std::vector<std::uint32_t>& pages = scratch_pages_;
   src.clear();
-  dst.clear();
   waits.clear();
   pages.clear();
   const Row* have = find_row(tr.session, tr.layer);
@@ -927,17 +925,15 @@ void NodePayload::transfer_posted(const TransferInfo& tr) {
   // Ascending pages only matter for copy-engine runs (host / disk pools);
   // the HBM movers take any permutation.
   if (dest == kHostPool || dest == kDiskPool) sort_pages(pages);
-  dst.resize(pages.size());
-  f.pages.resize(pages.size());
+  f.pages.resize(pages.size());  // the flight's pages are the move's destinations
   {
-    Ref* const dp = dst.data();
     Ref* const fp = f.pages.data();
     const std::uint32_t* const pg = pages.data();
-    for (std::size_t i = 0; i < pages.size(); ++i) dp[i] = fp[i] = Ref{static_cast<std::int8_t>(dest), pg[i]};
+    for (std::size_t i = 0; i < pages.size(); ++i) fp[i] = Ref{static_cast<std::int8_t>(dest), pg[i]};
   }
   std::sort(waits.begin(), waits.end());
   waits.erase(std::unique(waits.begin(), waits.end()), waits.end());
-  void* lane_stream = issue(src, dst, *src_node, push, waits, srow ? srow->fill_ticket : 0);
+  void* lane_stream = issue(src, f.pages, *src_node, push, waits, srow ? srow->fill_ticket : 0);
   kvx_check(kvx_event_create(&f.event), "event");
   kvx_check(kvx_event_record(f.event, lane_stream), "event record");
   {

@@ -12,6 +12,10 @@ append_blocks); then, as the reference's Simulation::start_migration does
   plan_layerwise_load(receiver)    kvstore.cpp:433-543  -> 80 LoadH2D (HBM->HBM)
   apply_transfer x 80
 
+A first full-size session (COLD) runs the same calls untimed-for-the-headline
+(its numbers are reported as cold_*), then the timed one: a serving node's
+steady state, with its host rows, flight slots and free lists already warm.
+
 Host time of each call is measured (perf_counter_ns around the ctypes call)
 and split into the store+payload bookkeeping and the time apply spent
 blocked on the GPU (NodePayload::apply_wait_ns); the per-layer host cost is
@@ -32,7 +36,7 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 LAYERS, BLOCKS, TOKENS = 80, 2048, 32768
-HEADS, DIM, SEED, SESSION, WARM = 8, 128, 0x70B, 9, 10
+HEADS, DIM, SEED, SESSION, WARM, COLD = 8, 128, 0x70B, 9, 10, 11
 
 
 def run(verify: bool = True, oracle_samples: int = 4):
@@ -56,6 +60,7 @@ def run(verify: bool = True, oracle_samples: int = 4):
         nd.attach(st)
         st.register_session(SESSION, "seventy-b")
         st.register_session(WARM, "warm-up")
+        st.register_session(COLD, "seventy-b-cold")
         st.finalize_sessions()
         stores.append(st)
         nodes.append(nd)
@@ -95,27 +100,47 @@ def run(verify: bool = True, oracle_samples: int = 4):
     dst.release_session(WARM, 40)
     for n in nodes:
         n.synchronize()
+
+    def migrate(sid, t0_ns):
+        """One full-size session through the store path; returns the migration's wall ms."""
+        _, sched = timed("append_blocks(32K)", lambda: src.append_blocks(sid, TOKENS, t0_ns))
+        apply_all(src, sched, "apply(created)")
+        nodes[0].synchronize()
+        timed("mark_migrating_out", lambda: src.mark_migrating_out(sid))
+        sched = timed("import_migration", lambda: dst.import_migration(sid, TOKENS, t0_ns + 1_000_000))
+        assert len(sched) == LAYERS, len(sched)
+        g0 = time.perf_counter_ns()
+        res = apply_all(dst, sched, "apply(net_arrive)")
+        assert sum(r.migration_complete for r in res) == 1
+        nodes[1].synchronize()
+        wall = (time.perf_counter_ns() - g0) / 1e6
+        timed("release_session", lambda: src.release_session(sid, t0_ns + 100_000_000))
+        assert sum(nodes[0].pages_in_use(p) for p in range(4)) == 0
+        plan, sched = timed("plan_layerwise_load",
+                            lambda: dst.plan_layerwise_load(sid, t0_ns + 200_000_000, 100_000, K.DEMAND))
+        assert plan.any_load and len(sched) == LAYERS
+        apply_all(dst, sched, "apply(load_h2d)")
+        nodes[1].synchronize()
+        assert dst.fully_device_resident(sid)
+        return wall
+
+    # Cold pass: the first full-size session pays first-use costs of the
+    # 2,048-block rows, flight slots and free lists (fresh host memory); the
+    # steady state a serving node runs in is the second session, timed below.
+    h_cold = [n.host_ns() for n in nodes]
+    migrate(COLD, 0)
+    cold = {k: round(v["host_ns"] / 1e3 / LAYERS, 3) for k, v in t.items()
+            if k in ("import_migration", "apply(net_arrive)", "plan_layerwise_load", "apply(load_h2d)")}
+    cold_phases = {f"node{i}": {k: round((v - h_cold[i][k]) / 1e3 / LAYERS, 3) for k, v in n.host_ns().items()}
+                   for i, n in enumerate(nodes)}
+    dst.release_session(COLD, 300_000_000)
+    for n in nodes:
+        n.synchronize()
+    t.clear()
+
     host0 = [n.host_ns() for n in nodes]
     moved0 = nodes[1].bytes_moved()
-
-    _, sched = timed("append_blocks(32K)", lambda: src.append_blocks(SESSION, TOKENS, 0))
-    apply_all(src, sched, "apply(created)")
-    nodes[0].synchronize()
-    timed("mark_migrating_out", lambda: src.mark_migrating_out(SESSION))
-    sched = timed("import_migration", lambda: dst.import_migration(SESSION, TOKENS, 1_000_000))
-    assert len(sched) == LAYERS, len(sched)
-    g0 = time.perf_counter_ns()
-    res = apply_all(dst, sched, "apply(net_arrive)")
-    assert sum(r.migration_complete for r in res) == 1
-    nodes[1].synchronize()
-    migrate_wall_ms = (time.perf_counter_ns() - g0) / 1e6
-    timed("release_session", lambda: src.release_session(SESSION, 100_000_000))
-    assert sum(nodes[0].pages_in_use(p) for p in range(4)) == 0
-    plan, sched = timed("plan_layerwise_load", lambda: dst.plan_layerwise_load(SESSION, 200_000_000, 100_000, K.DEMAND))
-    assert plan.any_load and len(sched) == LAYERS
-    apply_all(dst, sched, "apply(load_h2d)")
-    nodes[1].synchronize()
-    assert dst.fully_device_resident(SESSION)
+    migrate_wall_ms = migrate(SESSION, 1_000_000_000)
     moved = nodes[1].bytes_moved()
     assert moved["net_arrive"] - moved0["net_arrive"] == pages * pb
     assert moved["load_h2d"] - moved0["load_h2d"] == pages * pb
@@ -135,6 +160,10 @@ def run(verify: bool = True, oracle_samples: int = 4):
                       "gpu_wait_ms": round(v["gpu_wait_ns"] / 1e6, 3)} for k, v in t.items()},
         "migrate_wall_ms": round(migrate_wall_ms, 3),
         "payload_host_us_per_layer_by_phase": out_host,
+        "cold_host_us_per_layer": cold,
+        "cold_host_us_per_layer_migration_total": round(sum(cold.values()), 3),
+        "cold_payload_host_us_per_layer_by_phase": cold_phases,
+        "timed_pass": "second full-size session (steady state); cold_* = the first one",
         "note": "host_ns excludes time apply spent blocked on GPU events (NodePayload::apply_wait_ns); "
                 "includes ctypes call overhead (~1-3 us per call)",
     }
