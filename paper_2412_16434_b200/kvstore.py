@@ -187,7 +187,7 @@ class LoadPlan:
     any_load: bool
 
 
-@dataclass
+@dataclass(slots=True)
 class ApplyResult:
     session: int
     layer: int
@@ -319,6 +319,12 @@ class KvStore:
         _check(self._lib, self._lib.kvs_create(C.byref(g), C.byref(self.links._c()), C.byref(self.opts._c()),
                                                C.byref(handle)))
         self._h = handle
+        # Hot per-transfer call: bound once, result struct reused (ctypes
+        # attribute lookup + struct allocation per apply cost more host time
+        # than the store's own bookkeeping).
+        self._apply_fn = self._lib.kvs_apply_transfer
+        self._apply_buf = _Apply()
+        self._apply_ref = C.byref(self._apply_buf)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -333,7 +339,14 @@ class KvStore:
     def _scheduled(self) -> List[Tuple[int, int]]:
         p = C.POINTER(_Sched)()
         n = self._lib.kvs_out_scheduled(self._h, C.byref(p))
-        return [(p[i].id, p[i].complete_at) for i in range(n)]
+        if n <= 0:
+            return []
+        # One bulk read of the (id u64, complete_at i64) pairs instead of a
+        # struct object per element.
+        addr = C.addressof(p.contents)
+        ids = (C.c_uint64 * (2 * n)).from_address(addr)[0::2]
+        at = (C.c_int64 * (2 * n)).from_address(addr)[1::2]
+        return list(zip(ids, at))
 
     # ---- registry ----
     def register_session(self, session: int, sid: str, high_priority: bool = False) -> None:
@@ -475,8 +488,10 @@ class KvStore:
         return self._scheduled()
 
     def apply_transfer(self, tid: int, now: int) -> ApplyResult:
-        r = _Apply()
-        self._call("kvs_apply_transfer", tid, now, C.byref(r))
+        r = self._apply_buf
+        rc = self._apply_fn(self._h, tid, now, self._apply_ref)
+        if rc:
+            _check(self._lib, rc)
         return ApplyResult(r.session, r.layer, bool(r.device_layer_ready), bool(r.persists_drained),
                            bool(r.migration_arrived), bool(r.migration_complete), bool(r.voided))
 
